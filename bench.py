@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""Headline benchmark: SCAN end-to-end on R-MAT scale-24 (eps=0.5, mu=5).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full clustering call of the hot path (device CSR build with
+degree-rank relabel + identify + cluster + classify) over the synthetic
+R-MAT s24 edge list (BASELINE.json configs[1], the in-HBM config the metric is
+quoted on).  Inputs exceed L2 (2.1 GB edge list vs 126 MB), so no flush is
+needed between steps.
+
+  value   edges/s = m / device time per step, edge list resident in HBM,
+          results left in HBM (CUDA events on the engine stream)
+  e2e     same metric through the C-ABI with HOST buffers: pinned edge list
+          H2D + build + scan + roles/cluster ids D2H inside the timed region
+  roofline  similarity pass (identify) algorithmic bytes W_sim
+          / its measured time vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference hot loop (_eval_edge, scan.py:203-233, C port in
+          oracle/) on a bounded uniform edge sample, all host threads
+--impl reference times that CPU port alone (rank 0), same metric and config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SCAN end-to-end sec & edges/sec (R-MAT s24 ε=0.5 μ=5); HBM GB/s vs peak, 1-8 GPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edgefactor", type=int, default=16)
+    ap.add_argument("--eps", default="0.5")
+    ap.add_argument("--mu", type=int, default=5)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5
+                ).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_sample(csr, eps, seconds, threads, rng_seed=0):
+    """Reference hot loop on uniformly sampled edges for ~`seconds`."""
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    rng = np.random.default_rng(rng_seed)
+    probe = rng.integers(0, 2 * csr.m, 2000)
+    t, _, _ = orc.sample_eval_slots(csr, eps, probe, threads)
+    rate = len(probe) / max(t, 1e-6)
+    count = int(max(2000, min(rate * seconds, 50_000_000)))
+    slots = rng.integers(0, 2 * csr.m, count)
+    secs, probes, similar = orc.sample_eval_slots(csr, eps, slots, threads)
+    return count, secs, probes, similar
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as orc
+
+    threads = orc.max_threads()
+    t0 = time.time()
+    n, edges = orc.rmat(args.scale, seed=args.seed, edgefactor=args.edgefactor)
+    csr = orc.PlainCSR(n, edges)
+    prep = time.time() - t0
+    m = csr.m
+    per_step = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    vals = []
+    tot_edges = 0
+    tot_secs = 0.0
+    for i in range(args.warmup + args.steps):
+        cnt, secs, probes, _ = cpu_sample(csr, args.eps, per_step, threads, rng_seed=i)
+        if i >= args.warmup:
+            vals.append(cnt / secs)
+            tot_edges += cnt
+            tot_secs += secs
+    value = tot_edges / tot_secs
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "edges/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * m / value,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int32",
+        "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05), generated on the host",
+        "config": {"workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
+                   f"eps={args.eps} mu={args.mu}", "n": n, "m": m,
+                   "parallelism": f"{threads} host threads"},
+        "cpu_baseline": {
+            "value": value, "unit": "edges/s", "cores": threads, "kind": "port",
+            "sample": f"{tot_edges} uniformly sampled edges per {args.steps} steps; reference "
+                      f"_eval_edge (scan.py:203-233) binary-search probing, C port in oracle/; "
+                      f"ms_per_step extrapolates the full m={m} edges",
+        },
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "prep_s": round(prep, 1),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2311_12281_b200 as gs
+    from paper_2311_12281_b200 import _lib
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    f = gs.epsilon_fraction(args.eps)
+    eps2 = _lib.eps2_struct(f)
+
+    # ---- synthetic input, generated and normalised on the device (not timed)
+    n = 1 << args.scale
+    cnt = args.edgefactor << args.scale
+    src = torch.empty(cnt, dtype=torch.int32, device="cuda")
+    dst = torch.empty(cnt, dtype=torch.int32, device="cuda")
+    _lib.check(lib.gs_rmat_generate(args.scale, args.edgefactor, args.seed, src.data_ptr(),
+                                    dst.data_ptr(), None))
+    torch.cuda.synchronize()
+    uv = torch.empty(2 * cnt, dtype=torch.int32, device="cuda")
+    mm = ctypes.c_int64(0)
+    _lib.check(lib.gs_normalize_edges(cnt, src.data_ptr(), dst.data_ptr(), uv.data_ptr(),
+                                      ctypes.byref(mm), None))
+    del src, dst
+    m = int(mm.value)
+    uv = uv[: 2 * m].clone()
+    torch.cuda.empty_cache()
+
+    eng = _lib.Engine(device=local)
+    stream = torch.cuda.ExternalStream(eng.stream())
+    role_d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    clus_d = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = _lib.GsStats()
+
+    def step_device():
+        _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv.data_ptr(), 1))
+        _lib.check(lib.gs_engine_scan(eng.handle, args.mu, ctypes.byref(eps2), role_d.data_ptr(),
+                                      clus_d.data_ptr(), 1, ctypes.byref(st)))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step_device()
+    sim_ms, ident_ms, launches, phase = [], [], 0, {}
+    barrier()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+            ident_ms.append(st.phase_ms[_lib.GS_PH_IDENTIFY])
+            launches += int(st.kernel_launches)
+        e1.record(stream)
+        barrier()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    stats = gs.scan.stats_from_native(st, n, m, 1)
+    value = world * m / (ms_step / 1000.0)
+    for k in range(_lib.GS_PH_COUNT):
+        phase[k] = round(st.phase_ms[k], 3)
+
+    # ---- roofline of the dominant kernel (similarity pass of identify)
+    peak, peak_src = peaks()
+    w_sim = stats.extra["hbm_bytes_alg"]
+    t_sim = statistics.median(ident_ms) / 1000.0
+    achieved = w_sim / t_sim / 1e9 if t_sim > 0 else 0.0
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "sim_traffic.json")
+    if os.path.exists(tf):
+        with open(tf) as fh:
+            td = json.load(fh)
+        if td.get("config") == f"s{args.scale} eps={args.eps} mu={args.mu}":
+            traffic = td.get("dram_bytes_per_step")
+
+    # ---- e2e through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        uv_h = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
+        uv_h.copy_(uv)
+        role_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        clus_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        st2 = _lib.GsStats()
+
+        def step_host():
+            _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv_h.data_ptr(), 0))
+            _lib.check(lib.gs_engine_scan(eng.handle, args.mu, ctypes.byref(eps2),
+                                          role_h.data_ptr(), clus_h.data_ptr(), 0,
+                                          ctypes.byref(st2)))
+
+        for _ in range(max(1, args.warmup)):
+            step_host()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_host()
+        e1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        # parity of the two paths on the same input
+        assert torch.equal(role_h, role_d.cpu()) and torch.equal(clus_h, clus_d.cpu())
+        e2e = {"value": world * m / (ms_e2e / 1000.0), "unit": "edges/s",
+               "ms_per_step": ms_e2e, "h2d_bytes_per_step": 8 * m,
+               "d2h_bytes_per_step": 5 * n}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+
+        edges = uv.view(-1, 2).cpu().numpy()
+        csr = orc.PlainCSR(n, edges)
+        threads = orc.max_threads()
+        count, secs, probes, _ = cpu_sample(csr, args.eps, args.cpu_seconds, threads)
+        cpu = {"value": count / secs, "unit": "edges/s", "cores": threads, "kind": "port",
+               "sample": f"{count} uniformly sampled edges of the same s{args.scale} graph, "
+                         f"reference _eval_edge (scan.py:203-233) C port, {secs:.1f}s; "
+                         f"{probes / max(count, 1):.0f} probes/edge"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "edges/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "int32",
+            "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05, scrambled ids), "
+                    "generated + normalised on the device",
+            "config": {
+                "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
+                            f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
+                "n": n, "m": m, "seed": args.seed,
+                "parallelism": "replicas" if world > 1 else "single",
+                "l2": "inputs larger than L2 (edge list 8m bytes), no flush",
+                "step": "device CSR build (degree-rank relabel) + identify + cluster + classify",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "similarity pass (identify phase: k_sim_hash*/k_sim_tiny)",
+                         "alg_bytes_per_step": w_sim, "t_ms": t_sim * 1000, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "phases_ms": {"h2d": phase[0], "build": phase[1], "identify": phase[2],
+                          "cleanup": phase[3], "cluster": phase[4], "classify": phase[5],
+                          "d2h": phase[6], "scan_total": phase[7]},
+            "counts": {"sim_evals": stats.sim_evals, "sim_evals_avoided": m - stats.sim_evals,
+                       "decided_by_bound": stats.extra["sim_decided_by_bound"],
+                       "intersections": stats.extra["sim_intersections"],
+                       "adj_probes": stats.adj_probes, "cores": int(st.n_core),
+                       "members": int(st.n_member), "hubs": int(st.n_hub),
+                       "outliers": int(st.n_outlier), "clusters": int(st.n_clusters)},
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

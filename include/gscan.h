@@ -1,0 +1,168 @@
+/*
+ * gscan.h -- C-ABI of libgscan.so, the B200 (sm_100a) structural-clustering
+ * engine that replaces the reference's clustering call.
+ *
+ * The reference (graphscan, pure Python) has no FFI; its drop-in boundary is
+ * the pair of Python entry points below.  Each C entry point states which
+ * reference interface it replaces; INTEGRATION.md shows the ctypes binding
+ * the reference would add.  The Python host package
+ * paper_2311_12281_b200 binds exactly these symbols.
+ *
+ *   gs_scan_csr        scan_in_memory(g, mu, epsilon, workers)   scan.py:965-982
+ *   gs_scan_edges      build_graph(el) + scan_in_memory(...)     graph.py:162-259, scan.py:965
+ *   gs_build_graph     build_graph(el)                           graph.py:162-259
+ *   gs_scan_partitioned scan_out_of_core(meta, plan, mu, eps)    partition.py:666-757
+ *   gs_check_sim       check_sim over a batch of edges           scan.py:241-258
+ *   gs_engine_*        a reusable device context (stream, memory pool,
+ *                      resident graph) behind the one-shot calls
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Host pointers unless a flag says device.
+ *   - Return 0 (GS_OK) or a GS_E* code; gs_last_error() gives the message of
+ *     the calling thread's last failure.  No C++ exception crosses the ABI.
+ *   - Error mapping used by the Python host (same taxonomy as the reference):
+ *       GS_EINVAL -> ValueError       (scan.py:969-973, graph.py:181-195)
+ *       GS_EBUDGET -> InfeasibleBudgetError(ValueError)  (partition.py:79-89)
+ *       GS_ENOMEM -> MemoryError, GS_ECUDA/GS_EINTERNAL -> RuntimeError
+ *   - The caller owns every buffer it passes; the library owns device memory
+ *     and releases per-call temporaries before returning.  Engines are not
+ *     shared between threads; one-shot calls are reentrant (no global
+ *     mutable state besides the thread-local error string).
+ *   - Epsilon enters as its exact square p/q (scan.py:155-158), each as two
+ *     64-bit halves; the device threshold test is the integer predicate
+ *     (c+2)^2 * q >= p * (da+1)(db+1) (scan.py:232-233) in 192-bit arithmetic.
+ *
+ * Role codes written to role_out (the reference's byte codes, scan.py:43-52):
+ *   1 core, 3 member, 5 hub, 6 outlier.
+ * cluster_out: canonical cluster id = minimum core vertex id of the cluster
+ *   (for members: the minimum eligible cluster), -1 for hubs and outliers.
+ */
+#ifndef GSCAN_H
+#define GSCAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ABI_VERSION 1
+
+#define GS_OK 0
+#define GS_EINVAL 1
+#define GS_EBUDGET 2
+#define GS_ECUDA 3
+#define GS_ENOMEM 4
+#define GS_EINTERNAL 5
+
+#define GS_ROLE_CORE 1
+#define GS_ROLE_MEMBER 3
+#define GS_ROLE_HUB 5
+#define GS_ROLE_OUTLIER 6
+
+/* epsilon^2 = p / q exactly; both < 2^128. */
+typedef struct gs_eps2 {
+  uint64_t p_lo, p_hi, q_lo, q_hi;
+} gs_eps2;
+
+/* Phase timings in milliseconds (CUDA events on the engine stream). */
+enum {
+  GS_PH_H2D = 0,      /* host -> device copy of the graph */
+  GS_PH_BUILD = 1,    /* degree-rank relabel + CSR build on the device */
+  GS_PH_IDENTIFY = 2, /* phase 1 similarity sweep (identify_core) */
+  GS_PH_CLEANUP = 3,  /* role resolution (+ rare re-evaluation) */
+  GS_PH_CLUSTER = 4,  /* phase 2: union-find, flatten, labels, attach */
+  GS_PH_CLASSIFY = 5, /* phase 3: hub / outlier */
+  GS_PH_D2H = 6,      /* result copy back */
+  GS_PH_TOTAL = 7,
+  GS_PH_SIM_KERNELS = 8, /* summed duration of the similarity kernels */
+  GS_PH_COUNT = 16
+};
+
+/* StatsReport counters (scan.py:911-947) plus engine extras. */
+typedef struct gs_stats {
+  int64_t n, m;
+  int64_t sim_evals;              /* edges whose similarity was decided */
+  int64_t adj_probes;             /* adjacency elements probed */
+  int64_t union_retries;          /* failed CAS hooks in union-find */
+  int64_t probe_bound_violations; /* always 0: probes <= min degree */
+  int64_t sim_decided_by_bound;   /* decided by the O(1) degree bounds */
+  int64_t sim_intersections;      /* edges that ran a set intersection */
+  int64_t alg_bytes_sim;          /* SURVEY 8(d) W_sim of the similarity pass */
+  int64_t n_core, n_member, n_hub, n_outlier, n_clusters;
+  int64_t partitions;             /* out-of-core / sharded passes */
+  int64_t kernel_launches;        /* kernels launched by this call */
+  int64_t peak_device_bytes;      /* high-water mark of engine allocations */
+  double phase_ms[GS_PH_COUNT];
+} gs_stats;
+
+typedef struct gs_engine gs_engine;
+
+/* device < 0 selects the current device.  hbm_cap_bytes = 0: no cap.  With
+ * a cap, every device allocation of the engine is counted against it and a
+ * call that cannot fit returns GS_EBUDGET (the partitioned path is chosen
+ * automatically by gs_scan_partitioned). */
+int gs_engine_create(int device, uint64_t hbm_cap_bytes, gs_engine** out);
+void gs_engine_destroy(gs_engine* e);
+/* cudaStream_t the engine launches on (for callers timing with events). */
+void* gs_engine_stream(gs_engine* e);
+
+/* Load a graph into the engine.  `on_device` = 1 means the pointers are
+ * device pointers (e.g. torch CUDA tensors); 0 means host memory (pinned or
+ * pageable).  The CSR form is the reference Graph layout (vertex_offsets i64
+ * [n+1], adjacency i32 [2m], sorted runs); the edge form is a normalised
+ * EdgeList (pairs u<v, unique, interleaved i32 [2m]). */
+int gs_engine_load_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* offsets,
+                       const int32_t* adjacency, int on_device);
+int gs_engine_load_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_uv,
+                         int on_device);
+
+/* Run the three phases on the loaded graph.  Outputs are written to host
+ * buffers (out_on_device = 0) or device buffers (1), indexed by the caller's
+ * vertex ids.  role_out / cluster_out may be NULL to skip the copy. */
+int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_out,
+                   int32_t* cluster_out, int out_on_device, gs_stats* stats);
+
+/* One-shot calls (temporary engine on the current device). */
+int gs_scan_csr(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
+                int32_t mu, const gs_eps2* eps2, uint8_t* role_out,
+                int32_t* cluster_out, gs_stats* stats);
+int gs_scan_edges(int64_t n, int64_t m, const int32_t* edges_uv, int32_t mu,
+                  const gs_eps2* eps2, uint8_t* role_out, int32_t* cluster_out,
+                  gs_stats* stats);
+
+/* build_graph on the device, reference layout, host in / host out. */
+int gs_build_graph(int64_t n, int64_t m, const int32_t* edges_uv, int64_t* offsets,
+                   int32_t* adjacency, int32_t* edge_ids, int32_t* edge_list);
+
+/* check_sim for k edges (u_i, v_i) of the loaded graph: out[i] = 1 similar,
+ * 0 dissimilar, -1 not an edge. */
+int gs_engine_check_sim(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,
+                        const gs_eps2* eps2, int8_t* out);
+
+/* Partitioned (out-of-core) scan: the graph stays in HOST memory (the CSR
+ * arrays, ideally pinned); only per-vertex state plus one streamed partition
+ * of adjacency live in HBM, under hbm_cap_bytes.  Returns GS_EBUDGET if the
+ * resident state alone cannot fit. */
+int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets,
+                        const int32_t* adjacency, int32_t mu, const gs_eps2* eps2,
+                        uint64_t hbm_cap_bytes, uint8_t* role_out, int32_t* cluster_out,
+                        gs_stats* stats);
+
+/* Deterministic R-MAT workload generator (bench/test input; same stream as
+ * the CPU generator in oracle/): raw samples, device pointers. */
+int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,
+                     int32_t* dst_dev, void* stream);
+/* Normalise raw device samples in place (drop loops, orient, sort, dedupe);
+ * writes the unique count to *m_out and interleaved pairs to edges_dev. */
+int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev,
+                       int32_t* edges_dev, int64_t* m_out, void* stream);
+
+const char* gs_last_error(void);
+int gs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

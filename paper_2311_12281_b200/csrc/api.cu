@@ -1,0 +1,381 @@
+// api.cu -- the C-ABI of libgscan.so (include/gscan.h) and the engine
+// context.  No C++ exception crosses this boundary; every entry point
+// returns a GS_* code and leaves a message in gs_last_error().
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "engine.cuh"
+
+namespace gs {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+std::string cuda_msg(cudaError_t e, const char* what, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "CUDA error %s (%s) in %s at %s:%d", cudaGetErrorName(e),
+           cudaGetErrorString(e), what, file, line);
+  return buf;
+}
+int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv_dev,
+                           int64_t* off_dev, int32_t* adj_dev, int32_t* eids_dev,
+                           int32_t* elist_dev);
+int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t* dst,
+                  cudaStream_t st);
+int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32_t* dst,
+                    int32_t* uv, int64_t* m_out);
+int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
+                     const int32_t* adj, int32_t mu, const Eps2& eps, uint8_t* role_out,
+                     int32_t* cluster_out, gs_stats* st);
+int check_sim_batch(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,
+                    const Eps2& eps, int8_t* out);
+
+static Eps2 to_eps(const gs_eps2* p) {
+  Eps2 e;
+  e.p_lo = p->p_lo;
+  e.p_hi = p->p_hi;
+  e.q_lo = p->q_lo;
+  e.q_hi = p->q_hi;
+  const double two64 = 18446744073709551616.0;
+  const double pd = (double)p->p_hi * two64 + (double)p->p_lo;
+  const double qd = (double)p->q_hi * two64 + (double)p->q_lo;
+  e.ratio = pd / qd;
+  return e;
+}
+
+static int check_eps(const gs_eps2* p) {
+  if (!p) { set_error("epsilon is NULL"); return GS_EINVAL; }
+  if ((p->q_lo | p->q_hi) == 0) { set_error("epsilon^2 denominator is 0"); return GS_EINVAL; }
+  if ((p->p_lo | p->p_hi) == 0) { set_error("epsilon must be in (0, 1]"); return GS_EINVAL; }
+  if (p->p_hi > p->q_hi || (p->p_hi == p->q_hi && p->p_lo > p->q_lo)) {
+    set_error("epsilon must be in (0, 1]");
+    return GS_EINVAL;
+  }
+  return GS_OK;
+}
+}  // namespace gs
+
+using namespace gs;
+
+int gs_engine::alloc(void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 1;
+  bytes = (bytes + 255) & ~size_t(255);
+  if (cap && live + bytes > cap) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "device allocation of %zu bytes exceeds the HBM cap (%llu live of %llu)", bytes,
+             (unsigned long long)live, (unsigned long long)cap);
+    set_error(buf);
+    return GS_EBUDGET;
+  }
+  cudaError_t err = cudaMallocAsync(p, bytes, stream);
+  if (err != cudaSuccess) {
+    set_error(cuda_msg(err, "cudaMallocAsync", __FILE__, __LINE__));
+    *p = nullptr;
+    return err == cudaErrorMemoryAllocation ? GS_ENOMEM : GS_ECUDA;
+  }
+  sizes[*p] = bytes;
+  live += bytes;
+  if (live > peak) peak = live;
+  return GS_OK;
+}
+
+void gs_engine::release(void* p) {
+  if (!p) return;
+  auto it = sizes.find(p);
+  if (it != sizes.end()) {
+    live -= it->second;
+    sizes.erase(it);
+  }
+  cudaFreeAsync(p, stream);
+}
+
+void gs_engine::free_graph() {
+  release(g.off);
+  release(g.adj);
+  release(g.orig);
+  release(g.rank);
+  release(g.eoff);
+  release(g.elo);
+  release(g.ehi);
+  g = DevGraph();
+}
+
+void gs_engine::free_state() {
+  release(s.sim);
+  release(s.bounds);
+  release(s.role);
+  release(s.parent);
+  release(s.label);
+  release(s.lmin);
+  release(s.lmax);
+  release(s.ctr);
+  release(s.wq);
+  s = DevState();
+}
+
+extern "C" {
+
+int gs_version(void) { return GS_ABI_VERSION; }
+const char* gs_last_error(void) { return g_err.c_str(); }
+
+int gs_engine_create(int device, uint64_t hbm_cap_bytes, gs_engine** out) {
+  if (!out) { set_error("out is NULL"); return GS_EINVAL; }
+  *out = nullptr;
+  int dev = device;
+  if (dev < 0) GS_CUDA(cudaGetDevice(&dev));
+  GS_CUDA(cudaSetDevice(dev));
+  gs_engine* e = new gs_engine();
+  e->device = dev;
+  e->cap = hbm_cap_bytes;
+  cudaError_t err = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking);
+  if (err != cudaSuccess) {
+    delete e;
+    set_error(cuda_msg(err, "cudaStreamCreate", __FILE__, __LINE__));
+    return GS_ECUDA;
+  }
+  cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;  // keep freed blocks for the next call
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = e;
+  return GS_OK;
+}
+
+void gs_engine_destroy(gs_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  e->free_state();
+  e->free_graph();
+  for (auto& kv : e->sizes) cudaFreeAsync(kv.first, e->stream);
+  cudaStreamSynchronize(e->stream);
+  cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+void* gs_engine_stream(gs_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+static int load_common(gs_engine* e, int64_t n, int64_t m) {
+  if (!e) { set_error("engine is NULL"); return GS_EINVAL; }
+  if (n < 0 || m < 0) { set_error("negative n or m"); return GS_EINVAL; }
+  if (n > 0x7fffffffLL) { set_error("vertex count exceeds the 4-byte id range"); return GS_EINVAL; }
+  GS_CUDA(cudaSetDevice(e->device));
+  e->launches = 0;
+  return GS_OK;
+}
+
+int gs_engine_load_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* offsets,
+                       const int32_t* adjacency, int on_device) {
+  GS_TRY(load_common(e, n, m));
+  cudaEvent_t t0, t1, t2;
+  cudaEventCreate(&t0); cudaEventCreate(&t1); cudaEventCreate(&t2);
+  cudaEventRecord(t0, e->stream);
+  const int64_t* off = offsets;
+  const int32_t* adj = adjacency;
+  int64_t* d_off = nullptr;
+  int32_t* d_adj = nullptr;
+  if (!on_device) {
+    GS_TRY(e->alloc_n(&d_off, n + 1));
+    GS_TRY(e->alloc_n(&d_adj, 2 * m));
+    GS_CUDA(cudaMemcpyAsync(d_off, offsets, sizeof(int64_t) * (size_t)(n + 1),
+                            cudaMemcpyHostToDevice, e->stream));
+    if (m > 0)
+      GS_CUDA(cudaMemcpyAsync(d_adj, adjacency, sizeof(int32_t) * (size_t)(2 * m),
+                              cudaMemcpyHostToDevice, e->stream));
+    off = d_off;
+    adj = d_adj;
+  }
+  int64_t h_ends[2] = {0, 0};
+  GS_CUDA(cudaMemcpyAsync(&h_ends[0], off, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaMemcpyAsync(&h_ends[1], off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
+  cudaEventRecord(t1, e->stream);
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  if (h_ends[0] != 0 || h_ends[1] != 2 * m) {
+    e->release(d_off);
+    e->release(d_adj);
+    set_error("invalid graph: vertex_offsets must start at 0 and end at 2m");
+    return GS_EINVAL;
+  }
+  int rc = build_from_csr(e, n, m, off, adj);
+  cudaEventRecord(t2, e->stream);
+  cudaStreamSynchronize(e->stream);
+  e->release(d_off);
+  e->release(d_adj);
+  cudaEventElapsedTime(&e->last_h2d_ms, t0, t1);
+  cudaEventElapsedTime(&e->last_build_ms, t1, t2);
+  cudaEventDestroy(t0); cudaEventDestroy(t1); cudaEventDestroy(t2);
+  return rc;
+}
+
+int gs_engine_load_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_uv,
+                         int on_device) {
+  GS_TRY(load_common(e, n, m));
+  cudaEvent_t t0, t1, t2;
+  cudaEventCreate(&t0); cudaEventCreate(&t1); cudaEventCreate(&t2);
+  cudaEventRecord(t0, e->stream);
+  const int32_t* uv = edges_uv;
+  int32_t* d_uv = nullptr;
+  if (!on_device && m > 0) {
+    GS_TRY(e->alloc_n(&d_uv, 2 * m));
+    GS_CUDA(cudaMemcpyAsync(d_uv, edges_uv, sizeof(int32_t) * (size_t)(2 * m),
+                            cudaMemcpyHostToDevice, e->stream));
+    uv = d_uv;
+  }
+  cudaEventRecord(t1, e->stream);
+  int rc = build_from_edges(e, n, m, uv);
+  cudaEventRecord(t2, e->stream);
+  cudaStreamSynchronize(e->stream);
+  e->release(d_uv);
+  cudaEventElapsedTime(&e->last_h2d_ms, t0, t1);
+  cudaEventElapsedTime(&e->last_build_ms, t1, t2);
+  cudaEventDestroy(t0); cudaEventDestroy(t1); cudaEventDestroy(t2);
+  return rc;
+}
+
+int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_out,
+                   int32_t* cluster_out, int out_on_device, gs_stats* stats) {
+  if (!e) { set_error("engine is NULL"); return GS_EINVAL; }
+  if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  GS_CUDA(cudaSetDevice(e->device));
+  if (stats) memset(stats, 0, sizeof(*stats));
+  const int64_t launches0 = e->launches;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0); cudaEventCreate(&t1);
+  cudaEventRecord(t0, e->stream);
+  int rc = run_scan(e, mu, to_eps(eps2), role_out, cluster_out, out_on_device, stats);
+  cudaEventRecord(t1, e->stream);
+  cudaStreamSynchronize(e->stream);
+  if (stats) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t0, t1);
+    stats->phase_ms[GS_PH_TOTAL] = ms;
+    stats->phase_ms[GS_PH_H2D] = e->last_h2d_ms;
+    stats->phase_ms[GS_PH_BUILD] = e->last_build_ms;
+    stats->kernel_launches = e->launches - launches0;
+    stats->peak_device_bytes = (int64_t)e->peak;
+  }
+  cudaEventDestroy(t0); cudaEventDestroy(t1);
+  return rc;
+}
+
+int gs_scan_csr(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
+                int32_t mu, const gs_eps2* eps2, uint8_t* role_out, int32_t* cluster_out,
+                gs_stats* stats) {
+  if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  int rc = gs_engine_load_csr(e, n, m, offsets, adjacency, 0);
+  int64_t build_launches = e->launches;
+  if (rc == GS_OK) rc = gs_engine_scan(e, mu, eps2, role_out, cluster_out, 0, stats);
+  if (rc == GS_OK && stats) {
+    stats->kernel_launches += build_launches;
+    stats->phase_ms[GS_PH_TOTAL] += stats->phase_ms[GS_PH_H2D] + stats->phase_ms[GS_PH_BUILD];
+  }
+  gs_engine_destroy(e);
+  return rc;
+}
+
+int gs_scan_edges(int64_t n, int64_t m, const int32_t* edges_uv, int32_t mu,
+                  const gs_eps2* eps2, uint8_t* role_out, int32_t* cluster_out,
+                  gs_stats* stats) {
+  if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  int rc = gs_engine_load_edges(e, n, m, edges_uv, 0);
+  int64_t build_launches = e->launches;
+  if (rc == GS_OK) rc = gs_engine_scan(e, mu, eps2, role_out, cluster_out, 0, stats);
+  if (rc == GS_OK && stats) {
+    stats->kernel_launches += build_launches;
+    stats->phase_ms[GS_PH_TOTAL] += stats->phase_ms[GS_PH_H2D] + stats->phase_ms[GS_PH_BUILD];
+  }
+  gs_engine_destroy(e);
+  return rc;
+}
+
+int gs_build_graph(int64_t n, int64_t m, const int32_t* edges_uv, int64_t* offsets,
+                   int32_t* adjacency, int32_t* edge_ids, int32_t* edge_list) {
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  int rc = load_common(e, n, m);
+  int32_t *d_uv = nullptr, *d_adj = nullptr, *d_eids = nullptr, *d_el = nullptr;
+  int64_t* d_off = nullptr;
+  if (rc == GS_OK) rc = e->alloc_n(&d_uv, 2 * m);
+  if (rc == GS_OK) rc = e->alloc_n(&d_off, n + 1);
+  if (rc == GS_OK) rc = e->alloc_n(&d_adj, 2 * m);
+  if (rc == GS_OK) rc = e->alloc_n(&d_eids, 2 * m);
+  if (rc == GS_OK) rc = e->alloc_n(&d_el, 2 * m);
+  if (rc == GS_OK && m > 0 &&
+      cudaMemcpyAsync(d_uv, edges_uv, 8 * (size_t)m, cudaMemcpyHostToDevice, e->stream) !=
+          cudaSuccess) {
+    set_error("host to device copy failed");
+    rc = GS_ECUDA;
+  }
+  if (rc == GS_OK) rc = build_reference_layout(e, n, m, d_uv, d_off, d_adj, d_eids, d_el);
+  if (rc == GS_OK) {
+    cudaMemcpyAsync(offsets, d_off, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost, e->stream);
+    if (m > 0) {
+      cudaMemcpyAsync(adjacency, d_adj, 8 * (size_t)m, cudaMemcpyDeviceToHost, e->stream);
+      cudaMemcpyAsync(edge_ids, d_eids, 8 * (size_t)m, cudaMemcpyDeviceToHost, e->stream);
+      cudaMemcpyAsync(edge_list, d_el, 8 * (size_t)m, cudaMemcpyDeviceToHost, e->stream);
+    }
+    cudaError_t err = cudaStreamSynchronize(e->stream);
+    if (err != cudaSuccess) {
+      set_error(cuda_msg(err, "gs_build_graph copy-back", __FILE__, __LINE__));
+      rc = GS_ECUDA;
+    }
+  }
+  gs_engine_destroy(e);
+  return rc;
+}
+
+int gs_engine_check_sim(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,
+                        const gs_eps2* eps2, int8_t* out) {
+  if (!e) { set_error("engine is NULL"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  GS_CUDA(cudaSetDevice(e->device));
+  return check_sim_batch(e, k, u, v, to_eps(eps2), out);
+}
+
+int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
+                        int32_t mu, const gs_eps2* eps2, uint64_t hbm_cap_bytes,
+                        uint8_t* role_out, int32_t* cluster_out, gs_stats* stats) {
+  if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, hbm_cap_bytes, &e));
+  int rc = load_common(e, n, m);
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (rc == GS_OK)
+    rc = scan_partitioned(e, n, m, offsets, adjacency, mu, to_eps(eps2), role_out, cluster_out,
+                          stats);
+  if (stats) stats->peak_device_bytes = (int64_t)e->peak;
+  gs_engine_destroy(e);
+  return rc;
+}
+
+int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,
+                     int32_t* dst_dev, void* stream) {
+  if (scale < 1 || scale > 31 || edgefactor < 1) {
+    set_error("invalid R-MAT scale / edgefactor");
+    return GS_EINVAL;
+  }
+  return rmat_generate(scale, seed, (int64_t)edgefactor << scale, src_dev, dst_dev,
+                       (cudaStream_t)stream);
+}
+
+int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev, int32_t* edges_dev,
+                       int64_t* m_out, void* stream) {
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  if (stream) GS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int rc = normalize_edges(e, count, src_dev, dst_dev, edges_dev, m_out);
+  gs_engine_destroy(e);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,632 @@
+// build.cu -- degree-rank relabel + CSR build on the device (replaces
+// build_graph, graph.py:162-259), the reference-layout build, and the
+// synthetic R-MAT workload generator.
+#include <cub/cub.cuh>
+
+#include "engine.cuh"
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// small helpers
+
+template <class F>
+static int cub_call(gs_engine* e, F&& f) {
+  size_t bytes = 0;
+  GS_CUDA(f(nullptr, bytes));
+  void* tmp = nullptr;
+  GS_TRY(e->alloc(&tmp, bytes > 0 ? bytes : 1));
+  cudaError_t err = f(tmp, bytes);
+  e->release(tmp);
+  GS_CUDA(err);
+  return GS_OK;
+}
+
+static int bits_for(int64_t x) {  // bits needed to represent values in [0, x]
+  int b = 0;
+  while (b < 62 && (int64_t(1) << b) <= x) ++b;
+  return b < 1 ? 1 : b;
+}
+
+__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo, int64_t hi,
+                                                   int64_t x) {
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+__global__ void k_count_deg_edges(const int32_t* __restrict__ uv, int64_t m, int64_t n,
+                                  uint32_t* __restrict__ deg, int* __restrict__ bad) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int2 p = reinterpret_cast<const int2*>(uv)[k];
+    if (p.x < 0 || p.y < 0 || p.x >= n || p.y >= n || p.x == p.y) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    atomicAdd(&deg[p.x], 1u);
+    atomicAdd(&deg[p.y], 1u);
+  }
+}
+
+__global__ void k_deg_from_off(const int64_t* __restrict__ off, int64_t n,
+                               uint32_t* __restrict__ deg, int* __restrict__ bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = off[v + 1] - off[v];
+    if (d < 0 || d > 0x7fffffff) { atomicExch(bad, 2); d = 0; }
+    deg[v] = (uint32_t)d;
+  }
+}
+
+__global__ void k_rank_keys(const uint32_t* __restrict__ deg, int64_t n,
+                            uint64_t* __restrict__ keys) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    keys[v] = ((uint64_t)deg[v] << 32) | (uint64_t)v;
+}
+
+// sorted (deg, id) keys -> orig[rank], rank[orig], ndeg[rank]
+__global__ void k_rank_scatter(const uint64_t* __restrict__ keys, int64_t n,
+                               int32_t* __restrict__ orig, int32_t* __restrict__ rank,
+                               int64_t* __restrict__ ndeg) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[r];
+    int32_t v = (int32_t)(uint32_t)k;
+    orig[r] = v;
+    rank[v] = (int32_t)r;
+    ndeg[r] = (int64_t)(k >> 32);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ndeg[n] = 0;
+}
+
+__global__ void k_arc_keys_edges(const int32_t* __restrict__ uv, int64_t m,
+                                 const int32_t* __restrict__ rank, int B,
+                                 uint64_t* __restrict__ keys) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int2 p = reinterpret_cast<const int2*>(uv)[k];
+    uint64_t ru = rank ? (uint64_t)rank[p.x] : (uint64_t)p.x;
+    uint64_t rv = rank ? (uint64_t)rank[p.y] : (uint64_t)p.y;
+    keys[2 * k] = (ru << B) | rv;
+    keys[2 * k + 1] = (rv << B) | ru;
+  }
+}
+
+// CSR input: owner of each slot by a binary search narrowed per block.
+__global__ void k_arc_keys_csr(const int64_t* __restrict__ off, int64_t n,
+                               const int32_t* __restrict__ adj, int64_t slots,
+                               const int32_t* __restrict__ rank, int B,
+                               uint64_t* __restrict__ keys, int* __restrict__ bad) {
+  int64_t base = blockIdx.x * (int64_t)blockDim.x;
+  int64_t i = base + threadIdx.x;
+  __shared__ int64_t vlo, vhi;
+  if (threadIdx.x == 0) {
+    int64_t last = base + blockDim.x - 1;
+    if (last >= slots) last = slots - 1;
+    vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
+    vhi = upper_bound_i64(off, 0, n + 1, last);
+  }
+  __syncthreads();
+  if (i >= slots) return;
+  int64_t u = upper_bound_i64(off, vlo, vhi, i) - 1;
+  int32_t v = adj[i];
+  if (v < 0 || v >= n || v == u) { atomicExch(bad, 3); v = 0; }
+  if (i > off[u] && adj[i - 1] >= v) atomicExch(bad, 4);  // runs strictly increasing
+  uint64_t ru = rank ? (uint64_t)rank[u] : (uint64_t)u;
+  uint64_t rv = rank ? (uint64_t)rank[v] : (uint64_t)v;
+  keys[i] = (ru << B) | rv;
+}
+
+__global__ void k_extract_adj(const uint64_t* __restrict__ keys, int64_t slots, int B,
+                              int32_t* __restrict__ adj, int* __restrict__ bad) {
+  const uint64_t mask = (uint64_t(1) << B) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    adj[i] = (int32_t)(k & mask);
+    if (i > 0 && keys[i - 1] == k) atomicExch(bad, 5);  // duplicate undirected edge
+  }
+}
+
+// number of neighbours with smaller rank (the prefix owned by b)
+__global__ void k_lowcnt(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                         int64_t n, int64_t* __restrict__ cnt) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = off[b], hi = off[b + 1];
+    int64_t l = lo, h = hi;
+    while (l < h) {
+      int64_t mid = (l + h) >> 1;
+      if (adj[mid] < (int32_t)b) l = mid + 1; else h = mid;
+    }
+    cnt[b] = l - lo;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[n] = 0;
+}
+
+// expand oriented edges: light vertices, one thread each
+__global__ void k_expand_light(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                               const int64_t* __restrict__ eoff, int64_t rlo, int64_t rhi,
+                               int32_t* __restrict__ elo, int32_t* __restrict__ ehi) {
+  for (int64_t b = rlo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < rhi;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e0 = eoff[b], e1 = eoff[b + 1], s = off[b];
+    for (int64_t e = e0; e < e1; ++e) {
+      elo[e] = adj[s + (e - e0)];
+      ehi[e] = (int32_t)b;
+    }
+  }
+}
+
+// heavy vertices: one block per vertex
+__global__ void k_expand_heavy(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                               const int64_t* __restrict__ eoff, int64_t rlo, int64_t rhi,
+                               int32_t* __restrict__ elo, int32_t* __restrict__ ehi) {
+  for (int64_t b = rlo + blockIdx.x; b < rhi; b += gridDim.x) {
+    int64_t e0 = eoff[b], e1 = eoff[b + 1], s = off[b];
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      elo[e] = adj[s + (e - e0)];
+      ehi[e] = (int32_t)b;
+    }
+  }
+}
+
+// first rank whose degree >= each class threshold (degrees sorted ascending)
+__global__ void k_class_bounds(const int64_t* __restrict__ ndeg, int64_t n,
+                               int64_t* __restrict__ out) {
+  int c = threadIdx.x;
+  if (c < DevGraph::kClasses) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (ndeg[mid] < deg_class(c)) lo = mid + 1; else hi = mid;
+    }
+    out[c] = lo;
+  }
+  if (c == DevGraph::kClasses) out[c] = n > 0 ? ndeg[n - 1] : 0;
+}
+
+// ---------------------------------------------------------------------------
+// shared tail of both builds: given rank[] (or null) and arc keys, finish CSR
+
+static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int B,
+                        uint64_t* keys_alt, int64_t* ndeg, int* d_bad) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  const int64_t slots = 2 * m;
+  // sort the 2m arc keys (rank_u, rank_v) -> CSR order
+  cub::DoubleBuffer<uint64_t> db(keys, keys_alt);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, slots, 0, 2 * B, st);
+  }));
+  uint64_t* sorted = db.Current();
+  GS_TRY(e->alloc_n(&g.adj, slots));
+  if (slots > 0) {
+    k_extract_adj<<<e->sms * 16, 256, 0, st>>>(sorted, slots, B, g.adj, d_bad);
+    e->launches++;
+  }
+  e->release(keys);
+  e->release(keys_alt);
+  // offsets from the rank-ordered degrees
+  GS_TRY(e->alloc_n(&g.off, n + 1));
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, ndeg, g.off, n + 1, st);
+  }));
+  // class bounds + dmax
+  int64_t* d_cls = nullptr;
+  GS_TRY(e->alloc_n(&d_cls, DevGraph::kClasses + 1));
+  k_class_bounds<<<1, 32, 0, st>>>(ndeg, n, d_cls);
+  e->launches++;
+  int64_t h_cls[DevGraph::kClasses + 1];
+  GS_CUDA(cudaMemcpyAsync(h_cls, d_cls, sizeof(h_cls), cudaMemcpyDeviceToHost, st));
+  e->release(ndeg);
+  // oriented edge offsets
+  int64_t* cnt = nullptr;
+  GS_TRY(e->alloc_n(&cnt, n + 1));
+  if (n > 0) {
+    k_lowcnt<<<grid_for(n, 256), 256, 0, st>>>(g.off, g.adj, n, cnt);
+    e->launches++;
+  }
+  GS_TRY(e->alloc_n(&g.eoff, n + 1));
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, cnt, g.eoff, n + 1, st);
+  }));
+  e->release(cnt);
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(d_cls);
+  int h_bad = 0;
+  GS_CUDA(cudaMemcpy(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  e->release(d_bad);
+  if (h_bad) {
+    const char* why = h_bad == 1   ? "edge has an id outside [0, n) or is a self-loop"
+                      : h_bad == 2 ? "vertex_offsets not monotone"
+                      : h_bad == 3 ? "adjacency entry outside [0, n) or a self-loop"
+                      : h_bad == 4 ? "adjacency runs not strictly increasing"
+                                   : "duplicate undirected edge";
+    set_error(std::string("invalid graph: ") + why);
+    return GS_EINVAL;
+  }
+  for (int c = 0; c < DevGraph::kClasses; ++c) g.rclass[c] = h_cls[c];
+  g.dmax = h_cls[DevGraph::kClasses];
+  int64_t mm = 0;
+  GS_CUDA(cudaMemcpy(&mm, g.eoff + n, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (mm != m) {
+    set_error("invalid graph: adjacency is not symmetric");
+    return GS_EINVAL;
+  }
+  GS_TRY(e->alloc_n(&g.elo, m));
+  GS_TRY(e->alloc_n(&g.ehi, m));
+  const int64_t rsplit = g.rclass[1];  // degree >= 64 -> block per vertex
+  if (rsplit > 0) {
+    k_expand_light<<<grid_for(rsplit, 256), 256, 0, st>>>(g.off, g.adj, g.eoff, 0, rsplit,
+                                                          g.elo, g.ehi);
+    e->launches++;
+  }
+  if (n > rsplit) {
+    int64_t nb = n - rsplit;
+    k_expand_heavy<<<(unsigned)(nb < 65535 * 4 ? nb : 65535 * 4), 256, 0, st>>>(
+        g.off, g.adj, g.eoff, rsplit, n, g.elo, g.ehi);
+    e->launches++;
+  }
+  GS_CUDA(cudaGetLastError());
+  g.n = n;
+  g.m = m;
+  return GS_OK;
+}
+
+int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
+  cudaStream_t st = e->stream;
+  DevGraph& g = e->g;
+  e->free_graph();
+  int* d_bad = nullptr;
+  GS_TRY(e->alloc_n(&d_bad, 1));
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  uint32_t* deg = nullptr;
+  GS_TRY(e->alloc_n(&deg, n));
+  GS_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1), st));
+  if (m > 0) {
+    k_count_deg_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, n, deg, d_bad);
+    e->launches++;
+  }
+  uint64_t *vk = nullptr, *vk2 = nullptr;
+  GS_TRY(e->alloc_n(&vk, n));
+  GS_TRY(e->alloc_n(&vk2, n));
+  if (n > 0) {
+    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
+    e->launches++;
+  }
+  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
+  }));
+  int64_t* ndeg = nullptr;
+  GS_TRY(e->alloc_n(&g.orig, n));
+  GS_TRY(e->alloc_n(&g.rank, n));
+  int32_t* rank = g.rank;
+  GS_TRY(e->alloc_n(&ndeg, n + 1));
+  if (n > 0) {
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, rank, ndeg);
+    e->launches++;
+  } else {
+    GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
+  }
+  e->release(vk);
+  e->release(vk2);
+  e->release(deg);
+  const int B = bits_for(n > 0 ? n - 1 : 0);
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  GS_TRY(e->alloc_n(&keys, 2 * m));
+  GS_TRY(e->alloc_n(&keys2, 2 * m));
+  if (m > 0) {
+    k_arc_keys_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, rank, B, keys);
+    e->launches++;
+  }
+  return finish_build(e, n, m, keys, B, keys2, ndeg, d_bad);
+}
+
+int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
+                   const int32_t* adj) {
+  cudaStream_t st = e->stream;
+  DevGraph& g = e->g;
+  e->free_graph();
+  int* d_bad = nullptr;
+  GS_TRY(e->alloc_n(&d_bad, 1));
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  uint32_t* deg = nullptr;
+  GS_TRY(e->alloc_n(&deg, n));
+  if (n > 0) {
+    k_deg_from_off<<<grid_for(n, 256), 256, 0, st>>>(off, n, deg, d_bad);
+    e->launches++;
+  }
+  uint64_t *vk = nullptr, *vk2 = nullptr;
+  GS_TRY(e->alloc_n(&vk, n));
+  GS_TRY(e->alloc_n(&vk2, n));
+  if (n > 0) {
+    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
+    e->launches++;
+  }
+  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
+  }));
+  int64_t* ndeg = nullptr;
+  GS_TRY(e->alloc_n(&g.orig, n));
+  GS_TRY(e->alloc_n(&g.rank, n));
+  int32_t* rank = g.rank;
+  GS_TRY(e->alloc_n(&ndeg, n + 1));
+  if (n > 0) {
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, rank, ndeg);
+    e->launches++;
+  } else {
+    GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
+  }
+  e->release(vk);
+  e->release(vk2);
+  e->release(deg);
+  const int B = bits_for(n > 0 ? n - 1 : 0);
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  GS_TRY(e->alloc_n(&keys, 2 * m));
+  GS_TRY(e->alloc_n(&keys2, 2 * m));
+  if (m > 0) {
+    k_arc_keys_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 2 * m, rank, B, keys,
+                                                         d_bad);
+    e->launches++;
+  }
+  return finish_build(e, n, m, keys, B, keys2, ndeg, d_bad);
+}
+
+__global__ void k_widen(const uint32_t* __restrict__ d, int64_t n, int64_t* __restrict__ o) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    o[v] = d[v];
+}
+
+// ---------------------------------------------------------------------------
+// reference-layout build (gs_build_graph): original ids, edge_list, edge_ids
+
+__global__ void k_orient_flags(const int64_t* __restrict__ off, int64_t n,
+                               const int32_t* __restrict__ adj, int64_t slots,
+                               int64_t* __restrict__ flag) {
+  int64_t base = blockIdx.x * (int64_t)blockDim.x;
+  int64_t i = base + threadIdx.x;
+  __shared__ int64_t vlo, vhi;
+  if (threadIdx.x == 0) {
+    int64_t last = base + blockDim.x - 1;
+    if (last >= slots) last = slots - 1;
+    vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
+    vhi = upper_bound_i64(off, 0, n + 1, last);
+  }
+  __syncthreads();
+  if (i >= slots) return;
+  int64_t a = upper_bound_i64(off, vlo, vhi, i) - 1;
+  int32_t b = adj[i];
+  int64_t da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+  flag[i] = (da < db || (da == db && a < b)) ? 1 : 0;  // graph.py:226
+}
+
+__global__ void k_orient_emit(const int64_t* __restrict__ off, int64_t n,
+                              const int32_t* __restrict__ adj, int64_t slots,
+                              const int64_t* __restrict__ pos, int32_t* __restrict__ edge_ids,
+                              int32_t* __restrict__ edge_list) {
+  int64_t base = blockIdx.x * (int64_t)blockDim.x;
+  int64_t i = base + threadIdx.x;
+  __shared__ int64_t vlo, vhi;
+  if (threadIdx.x == 0) {
+    int64_t last = base + blockDim.x - 1;
+    if (last >= slots) last = slots - 1;
+    vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
+    vhi = upper_bound_i64(off, 0, n + 1, last);
+  }
+  __syncthreads();
+  if (i >= slots) return;
+  if (pos[i + 1] == pos[i]) return;  // not an owned slot
+  int64_t k = pos[i];
+  int32_t a = (int32_t)(upper_bound_i64(off, vlo, vhi, i) - 1);
+  int32_t b = adj[i];
+  edge_list[2 * k] = a;
+  edge_list[2 * k + 1] = b;
+  edge_ids[i] = (int32_t)k;
+  int64_t l = off[b], h = off[b + 1];  // bisect_left(adjacency, a, ...) graph.py:236
+  while (l < h) {
+    int64_t mid = (l + h) >> 1;
+    if (adj[mid] < a) l = mid + 1; else h = mid;
+  }
+  edge_ids[l] = (int32_t)k;
+}
+
+int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv_dev,
+                           int64_t* off_dev, int32_t* adj_dev, int32_t* eids_dev,
+                           int32_t* elist_dev) {
+  cudaStream_t st = e->stream;
+  int* d_bad = nullptr;
+  GS_TRY(e->alloc_n(&d_bad, 1));
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  uint32_t* deg = nullptr;
+  GS_TRY(e->alloc_n(&deg, n));
+  GS_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1), st));
+  if (m > 0) {
+    k_count_deg_edges<<<e->sms * 8, 256, 0, st>>>(uv_dev, m, n, deg, d_bad);
+    e->launches++;
+  }
+  int64_t* deg64 = nullptr;
+  GS_TRY(e->alloc_n(&deg64, n + 1));
+  GS_CUDA(cudaMemsetAsync(deg64, 0, sizeof(int64_t) * (size_t)(n + 1), st));
+  if (n > 0) {
+    k_widen<<<grid_for(n, 256), 256, 0, st>>>(deg, n, deg64);
+    e->launches++;
+  }
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, deg64, off_dev, n + 1, st);
+  }));
+  e->release(deg64);
+  e->release(deg);
+  const int B = bits_for(n > 0 ? n - 1 : 0);
+  const int64_t slots = 2 * m;
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  GS_TRY(e->alloc_n(&keys, slots));
+  GS_TRY(e->alloc_n(&keys2, slots));
+  if (m > 0) {
+    k_arc_keys_edges<<<e->sms * 8, 256, 0, st>>>(uv_dev, m, nullptr, B, keys);
+    e->launches++;
+  }
+  cub::DoubleBuffer<uint64_t> db(keys, keys2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, slots, 0, 2 * B, st);
+  }));
+  if (slots > 0) {
+    k_extract_adj<<<e->sms * 16, 256, 0, st>>>(db.Current(), slots, B, adj_dev, d_bad);
+    e->launches++;
+  }
+  e->release(keys);
+  e->release(keys2);
+  int64_t* flag = nullptr;
+  int64_t* pos = nullptr;
+  GS_TRY(e->alloc_n(&flag, slots + 1));
+  GS_TRY(e->alloc_n(&pos, slots + 1));
+  GS_CUDA(cudaMemsetAsync(flag + slots, 0, sizeof(int64_t), st));
+  if (slots > 0) {
+    k_orient_flags<<<grid_for(slots, 256), 256, 0, st>>>(off_dev, n, adj_dev, slots, flag);
+    e->launches++;
+  }
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, flag, pos, slots + 1, st);
+  }));
+  if (slots > 0) {
+    k_orient_emit<<<grid_for(slots, 256), 256, 0, st>>>(off_dev, n, adj_dev, slots, pos,
+                                                        eids_dev, elist_dev);
+    e->launches++;
+  }
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(flag);
+  e->release(pos);
+  int h_bad = 0;
+  GS_CUDA(cudaMemcpy(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  e->release(d_bad);
+  if (h_bad) {
+    set_error(h_bad == 1 ? "invalid edge list: id outside [0, n) or self-loop"
+                         : "invalid edge list: duplicate undirected edge");
+    return GS_EINVAL;
+  }
+  return GS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// R-MAT generator (same stream as oracle/gscan_oracle.c orc_rmat_edges)
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint32_t rmat_scramble(uint32_t x, int scale, uint64_t sm) {
+  const uint64_t mask = (scale >= 32) ? 0xFFFFFFFFull : ((1ull << scale) - 1);
+  const int h = (scale + 1) / 2;
+  uint64_t y = x;
+  y = (y * 0x9E3779B97F4A7C15ULL + (sm & mask)) & mask;
+  y ^= y >> h;
+  y = (y * 0xD6E8FEB86659FD93ULL) & mask;
+  y ^= y >> h;
+  return (uint32_t)y;
+}
+
+__global__ void k_rmat(int scale, uint64_t sm, int64_t count, int32_t* __restrict__ src,
+                       int32_t* __restrict__ dst) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = (uint64_t)t;
+    uint32_t u = 0, v = 0;
+    uint64_t r = 0;
+    for (int l = 0; l < scale; ++l) {
+      uint32_t x;
+      if ((l & 1) == 0) {
+        r = mix64(sm ^ (i * 32u + (uint64_t)(l >> 1)));
+        x = (uint32_t)(r >> 32);
+      } else {
+        x = (uint32_t)r;
+      }
+      const uint32_t qd = x < 2448131358u ? 0u : x < 3264175144u ? 1u : x < 4080218931u ? 2u : 3u;
+      u = (u << 1) | (qd >> 1);
+      v = (v << 1) | (qd & 1u);
+    }
+    src[t] = (int32_t)rmat_scramble(u, scale, sm);
+    dst[t] = (int32_t)rmat_scramble(v, scale, sm ^ 0x5bd1e995u);
+  }
+}
+
+__global__ void k_pair_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                            int64_t count, uint64_t* __restrict__ keys) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t u = (uint32_t)src[i], v = (uint32_t)dst[i];
+    if (u > v) { uint32_t t = u; u = v; v = t; }
+    keys[i] = (u == v) ? ~0ull : (((uint64_t)u << 32) | v);
+  }
+}
+
+__global__ void k_unpack_pairs(const uint64_t* __restrict__ keys, int64_t count,
+                               int32_t* __restrict__ uv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+    reinterpret_cast<int2*>(uv)[i] = make_int2((int32_t)(k >> 32), (int32_t)(uint32_t)k);
+  }
+}
+
+int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t* dst,
+                  cudaStream_t st) {
+  if (count > 0) k_rmat<<<148 * 16, 256, 0, st>>>(scale, mix64(seed), count, src, dst);
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32_t* dst,
+                    int32_t* uv, int64_t* m_out) {
+  cudaStream_t st = e->stream;
+  uint64_t *k1 = nullptr, *k2 = nullptr;
+  GS_TRY(e->alloc_n(&k1, count));
+  GS_TRY(e->alloc_n(&k2, count));
+  if (count > 0) {
+    k_pair_keys<<<e->sms * 8, 256, 0, st>>>(src, dst, count, k1);
+    e->launches++;
+  }
+  cub::DoubleBuffer<uint64_t> db(k1, k2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, count, 0, 64, st);
+  }));
+  uint64_t* sorted = db.Current();
+  uint64_t* other = db.Alternate();
+  int64_t* d_num = nullptr;
+  GS_TRY(e->alloc_n(&d_num, 1));
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, sorted, other, d_num, count, st);
+  }));
+  int64_t nu = 0;
+  GS_CUDA(cudaMemcpyAsync(&nu, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  uint64_t last = 0;
+  if (nu > 0) {
+    GS_CUDA(cudaMemcpy(&last, other + nu - 1, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (last == ~0ull) --nu;  // the self-loop sentinel sorts last
+  }
+  if (nu > 0) {
+    k_unpack_pairs<<<e->sms * 8, 256, 0, st>>>(other, nu, uv);
+    e->launches++;
+  }
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(k1);
+  e->release(k2);
+  e->release(d_num);
+  *m_out = nu;
+  return GS_OK;
+}
+
+}  // namespace gs

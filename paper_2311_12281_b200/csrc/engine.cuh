@@ -1,0 +1,143 @@
+// engine.cuh -- device context, resident graph and scan state of libgscan.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gs {
+
+// Degree-rank space graph (the engine's only internal layout).
+//
+// Vertices are relabelled by rank = position in (degree, original id) order,
+// the order the reference uses to orient edges (graph.py:218-231).  In rank
+// space the oriented edge (a, b) -- a the lower-degree endpoint -- is simply
+// "a < b", so the edges owned by the higher endpoint b are the prefix of b's
+// sorted adjacency run that is smaller than b.  Oriented edge ids are
+// e = eoff[b] + j for the j-th prefix element: edges are grouped by their
+// HIGH endpoint, which is the endpoint whose list the similarity kernels
+// stage in shared memory.
+struct DevGraph {
+  int64_t n = 0, m = 0;
+  int64_t* off = nullptr;   // [n+1] CSR offsets (rank space)
+  int32_t* adj = nullptr;   // [2m] sorted neighbour ranks
+  int32_t* orig = nullptr;  // [n] rank -> caller vertex id
+  int32_t* rank = nullptr;  // [n] caller vertex id -> rank
+  int64_t* eoff = nullptr;  // [n+1] oriented-edge offsets (prefix counts)
+  int32_t* elo = nullptr;   // [m] low endpoint a of edge e
+  int32_t* ehi = nullptr;   // [m] high endpoint b of edge e
+  int64_t dmax = 0;
+  // rank boundaries of degree classes: first rank with degree >= kDegClass[i]
+  static constexpr int kClasses = 6;
+  int64_t rclass[kClasses] = {0};
+};
+
+// degree-class thresholds used to route edges to kernels (by HIGH endpoint):
+// [1,64) tiny (thread per edge), [64,512) small, [512,4096) medium,
+// [4096,28672) large (CTA + shared-memory table), >= 28672 huge (L2 table)
+__host__ __device__ constexpr int64_t deg_class(int c) {
+  return c == 0 ? 1 : c == 1 ? 64 : c == 2 ? 512 : c == 3 ? 4096 : c == 4 ? 28672 : (1ll << 40);
+}
+
+// Scan working state (ClusterState, scan.py:87-134, re-laid out for atomics).
+struct DevState {
+  uint8_t* sim = nullptr;       // [m] similarity status per oriented edge
+  uint64_t* bounds = nullptr;   // [n] lower | upper << 32 (Lemma 1 counters)
+  uint8_t* role = nullptr;      // [n] ROLE_* (write-once during identify)
+  int32_t* parent = nullptr;    // [n] union-find forest over cores (ranks)
+  int32_t* label = nullptr;     // [n] canonical label (min caller id) per root
+  int32_t* lmin = nullptr;      // [n] min cluster label per clustered vertex
+  int32_t* lmax = nullptr;      // [n] max cluster label per clustered vertex
+  unsigned long long* ctr = nullptr;  // device counters (see Ctr)
+  int32_t* wq = nullptr;        // work-queue heads for persistent kernels
+};
+
+enum Ctr {
+  CTR_SIM_EVALS = 0,
+  CTR_PROBES,
+  CTR_UNION_RETRIES,
+  CTR_BOUND_DECIDED,
+  CTR_INTERSECTIONS,
+  CTR_ALG_BYTES,
+  CTR_UNRESOLVED,
+  CTR_N_CORE,
+  CTR_N_MEMBER,
+  CTR_N_HUB,
+  CTR_N_OUTLIER,
+  CTR_N_CLUSTERS,
+  CTR_COUNT
+};
+
+enum SimMode : int {
+  MODE_IDENTIFY = 0,  // identifyCore (Alg. 2): skip if both roles decided
+  MODE_CLEANUP = 1,   // unresolved endpoint, status unknown
+  MODE_UNION = 2,     // core-core, unknown, roots differ -> union if similar
+  MODE_ATTACH = 3     // core-noncore, unknown
+};
+
+struct SimParams {
+  const int64_t* off;
+  const int32_t* adj;
+  const int64_t* eoff;
+  const int32_t* elo;
+  const int32_t* ehi;
+  uint8_t* sim;
+  uint64_t* bounds;
+  uint8_t* role;
+  int32_t* parent;
+  unsigned long long* ctr;
+  int32_t* wq;
+  uint32_t* gtab;  // global hash scratch for very large lists
+  int64_t gtab_stride;
+  Eps2 eps;
+  int32_t mu;
+  int mode;
+};
+
+}  // namespace gs
+
+struct gs_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t cap = 0;
+  size_t live = 0, peak = 0;
+  std::unordered_map<void*, size_t> sizes;
+  gs::DevGraph g;
+  gs::DevState s;
+  int sms = 148;
+  int64_t launches = 0;
+  float last_h2d_ms = 0, last_build_ms = 0;
+  // host-side pinned staging for counters
+  unsigned long long* h_ctr = nullptr;
+  std::vector<cudaEvent_t> ev;
+
+  int alloc(void** p, size_t bytes);
+  void release(void* p);
+  template <class T>
+  int alloc_n(T** p, int64_t count) {
+    return alloc(reinterpret_cast<void**>(p), (size_t)(count > 0 ? count : 1) * sizeof(T));
+  }
+  void free_graph();
+  void free_state();
+};
+
+namespace gs {
+// build.cu
+int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_dev);
+int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
+                   const int32_t* adj_dev);
+// sim.cu
+int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
+// cluster.cu
+int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
+             int32_t* cluster_out, int out_on_device, gs_stats* st);
+// launch helper: grid for n items
+inline unsigned grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+}  // namespace gs

@@ -1,0 +1,343 @@
+"""Host mirror of the reference clustering call (graphscan/scan.py).
+
+``scan_in_memory(g, mu, epsilon, *, workers=1)`` keeps the reference
+signature, validation and error behaviour (scan.py:965-982) and returns the
+same result/stat types; the three phases run on the B200 through
+libgscan.so (``gs_engine_load_csr`` + ``gs_engine_scan``).  There is no CPU
+path: without the shared library the import of ``_lib`` fails.
+
+Cluster ids are canonical: the smallest core vertex id of the
+cluster, and for a border vertex eligible for several clusters the smallest
+such cluster.  The reference's own ids are union-find roots; both are valid
+under ``results_equivalent`` (oracle.py:220-297) and the canonical form is
+additionally bit-exact against ``serial_scan``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from enum import Enum
+from fractions import Fraction
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _lib
+from .graph import as_array, graph_arrays
+
+EpsilonLike = Union[str, float, int, Fraction]
+
+# byte codes (scan.py:38-56)
+SIM_UNKNOWN, SIM_SIMILAR, SIM_DISSIMILAR = 0, 1, 2
+ROLE_UNKNOWN, ROLE_CORE, ROLE_NONCORE, ROLE_MEMBER = 0, 1, 2, 3
+ROLE_MEMBER_SHARED, ROLE_HUB, ROLE_OUTLIER = 4, 5, 6
+PARENT_NONE, PARENT_HUB = -2, -1
+
+
+class Role(Enum):
+    UNKNOWN = "unknown"
+    CORE = "core"
+    NONCORE = "noncore"
+    MEMBER = "member"
+    HUB = "hub"
+    OUTLIER = "outlier"
+
+
+_PUBLIC_ROLE = {
+    ROLE_UNKNOWN: Role.UNKNOWN,
+    ROLE_CORE: Role.CORE,
+    ROLE_NONCORE: Role.NONCORE,
+    ROLE_MEMBER: Role.MEMBER,
+    ROLE_MEMBER_SHARED: Role.MEMBER,
+    ROLE_HUB: Role.HUB,
+    ROLE_OUTLIER: Role.OUTLIER,
+}
+ROLE_LETTERS = {Role.CORE: "C", Role.MEMBER: "M", Role.HUB: "H", Role.OUTLIER: "O"}
+_CODE_LETTER = np.array([b"?", b"C", b"N", b"M", b"M", b"H", b"O"], dtype="S1")
+
+
+def epsilon_fraction(epsilon: EpsilonLike) -> Fraction:
+    """scan.py:137-152: validate epsilon, exact Fraction in (0, 1]."""
+    if isinstance(epsilon, Fraction):
+        f = epsilon
+    elif isinstance(epsilon, (str, int)) and not isinstance(epsilon, bool):
+        try:
+            f = Fraction(epsilon)
+        except (ValueError, ZeroDivisionError):
+            raise ValueError(f"epsilon is not a number: {epsilon!r}") from None
+    elif isinstance(epsilon, float):
+        f = Fraction(epsilon)  # exact binary value
+    else:
+        raise TypeError(f"unsupported epsilon type: {type(epsilon).__name__}")
+    if not 0 < f <= 1:
+        raise ValueError(f"epsilon must be in (0, 1], got {epsilon!r}")
+    return f
+
+
+class ClusteringResult:
+    """Per-vertex roles and cluster ids (scan.py:858-908).
+
+    Backed by the device output arrays; ``roles`` / ``cluster_id`` are
+    materialised as the reference's Python lists on first access (they stay
+    mutable, as the reference's are).
+    """
+
+    def __init__(self, n: int, role_codes: np.ndarray, cluster_ids: np.ndarray,
+                 orig_ids: np.ndarray):
+        self.n = int(n)
+        self.role_codes = role_codes
+        self.cluster_ids = cluster_ids
+        self._orig = orig_ids
+        self._roles: Optional[list] = None
+        self._cluster: Optional[list] = None
+        self._orig_list: Optional[list] = None
+
+    @property
+    def roles(self) -> list:
+        if self._roles is None:
+            self._roles = [_PUBLIC_ROLE[int(c)] for c in self.role_codes]
+        return self._roles
+
+    @roles.setter
+    def roles(self, value: list) -> None:
+        self._roles = value
+
+    @property
+    def cluster_id(self) -> list:
+        if self._cluster is None:
+            self._cluster = self.cluster_ids.tolist()
+        return self._cluster
+
+    @cluster_id.setter
+    def cluster_id(self, value: list) -> None:
+        self._cluster = value
+
+    @property
+    def orig_ids(self) -> list:
+        if self._orig_list is None:
+            self._orig_list = np.asarray(self._orig).tolist()
+        return self._orig_list
+
+    def _codes(self) -> np.ndarray:
+        if self._roles is None:
+            return self.role_codes
+        letters = {Role.CORE: ROLE_CORE, Role.MEMBER: ROLE_MEMBER, Role.HUB: ROLE_HUB,
+                   Role.OUTLIER: ROLE_OUTLIER, Role.UNKNOWN: ROLE_UNKNOWN,
+                   Role.NONCORE: ROLE_NONCORE}
+        return np.array([letters[r] for r in self._roles], dtype=np.uint8)
+
+    def _ids(self) -> np.ndarray:
+        if self._cluster is None:
+            return self.cluster_ids
+        return np.asarray(self._cluster, dtype=np.int64)
+
+    def _set(self, code: int) -> set[int]:
+        c = self._codes()
+        if code == ROLE_MEMBER:
+            mask = (c == ROLE_MEMBER) | (c == ROLE_MEMBER_SHARED)
+        else:
+            mask = c == code
+        return set(np.flatnonzero(mask).tolist())
+
+    def core_set(self) -> set[int]:
+        return self._set(ROLE_CORE)
+
+    def member_set(self) -> set[int]:
+        return self._set(ROLE_MEMBER)
+
+    def hub_set(self) -> set[int]:
+        return self._set(ROLE_HUB)
+
+    def outlier_set(self) -> set[int]:
+        return self._set(ROLE_OUTLIER)
+
+    def core_equivalence(self) -> set[frozenset[int]]:
+        codes, ids = self._codes(), self._ids()
+        classes: dict[int, set[int]] = {}
+        for v in np.flatnonzero(codes == ROLE_CORE).tolist():
+            classes.setdefault(int(ids[v]), set()).add(v)
+        return {frozenset(s) for s in classes.values()}
+
+    def to_text(self) -> str:
+        """``orig<TAB>role<TAB>orig(cluster)|-1`` per vertex (scan.py:892-904)."""
+        if self.n == 0:
+            return ""
+        codes, ids = self._codes(), self._ids()
+        orig = np.asarray(self._orig, dtype=np.int64)
+        shown = np.where(ids >= 0, orig[np.clip(ids, 0, None)], -1)
+        letters = _CODE_LETTER[codes].astype(str)
+        lines = [f"{o}\t{r}\t{c}" for o, r, c in zip(orig.tolist(), letters.tolist(),
+                                                   shown.tolist())]
+        return "\n".join(lines) + "\n"
+
+    def write(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8") as f:
+            f.write(self.to_text())
+
+
+@dataclass
+class StatsReport:
+    """Operation counts and phase timings (scan.py:911-947)."""
+
+    n: int = 0
+    m: int = 0
+    workers: int = 1
+    sim_evals: int = 0
+    adj_probes: int = 0
+    union_retries: int = 0
+    probe_bound_violations: int = 0
+    phases: dict = field(default_factory=dict)  # name -> microseconds
+    extra: dict = field(default_factory=dict)
+
+    def to_text(self) -> str:
+        lines = [
+            f"n={self.n}",
+            f"m={self.m}",
+            f"workers={self.workers}",
+            f"sim_evals={self.sim_evals}",
+            f"adj_probes={self.adj_probes}",
+            f"union_retries={self.union_retries}",
+            f"probe_bound_violations={self.probe_bound_violations}",
+        ]
+        lines.extend(f"phase_{name}_us={us}" for name, us in self.phases.items())
+        lines.extend(f"{key}={val}" for key, val in sorted(self.extra.items()))
+        return "\n".join(lines) + "\n"
+
+    def write(self, path: str) -> None:
+        with open(path, "w", encoding="utf-8") as f:
+            f.write(self.to_text())
+
+
+def stats_from_native(st: _lib.GsStats, n: int, m: int, workers: int) -> StatsReport:
+    ph = st.phase_ms
+    us = lambda i: int(round(ph[i] * 1000.0))  # noqa: E731
+    rep = StatsReport(n=n, m=m, workers=workers, sim_evals=int(st.sim_evals),
+                      adj_probes=int(st.adj_probes), union_retries=int(st.union_retries),
+                      probe_bound_violations=int(st.probe_bound_violations))
+    rep.phases = {
+        "identify": us(_lib.GS_PH_IDENTIFY),
+        "cleanup": us(_lib.GS_PH_CLEANUP),
+        "cluster": us(_lib.GS_PH_CLUSTER),
+        "classify": us(_lib.GS_PH_CLASSIFY),
+        "total": us(_lib.GS_PH_TOTAL),
+    }
+    rep.extra = {
+        "build_us": us(_lib.GS_PH_BUILD),
+        "h2d_us": us(_lib.GS_PH_H2D),
+        "d2h_us": us(_lib.GS_PH_D2H),
+        "sim_evals_avoided": m - int(st.sim_evals),
+        "sim_decided_by_bound": int(st.sim_decided_by_bound),
+        "sim_intersections": int(st.sim_intersections),
+        "hbm_bytes_alg": int(st.alg_bytes_sim) + 9 * int(st.sim_evals) + 8 * (n + 1),
+        "clusters": int(st.n_clusters),
+        "kernel_launches": int(st.kernel_launches),
+        "peak_device_bytes": int(st.peak_device_bytes),
+    }
+    if st.partitions:
+        rep.extra["partitions"] = int(st.partitions)
+    return rep
+
+
+def _validate(mu: int, workers: int, epsilon: EpsilonLike) -> Fraction:
+    if mu < 2:
+        raise ValueError(f"mu must be >= 2, got {mu}")
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    return epsilon_fraction(epsilon)
+
+
+def _dmax(off: np.ndarray) -> int:
+    return int(np.diff(off).max()) if len(off) > 1 else 0
+
+
+def scan_in_memory(g, mu: int, epsilon: EpsilonLike, *, workers: int = 1):
+    """Run the three-phase pipeline on the device (scan.py:965-982).
+
+    ``g`` is any reference-layout graph (this package's ``Graph`` or the
+    reference's).  ``workers`` is accepted and validated for signature
+    compatibility; the device schedule is data-parallel regardless and the
+    canonical output does not depend on it.
+    """
+    f = _validate(mu, workers, epsilon)
+    n, m, off, adj = graph_arrays(g)
+    orig = as_array(g.orig_ids, np.uint32) if n else np.empty(0, np.uint32)
+    eps2 = _lib.eps2_struct(f, _dmax(off))
+    roles = np.empty(n, dtype=np.uint8)
+    cids = np.empty(n, dtype=np.int32)
+    st = _lib.GsStats()
+    if n:
+        lib = _lib.load()
+        eng = _lib.thread_engine()
+        _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off.ctypes.data, adj.ctypes.data, 0))
+        _lib.check(lib.gs_engine_scan(eng.handle, int(mu), ctypes.byref(eps2), roles.ctypes.data,
+                                      cids.ctypes.data, 0, ctypes.byref(st)))
+        st.phase_ms[_lib.GS_PH_TOTAL] += st.phase_ms[_lib.GS_PH_H2D] + st.phase_ms[_lib.GS_PH_BUILD]
+    stats = stats_from_native(st, n, m, workers)
+    return ClusteringResult(n, roles, cids, orig), stats
+
+
+def scan_edges(n: int, edges: np.ndarray, mu: int, epsilon: EpsilonLike,
+               orig_ids: Optional[np.ndarray] = None):
+    """build_graph + scan_in_memory in one device call from a normalised
+    edge array (m, 2) int32 with u < v (gs_scan_edges)."""
+    f = _validate(mu, 1, epsilon)
+    e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1, 2)
+    m = int(e.shape[0])
+    roles = np.empty(n, dtype=np.uint8)
+    cids = np.empty(n, dtype=np.int32)
+    st = _lib.GsStats()
+    eps2 = _lib.eps2_struct(f)
+    if n:
+        lib = _lib.load()
+        _lib.check(lib.gs_scan_edges(n, m, e.ctypes.data, int(mu), ctypes.byref(eps2),
+                                     roles.ctypes.data, cids.ctypes.data, ctypes.byref(st)))
+    orig = np.arange(n, dtype=np.uint32) if orig_ids is None else np.asarray(orig_ids, np.uint32)
+    return ClusteringResult(n, roles, cids, orig), stats_from_native(st, n, m, 1)
+
+
+_loaded: dict = {}
+
+
+def _ensure_loaded(eng: _lib.Engine, g) -> None:
+    n, m, off, adj = graph_arrays(g)
+    key = (n, m, off.ctypes.data, adj.ctypes.data)
+    if _loaded.get(id(eng)) != key:
+        lib = _lib.load()
+        _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off.ctypes.data, adj.ctypes.data, 0))
+        _loaded[id(eng)] = key
+
+
+def check_sim(g, u: int, v: int, epsilon: EpsilonLike) -> bool:
+    """scan.py:241-258: exact similarity test of an existing edge (device)."""
+    f = epsilon_fraction(epsilon)
+    if not (0 <= u < g.n and 0 <= v < g.n) or u == v:
+        raise ValueError(f"({u}, {v}) is not an edge")
+    eng = _lib.thread_engine()
+    _ensure_loaded(eng, g)
+    uu = np.array([u], dtype=np.int32)
+    vv = np.array([v], dtype=np.int32)
+    out = np.empty(1, dtype=np.int8)
+    eps2 = _lib.eps2_struct(f, g.deg_max if hasattr(g, "deg_max") else None)
+    lib = _lib.load()
+    _lib.check(lib.gs_engine_check_sim(eng.handle, 1, uu.ctypes.data, vv.ctypes.data,
+                                       ctypes.byref(eps2), out.ctypes.data))
+    if out[0] < 0:
+        raise ValueError(f"({u}, {v}) is not an edge")
+    return bool(out[0])
+
+
+def structural_similarity(g, u: int, v: int) -> float:
+    """scan.py:164-200: float sigma over closed neighbourhoods (diagnostic,
+    host-side as in the reference; the engine uses the exact predicate)."""
+    if not (0 <= u < g.n and 0 <= v < g.n):
+        raise IndexError(f"vertex id out of range: ({u}, {v})")
+    if u == v:
+        return 1.0
+    n, m, off, adj = graph_arrays(g)
+    nu = adj[off[u]:off[u + 1]]
+    nv = adj[off[v]:off[v + 1]]
+    common = len(np.intersect1d(nu, nv, assume_unique=True))
+    adjacent = bool(np.any(nu == v))
+    inter = common + (2 if adjacent else 0)
+    return inter / ((len(nu) + 1) * (len(nv) + 1)) ** 0.5
