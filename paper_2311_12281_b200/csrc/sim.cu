@@ -121,39 +121,45 @@ __device__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
 }
 
 // ---------------------------------------------------------------------------
-// tiny b: one thread per oriented edge, merge of two runs shorter than 64
+// tiny b: one thread per high endpoint b (deg < 64), its owned edges in
+// order, merging two short runs.  Walking b's edges sequentially lets each
+// decision (b's bounds are applied immediately) prune b's later edges, the
+// progressive deferral of Alg. 2 line 2.
 
-__global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t elo_id, int64_t ehi_id) {
+__global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int64_t rhi) {
   LocalCtr lc;
-  for (int64_t e = elo_id + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ehi_id;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t a = P.elo[e], b = P.ehi[e];
-    if (!edge_needed(P, e, a, b)) continue;
-    const int64_t ia0 = P.off[a], ea = P.off[a + 1];
-    int64_t ib = P.off[b];
-    const int64_t eb = P.off[b + 1];
-    const int64_t da = ea - ia0, db = eb - ib;
-    const int64_t cmax = da - 1;
-    bool res;
-    if (!is_similar(cmax, da, db, P.eps)) { res = false; lc.bound++; }
-    else if (is_similar(0, da, db, P.eps)) { res = true; lc.bound++; }
-    else {
-      const int64_t cmin = c_min_exact(da, db, cmax, P.eps);
-      int64_t c = 0, ia = ia0;
-      res = false;
-      while (ia < ea && ib < eb) {
-        const int32_t x = P.adj[ia], y = P.adj[ib];
-        if (x == y) { ++c; ++ia; ++ib; }
-        else if (x < y) ++ia;
-        else ++ib;
-        if (c >= cmin) { res = true; break; }
-        if (c + (ea - ia) < cmin) break;
+  for (int64_t b = rlo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < rhi;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = P.eoff[b], e1 = P.eoff[b + 1];
+    if (e0 == e1) continue;
+    const int64_t ob = P.off[b], eb = P.off[b + 1], db = eb - ob;
+    for (int64_t e = e0; e < e1; ++e) {
+      const int32_t a = P.adj[ob + (e - e0)];
+      if (!edge_needed(P, e, a, (int32_t)b)) continue;
+      const int64_t ia0 = P.off[a], ea = P.off[a + 1];
+      const int64_t da = ea - ia0;
+      const int64_t cmax = da - 1;
+      bool res;
+      if (!is_similar(cmax, da, db, P.eps)) { res = false; lc.bound++; }
+      else if (is_similar(0, da, db, P.eps)) { res = true; lc.bound++; }
+      else {
+        const int64_t cmin = c_min_exact(da, db, cmax, P.eps);
+        int64_t c = 0, ia = ia0, ib = ob;
+        res = false;
+        while (ia < ea && ib < eb) {
+          const int32_t x = P.adj[ia], y = P.adj[ib];
+          if (x == y) { ++c; ++ia; ++ib; }
+          else if (x < y) ++ia;
+          else ++ib;
+          if (c >= cmin) { res = true; break; }
+          if (c + (ea - ia) < cmin) break;
+        }
+        lc.probes += (unsigned long long)(ia - ia0);
+        lc.inters++;
+        lc.bytes += 4ull * (unsigned long long)(da + db);
       }
-      lc.probes += (unsigned long long)(ia - ia0);
-      lc.inters++;
-      lc.bytes += 4ull * (unsigned long long)(da + db);
+      record_edge(P, e, a, (int32_t)b, res, true, lc);
     }
-    record_edge(P, e, a, b, res, true, lc);
   }
   flush_ctr(P, lc);
 }
@@ -161,13 +167,35 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t elo_id, i
 // ---------------------------------------------------------------------------
 // CTA per high endpoint b with a hash table of N(b)
 
+// Bucketed open addressing: T buckets of 4 keys (16 B).  A key hashes to a
+// bucket; inserters claim the bucket's slots in order 0..3 with atomicCAS and
+// spill to the next bucket only when all four are taken, so slots fill as a
+// prefix and a bucket whose last slot is empty ends a miss.  One 16-byte
+// load answers almost every probe (load <= 0.55 keys/slot), which keeps the
+// 32 lanes of a warp in lock-step instead of waiting for the longest
+// linear-probing chain.
+__device__ __forceinline__ void bucket_insert(uint32_t* tab, uint32_t T, uint32_t w) {
+  uint32_t h = hslot(w, T);
+  for (;;) {
+    uint32_t* bk = tab + 4 * h;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const uint32_t old = atomicCAS(&bk[s], kEmpty, w);
+      if (old == kEmpty || old == w) return;
+    }
+    h = (h + 1 == T) ? 0 : h + 1;
+  }
+}
+
 template <bool GTAB>
 __device__ __forceinline__ bool probe(const uint32_t* __restrict__ tab, uint32_t T, uint32_t w) {
   uint32_t h = hslot(w, T);
   for (;;) {
-    const uint32_t x = tab[h];
-    if (x == w) return true;
-    if (x == kEmpty) return false;
+    // L2-resident tables are written with atomics at L2: bypass L1 (.cg)
+    const uint4 q = GTAB ? __ldcg(reinterpret_cast<const uint4*>(tab) + h)
+                         : reinterpret_cast<const uint4*>(tab)[h];
+    if (q.x == w || q.y == w || q.z == w || q.w == w) return true;
+    if (q.w == kEmpty) return false;
     h = (h + 1 == T) ? 0 : h + 1;
   }
 }
@@ -177,8 +205,10 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
                                                  uint32_t tcap, int qi, int chunk) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* table = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : smem;
-  int32_t* surv_j = reinterpret_cast<int32_t*>(smem + (GTAB ? 0 : tcap));
-  int32_t* surv_c = surv_j + chunk;
+  // survivors of the O(1) filter: where N(a) starts, (a, deg a), (j, c_min)
+  int64_t* surv_oa = reinterpret_cast<int64_t*>(smem + (GTAB ? 0 : 4 * (size_t)tcap));
+  int2* surv_ad = reinterpret_cast<int2*>(surv_oa + chunk);
+  int2* surv_jc = surv_ad + chunk;
   __shared__ int s_item, s_nsurv, s_next;
   __shared__ unsigned int s_bsim, s_bdis;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -191,7 +221,7 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
     if (b < rlo) break;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
-    uint32_t T = (uint32_t)(2 * db + 1);
+    uint32_t T = (uint32_t)(db / 2 + 1);  // buckets: <= 0.5 keys per slot
     if (T > tcap) T = tcap;
     bool built = false;
     for (int64_t base = 0; base < nlow; base += chunk) {
@@ -203,7 +233,8 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
         const int64_t e = e0 + j;
         const int32_t a = P.adj[ob + j];
         if (!edge_needed(P, e, a, (int32_t)b)) continue;
-        const int64_t da = P.off[a + 1] - P.off[a];
+        const int64_t oa = P.off[a];
+        const int64_t da = P.off[a + 1] - oa;
         const int64_t cmax = da - 1;
         if (!is_similar(cmax, da, db, P.eps)) {
           lc.bound++;
@@ -215,25 +246,19 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
           atomicAdd(&s_bsim, 1u);
         } else {
           const int slot = atomicAdd(&s_nsurv, 1);
-          surv_j[slot] = (int32_t)j;
-          surv_c[slot] = (int32_t)c_min_exact(da, db, cmax, P.eps);
+          surv_oa[slot] = oa;
+          surv_ad[slot] = make_int2(a, (int32_t)da);
+          surv_jc[slot] = make_int2((int32_t)j, (int32_t)c_min_exact(da, db, cmax, P.eps));
         }
       }
       __syncthreads();
       const int ns = s_nsurv;
       if (ns > 0) {
         if (!built) {  // stage N(b) once per b
-          for (uint32_t i = tid; i < T; i += NT) table[i] = kEmpty;
+          for (uint32_t i = tid; i < T; i += NT)
+            reinterpret_cast<uint4*>(table)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncthreads();
-          for (int64_t i = tid; i < db; i += NT) {
-            const uint32_t w = (uint32_t)P.adj[ob + i];
-            uint32_t h = hslot(w, T);
-            for (;;) {
-              const uint32_t old = atomicCAS(&table[h], kEmpty, w);
-              if (old == kEmpty || old == w) break;
-              h = (h + 1 == T) ? 0 : h + 1;
-            }
-          }
+          for (int64_t i = tid; i < db; i += NT) bucket_insert(table, T, (uint32_t)P.adj[ob + i]);
           __syncthreads();
           built = true;
           if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
@@ -244,11 +269,13 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
           if (lane == 0) s = atomicAdd(&s_next, 1);
           s = __shfl_sync(0xffffffffu, s, 0);
           if (s >= ns) break;
-          const int64_t j = surv_j[s];
-          const int32_t cmin = surv_c[s];
-          const int32_t a = P.adj[ob + j];
-          const int64_t oa = P.off[a], da = P.off[a + 1] - oa;
-          const int32_t* __restrict__ na = P.adj + oa;
+          const int2 jc = surv_jc[s];
+          const int2 ad = surv_ad[s];
+          const int64_t j = jc.x;
+          const int32_t cmin = jc.y;
+          const int32_t a = ad.x;
+          const int64_t da = ad.y;
+          const int32_t* __restrict__ na = P.adj + surv_oa[s];
           int32_t c = 0;
           int64_t scanned = 0;
           bool res = false;
@@ -295,7 +322,7 @@ template <int NT, bool GTAB, int U>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
                        uint32_t tcap, int qi, int chunk) {
   if (rhi <= rlo) return GS_OK;
-  const size_t smem = (GTAB ? 0 : (size_t)tcap * 4) + (size_t)chunk * 8;
+  const size_t smem = (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
   auto kern = k_sim_hash<NT, GTAB, U>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -336,24 +363,22 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   // huge b first (longest work items), with an L2-resident table per CTA
   const int64_t rhuge = rc[4];
   if (g.n > rhuge) {
-    const int64_t tcap_g = 2 * g.dmax + 1;
+    const int64_t tcap_g = g.dmax / 2 + 1;  // buckets
     const int64_t nblk = (int64_t)e->sms * 2;
-    GS_TRY(e->alloc_n(&P.gtab, tcap_g * nblk));
-    P.gtab_stride = tcap_g;
+    GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
+    P.gtab_stride = 4 * tcap_g;
     GS_TRY((launch_hash<1024, true, 4>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024)));
   }
-  GS_TRY((launch_hash<1024, false, 4>(e, P, rc[3], rc[4], 52224, 3, 1024)));
-  GS_TRY((launch_hash<256, false, 2>(e, P, rc[2], rc[3], 8192, 2, 1024)));
-  GS_TRY((launch_hash<128, false, 1>(e, P, rc[1], rc[2], 1024, 1, 512)));
-  const int64_t et0 = 0;  // edges owned by degree-0 vertices: none
-  int64_t et1 = 0;
-  GS_CUDA(cudaMemcpyAsync(&et1, g.eoff + rc[1], sizeof(int64_t), cudaMemcpyDeviceToHost,
-                          e->stream));
-  GS_CUDA(cudaStreamSynchronize(e->stream));
-  if (et1 > et0) {
-    int64_t grid = (et1 - et0 + 255) / 256;
+  // table capacities in 16-byte buckets: large 12544 (196 KB, <= 0.572
+  // keys/slot for deg < 28672), medium 2048 (32 KB), small 256 (4 KB);
+  // survivor lists take 24 B per candidate of a chunk
+  GS_TRY((launch_hash<1024, false, 4>(e, P, rc[3], rc[4], 12544, 3, 1024)));
+  GS_TRY((launch_hash<256, false, 4>(e, P, rc[2], rc[3], 2048, 2, 512)));
+  GS_TRY((launch_hash<128, false, 2>(e, P, rc[1], rc[2], 256, 1, 512)));
+  if (rc[1] > rc[0]) {
+    int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
-    k_sim_tiny<<<(unsigned)grid, 256, 0, e->stream>>>(P, et0, et1);
+    k_sim_tiny<<<(unsigned)grid, 256, 0, e->stream>>>(P, rc[0], rc[1]);
     e->launches++;
     GS_CUDA(cudaGetLastError());
   }
