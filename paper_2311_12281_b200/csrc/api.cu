@@ -56,19 +56,40 @@ static int check_eps(const gs_eps2* p) {
 
 using namespace gs;
 
+// Engine allocations are cached: a released block goes to a size-keyed free
+// list and the next request of a similar size reuses it, so repeated calls
+// (the same build + scan sequence every time) never touch the driver
+// allocator.  With an HBM cap the cached blocks count against it and are
+// trimmed first when a request would exceed it.
 int gs_engine::alloc(void** p, size_t bytes) {
   *p = nullptr;
   if (bytes == 0) bytes = 1;
-  bytes = (bytes + 255) & ~size_t(255);
-  if (cap && live + bytes > cap) {
+  bytes = (bytes + 511) & ~size_t(511);
+  auto it = cache.lower_bound(bytes);
+  if (it != cache.end() && it->first <= bytes + bytes / 4 + (1u << 20)) {
+    *p = it->second;
+    const size_t sz = it->first;
+    cache.erase(it);
+    sizes[*p] = sz;
+    live += sz;
+    if (live > peak) peak = live;
+    return GS_OK;
+  }
+  if (cap && reserved + bytes > cap) trim(bytes);
+  if (cap && reserved + bytes > cap) {
     char buf[256];
     snprintf(buf, sizeof(buf),
-             "device allocation of %zu bytes exceeds the HBM cap (%llu live of %llu)", bytes,
+             "device allocation of %zu bytes exceeds the HBM cap (%llu in use of %llu)", bytes,
              (unsigned long long)live, (unsigned long long)cap);
     set_error(buf);
     return GS_EBUDGET;
   }
   cudaError_t err = cudaMallocAsync(p, bytes, stream);
+  if (err == cudaErrorMemoryAllocation && !cache.empty()) {
+    cudaGetLastError();
+    trim(SIZE_MAX);
+    err = cudaMallocAsync(p, bytes, stream);
+  }
   if (err != cudaSuccess) {
     set_error(cuda_msg(err, "cudaMallocAsync", __FILE__, __LINE__));
     *p = nullptr;
@@ -76,6 +97,7 @@ int gs_engine::alloc(void** p, size_t bytes) {
   }
   sizes[*p] = bytes;
   live += bytes;
+  reserved += bytes;
   if (live > peak) peak = live;
   return GS_OK;
 }
@@ -83,11 +105,22 @@ int gs_engine::alloc(void** p, size_t bytes) {
 void gs_engine::release(void* p) {
   if (!p) return;
   auto it = sizes.find(p);
-  if (it != sizes.end()) {
-    live -= it->second;
-    sizes.erase(it);
+  if (it == sizes.end()) return;
+  live -= it->second;
+  cache.emplace(it->second, p);
+  sizes.erase(it);
+}
+
+void gs_engine::trim(size_t need) {
+  size_t freed = 0;
+  while (!cache.empty() && (need == SIZE_MAX || freed < need || (cap && reserved + need > cap))) {
+    auto it = std::prev(cache.end());  // largest first
+    cudaFreeAsync(it->second, stream);
+    reserved -= it->first;
+    freed += it->first;
+    cache.erase(it);
   }
-  cudaFreeAsync(p, stream);
+  cudaStreamSynchronize(stream);
 }
 
 void gs_engine::free_graph() {
@@ -150,6 +183,7 @@ void gs_engine_destroy(gs_engine* e) {
   e->free_state();
   e->free_graph();
   for (auto& kv : e->sizes) cudaFreeAsync(kv.first, e->stream);
+  for (auto& kv : e->cache) cudaFreeAsync(kv.second, e->stream);
   cudaStreamSynchronize(e->stream);
   cudaStreamDestroy(e->stream);
   delete e;

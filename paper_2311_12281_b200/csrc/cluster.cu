@@ -49,10 +49,17 @@ __global__ void k_resolve(int64_t n, int32_t mu, const uint64_t* __restrict__ bo
 
 // singletons: every core is its own tree (scan.py:725-727)
 __global__ void k_singletons(int64_t n, const uint8_t* __restrict__ role,
-                             int32_t* __restrict__ parent) {
+                             int32_t* __restrict__ parent, unsigned long long* __restrict__ ctr) {
+  unsigned long long cores = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    parent[v] = role[v] == ROLE_CORE ? (int32_t)v : -1;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const bool core = role[v] == ROLE_CORE;
+    parent[v] = core ? (int32_t)v : -1;
+    cores += core;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cores += __shfl_xor_sync(0xffffffffu, cores, o);
+  if ((threadIdx.x & 31) == 0 && cores) atomicAdd(&ctr[CTR_CORES_PRE], cores);
 }
 
 __device__ __forceinline__ int32_t uf_find_h(int32_t* parent, int32_t x) {
@@ -317,34 +324,45 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
   }
   tm.mark();  // 2
   // ---- phase 2: detect clusters (Alg. 3)
+  unsigned long long ncores = 0;
   if (n > 0) {
-    k_singletons<<<gv, T, 0, str>>>(n, s.role, s.parent);
+    k_singletons<<<gv, T, 0, str>>>(n, s.role, s.parent, s.ctr);
     e->launches++;
+    GS_CUDA(cudaMemcpyAsync(&ncores, s.ctr + CTR_CORES_PRE, sizeof(ncores),
+                            cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
   }
-  if (m > 0) {
-    k_union_known<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.parent, s.ctr);
-    e->launches++;
-  }
-  GS_TRY(run_similarity(e, MODE_UNION, eps, mu));
-  if (n > 0) {
+  if (ncores > 0) {  // no core, no cluster: the union / attach passes have no edge
+    if (m > 0) {
+      k_union_known<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.parent, s.ctr);
+      e->launches++;
+    }
+    GS_TRY(run_similarity(e, MODE_UNION, eps, mu));
     k_flatten<<<gv, T, 0, str>>>(n, s.role, s.parent, g.orig, s.label, s.ctr);
-    k_core_labels<<<gv, T, 0, str>>>(n, s.role, s.parent, s.label, s.lmin, s.lmax);
-    e->launches += 2;
-  }
-  GS_TRY(run_similarity(e, MODE_ATTACH, eps, mu));
-  if (m > 0) {
-    k_attach<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax);
     e->launches++;
+  }
+  if (n > 0) {
+    k_core_labels<<<gv, T, 0, str>>>(n, s.role, s.parent, s.label, s.lmin, s.lmax);
+    e->launches++;
+  }
+  if (ncores > 0) {
+    GS_TRY(run_similarity(e, MODE_ATTACH, eps, mu));
+    if (m > 0) {
+      k_attach<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax);
+      e->launches++;
+    }
   }
   tm.mark();  // 3
   // ---- phase 3: hubs and outliers (Alg. 4)
-  const int64_t rsplit = g.rclass[1];
+  const int64_t rsplit = ncores > 0 ? g.rclass[1] : 0;
+  if (ncores == 0 && n > 0)  // nothing is clustered: every vertex is an outlier
+    GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
   if (rsplit > 0) {
     k_classify_thread<<<(unsigned)std::min<int64_t>(grid_for(rsplit, T), (int64_t)e->sms * 32),
                         T, 0, str>>>(0, rsplit, g.off, g.adj, s.role, s.lmin, s.lmax, fin);
     e->launches++;
   }
-  if (n > rsplit) {
+  if (ncores > 0 && n > rsplit) {
     const int64_t nwarps = n - rsplit;
     k_classify_warp<<<(unsigned)std::min<int64_t>(grid_for(nwarps * 32, T), (int64_t)e->sms * 32),
                       T, 0, str>>>(rsplit, n, g.off, g.adj, s.role, s.lmin, s.lmax, fin);

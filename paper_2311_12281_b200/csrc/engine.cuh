@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <unordered_map>
 #include <vector>
 
@@ -68,6 +69,7 @@ enum Ctr {
   CTR_N_HUB,
   CTR_N_OUTLIER,
   CTR_N_CLUSTERS,
+  CTR_CORES_PRE,
   CTR_COUNT
 };
 
@@ -103,8 +105,11 @@ struct gs_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint64_t cap = 0;
-  size_t live = 0, peak = 0;
-  std::unordered_map<void*, size_t> sizes;
+  size_t live = 0, peak = 0;  // bytes in use (peak = high-water mark)
+  size_t reserved = 0;        // bytes held: in use + cached free blocks
+  std::unordered_map<void*, size_t> sizes;   // in-use blocks
+  std::multimap<size_t, void*> cache;         // free blocks by size, reused by alloc
+  void trim(size_t need);                     // free cached blocks until `need` fits
   gs::DevGraph g;
   gs::DevState s;
   int sms = 148;

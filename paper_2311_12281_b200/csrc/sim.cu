@@ -14,6 +14,8 @@
 // stops as soon as c >= c_min or c + remaining < c_min (exact, c_min is
 // computed with the integer predicate).  Progressive pruning (Lemma 1): in
 // MODE_IDENTIFY an edge whose endpoints both have a decided role is skipped.
+#include <algorithm>
+
 #include "engine.cuh"
 
 namespace gs {
@@ -167,52 +169,139 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
 // ---------------------------------------------------------------------------
 // CTA per high endpoint b with a hash table of N(b)
 
-// Bucketed open addressing: T buckets of 4 keys (16 B).  A key hashes to a
-// bucket; inserters claim the bucket's slots in order 0..3 with atomicCAS and
-// spill to the next bucket only when all four are taken, so slots fill as a
-// prefix and a bucket whose last slot is empty ends a miss.  One 16-byte
-// load answers almost every probe (load <= 0.55 keys/slot), which keeps the
-// 32 lanes of a warp in lock-step instead of waiting for the longest
-// linear-probing chain.
-__device__ __forceinline__ void bucket_insert(uint32_t* tab, uint32_t T, uint32_t w) {
-  uint32_t h = hslot(w, T);
-  for (;;) {
-    uint32_t* bk = tab + 4 * h;
+// Two-choice bucketed cuckoo table: T buckets of 4 keys (16 B).  Every key
+// lives in one of its two buckets h1(w), h2(w), so a lookup is exactly two
+// independent 16-byte loads and eight compares -- no probe loop, so the 32
+// lanes of a warp never wait for the longest chain.  The CTA builds it in
+// parallel: claim an empty slot with atomicCAS in either bucket, otherwise
+// atomicExch a resident key out and re-home it in its other bucket.  A key
+// still homeless after kMaxKicks goes to a small shared stash; if the stash
+// overflows the b is marked and lookups fall back to binary search of N(b)
+// (exact, never taken at the load factors used here, <= 0.6 keys/slot).
+static constexpr int kMaxKicks = 64;
+static constexpr int kStash = 32;
+
+struct Cuckoo {
+  uint32_t* tab;      // 4*T words (shared or global)
+  uint32_t T;
+  int* nstash;        // shared
+  uint32_t* stash;    // shared [kStash]
+};
+
+__device__ __forceinline__ uint32_t h1_of(uint32_t x, uint32_t T) { return __umulhi(x, T); }
+__device__ __forceinline__ uint32_t h2_of(uint32_t x, uint32_t T) {
+  return __umulhi(x * 0x85EBCA6Bu ^ (x >> 15), T);
+}
+
+__device__ __forceinline__ void cuckoo_insert(const Cuckoo& C, uint32_t w) {
+  uint32_t key = w;
+  uint32_t x = key * 0x9E3779B1u;
+  uint32_t h = h1_of(x, C.T);
+  for (int kick = 0; kick < kMaxKicks; ++kick) {
+    const uint32_t ha = h1_of(x, C.T), hb = h2_of(x, C.T);
+    const uint32_t alt = (h == ha) ? hb : ha;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const uint32_t old = atomicCAS(&bk[s], kEmpty, w);
-      if (old == kEmpty || old == w) return;
+    for (int pass = 0; pass < 2; ++pass) {
+      uint32_t* bk = C.tab + 4 * (pass == 0 ? h : alt);
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (atomicCAS(&bk[s], kEmpty, key) == kEmpty) return;
     }
-    h = (h + 1 == T) ? 0 : h + 1;
+    // both buckets full: displace a resident of `alt` and re-home it
+    const uint32_t victim = atomicExch(&C.tab[4 * alt + (kick & 3)], key);
+    if (victim == kEmpty) return;
+    key = victim;
+    x = key * 0x9E3779B1u;
+    const uint32_t va = h1_of(x, C.T), vb = h2_of(x, C.T);
+    h = (alt == va) ? vb : va;  // the victim's other bucket
   }
+  const int i = atomicAdd(C.nstash, 1);
+  if (i < kStash) C.stash[i] = key;
 }
 
 template <bool GTAB>
-__device__ __forceinline__ bool probe(const uint32_t* __restrict__ tab, uint32_t T, uint32_t w) {
-  uint32_t h = hslot(w, T);
-  for (;;) {
-    // L2-resident tables are written with atomics at L2: bypass L1 (.cg)
-    const uint4 q = GTAB ? __ldcg(reinterpret_cast<const uint4*>(tab) + h)
-                         : reinterpret_cast<const uint4*>(tab)[h];
-    if (q.x == w || q.y == w || q.z == w || q.w == w) return true;
-    if (q.w == kEmpty) return false;
-    h = (h + 1 == T) ? 0 : h + 1;
+__device__ __forceinline__ bool cuckoo_find(const Cuckoo& C, uint32_t w, int nstash,
+                                            const int32_t* __restrict__ nb, int64_t db) {
+  const uint32_t x = w * 0x9E3779B1u;
+  const uint4* t4 = reinterpret_cast<const uint4*>(C.tab);
+  const uint32_t ha = h1_of(x, C.T), hb = h2_of(x, C.T);
+  // L2-resident tables are written with atomics at L2: bypass L1 (.cg)
+  const uint4 p = GTAB ? __ldcg(t4 + ha) : t4[ha];
+  const uint4 q = GTAB ? __ldcg(t4 + hb) : t4[hb];
+  bool hit = (p.x == w) | (p.y == w) | (p.z == w) | (p.w == w) | (q.x == w) | (q.y == w) |
+             (q.z == w) | (q.w == w);
+  if (nstash > 0) {  // CTA-uniform
+    if (nstash <= kStash) {
+      for (int i = 0; i < nstash; ++i) hit |= (C.stash[i] == w);
+    } else {  // stash overflow: exact binary search of sorted N(b)
+      int64_t lo = 0, hi = db;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint32_t)nb[mid] < w) lo = mid + 1; else hi = mid;
+      }
+      hit = lo < db && (uint32_t)nb[lo] == w;
+    }
   }
+  return hit;
 }
 
-template <int NT, bool GTAB, int U>
-__global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64_t rhi,
-                                                 uint32_t tcap, int qi, int chunk) {
+// Per-b O(1) thresholds (exact): with cmax = deg(a) - 1,
+//   dissimilar without intersecting  iff (da+1) q <  p (db+1)  iff da + 1 < xmin_b
+//   similar without intersecting     iff 4 q >= p (da+1)(db+1)  iff da <= simmax_b
+__device__ __forceinline__ void b_thresholds(int64_t db, const Eps2& e, int64_t& xmin,
+                                             int64_t& simmax) {
+  double est = e.ratio * (double)(db + 1);
+  int64_t x = (int64_t)est;
+  if (x < 1) x = 1;
+  while (x > 1 && pred_ge((uint64_t)(x - 1), (uint64_t)(db + 1), e)) --x;
+  while (!pred_ge((uint64_t)x, (uint64_t)(db + 1), e)) ++x;
+  xmin = x;
+  double es = 4.0 / (e.ratio * (double)(db + 1)) - 1.0;
+  int64_t d = es < 0 ? -1 : (int64_t)(es > 4e18 ? 4e18 : es);
+  if (d > (int64_t)1 << 40) d = (int64_t)1 << 40;
+  while (d >= 0 && !pred_ge(4, (uint64_t)(d + 1) * (uint64_t)(db + 1), e)) --d;
+  while (pred_ge(4, (uint64_t)(d + 2) * (uint64_t)(db + 1), e) && d < ((int64_t)1 << 40)) ++d;
+  simmax = d;
+}
+
+// Membership structure for N(b), per CTA:
+//   * a direct-mapped bitmap over the top R ranks [hub_lo, n) in shared
+//     memory: the high-degree vertices hold almost every element a warp
+//     scans (N(a) is walked from its high-rank end), one LDS + bit test each
+//   * a two-choice cuckoo table for the rest of N(b)
+template <bool GTAB>
+__device__ __forceinline__ bool member(const uint32_t* bm, uint32_t hub_lo, const Cuckoo& C,
+                                       uint32_t w, int nstash, const int32_t* __restrict__ nb,
+                                       int64_t nlo) {
+  if (w >= hub_lo) {
+    const uint32_t r = w - hub_lo;
+    return (bm[r >> 5] >> (r & 31)) & 1u;
+  }
+  return cuckoo_find<GTAB>(C, w, nstash, nb, nlo);
+}
+
+template <int NT, bool GTAB>
+__global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_hash(SimParams P, int64_t rlo, int64_t rhi,
+                                                 uint32_t tcap, int qi, int chunk,
+                                                 uint32_t hub_lo, uint32_t bm_words) {
   extern __shared__ __align__(16) uint32_t smem[];
-  uint32_t* table = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : smem;
+  uint32_t* bm = smem;  // [bm_words] + zero guard words (kept 16-byte aligned)
+  uint32_t* tab_s = smem + bm_words + 4;
   // survivors of the O(1) filter: where N(a) starts, (a, deg a), (j, c_min)
-  int64_t* surv_oa = reinterpret_cast<int64_t*>(smem + (GTAB ? 0 : 4 * (size_t)tcap));
+  int64_t* surv_oa = reinterpret_cast<int64_t*>(tab_s + (GTAB ? 0 : 4 * (size_t)tcap));
   int2* surv_ad = reinterpret_cast<int2*>(surv_oa + chunk);
   int2* surv_jc = surv_ad + chunk;
-  __shared__ int s_item, s_nsurv, s_next;
+  __shared__ int s_item, s_nsurv, s_next, s_nstash;
   __shared__ unsigned int s_bsim, s_bdis;
+  __shared__ int64_t s_nlo;
+  __shared__ uint32_t s_stash[kStash];
   const int tid = threadIdx.x, lane = tid & 31;
   LocalCtr lc;
+  Cuckoo C;
+  C.tab = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : tab_s;
+  C.nstash = &s_nstash;
+  C.stash = s_stash;
+  for (uint32_t i = tid; i < bm_words + 4; i += NT) bm[i] = 0u;
 
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&P.wq[qi], 1);
@@ -221,8 +310,9 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
     if (b < rlo) break;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
-    uint32_t T = (uint32_t)(db / 2 + 1);  // buckets: <= 0.5 keys per slot
-    if (T > tcap) T = tcap;
+    const int32_t* __restrict__ nb = P.adj + ob;
+    int64_t xmin, simmax;
+    b_thresholds(db, P.eps, xmin, simmax);
     bool built = false;
     for (int64_t base = 0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
@@ -231,16 +321,15 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
       // filter + O(1) bounds, one candidate a per thread
       for (int64_t j = base + tid; j < lim; j += NT) {
         const int64_t e = e0 + j;
-        const int32_t a = P.adj[ob + j];
+        const int32_t a = nb[j];
         if (!edge_needed(P, e, a, (int32_t)b)) continue;
         const int64_t oa = P.off[a];
         const int64_t da = P.off[a + 1] - oa;
-        const int64_t cmax = da - 1;
-        if (!is_similar(cmax, da, db, P.eps)) {
+        if (da + 1 < xmin) {
           lc.bound++;
           record_edge(P, e, a, (int32_t)b, false, false, lc);
           atomicAdd(&s_bdis, 1u);
-        } else if (is_similar(0, da, db, P.eps)) {
+        } else if (da <= simmax) {
           lc.bound++;
           record_edge(P, e, a, (int32_t)b, true, false, lc);
           atomicAdd(&s_bsim, 1u);
@@ -248,22 +337,54 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
           const int slot = atomicAdd(&s_nsurv, 1);
           surv_oa[slot] = oa;
           surv_ad[slot] = make_int2(a, (int32_t)da);
-          surv_jc[slot] = make_int2((int32_t)j, (int32_t)c_min_exact(da, db, cmax, P.eps));
+          surv_jc[slot] = make_int2((int32_t)j, (int32_t)c_min_exact(da, db, da - 1, P.eps));
         }
       }
       __syncthreads();
       const int ns = s_nsurv;
       if (ns > 0) {
-        if (!built) {  // stage N(b) once per b
-          for (uint32_t i = tid; i < T; i += NT)
-            reinterpret_cast<uint4*>(table)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        if (!built) {  // stage N(b) once per b: hub suffix -> bitmap, rest -> cuckoo
+          if (tid == 0) {
+            int64_t l = 0, h = db;
+            while (l < h) {
+              const int64_t mid = (l + h) >> 1;
+              if ((uint32_t)nb[mid] < hub_lo) l = mid + 1; else h = mid;
+            }
+            s_nlo = l;
+            s_nstash = 0;
+          }
           __syncthreads();
-          for (int64_t i = tid; i < db; i += NT) bucket_insert(table, T, (uint32_t)P.adj[ob + i]);
+          const int64_t nlo = s_nlo;
+          uint32_t T = (uint32_t)((nlo * 5) / 12 + 1);  // <= 0.6 keys per slot
+          if (T > tcap) T = tcap;
+          C.T = T;
+          for (uint32_t i = tid; i < T; i += NT)
+              reinterpret_cast<uint4*>(C.tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          __syncthreads();
+          for (int64_t i = tid; i < db; i += NT) {
+            const uint32_t w = (uint32_t)nb[i];
+            if (i >= nlo) {
+              const uint32_t r = w - hub_lo;
+              atomicOr(&bm[r >> 5], 1u << (r & 31));
+            } else {
+              cuckoo_insert(C, w);
+            }
+          }
           __syncthreads();
           built = true;
           if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
         }
-        // one warp per surviving a, dynamic
+        const int nstash = s_nstash;
+        const int64_t nlo = s_nlo;
+        // one warp per surviving a, dynamic.  N(a) is walked from its
+        // high-rank end (hubs first).  The first step covers 32 elements --
+        // a survivor near the degree bound is rejected after one or two
+        // misses -- later steps 128 (4 coalesced loads per lane); the next
+        // step is prefetched only when this one cannot decide the edge.
+        // Steps whose elements all lie in the hub range (warp vote) take a
+        // branch-free bitmap path; past-the-end slots hold a sentinel >= n
+        // that lands on an always-zero bitmap word.
+        const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
         for (;;) {
           int s = 0;
           if (lane == 0) s = atomicAdd(&s_next, 1);
@@ -271,35 +392,65 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
           if (s >= ns) break;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
-          const int64_t j = jc.x;
           const int32_t cmin = jc.y;
-          const int32_t a = ad.x;
-          const int64_t da = ad.y;
-          const int32_t* __restrict__ na = P.adj + surv_oa[s];
-          int32_t c = 0;
-          int64_t scanned = 0;
+          const int32_t da = ad.y;
+          const int32_t* __restrict__ na = P.adj + surv_oa[s] + (da - 1);  // walk downwards
+          const int32_t need_miss = da - cmin + 1;  // misses that decide "dissimilar"
+          constexpr uint32_t kPast = 0x7fffffffu;   // sentinel, >= n
+          uint32_t cur[4], nxt[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
+          if (lane < da) cur[0] = (uint32_t)__ldg(na - lane);
+          int32_t cu = 1;  // loads per lane in the current step
+          int32_t c = 0, scanned = 0;
           bool res = false;
-          for (int64_t k0 = 0;; k0 += 32 * U) {
-            int32_t w[U];
+          for (;;) {
+            const int32_t wstep = min(32 * cu, da - scanned);
+            const int32_t nbase = scanned + wstep;
+            const bool pre = (cmin - c > wstep) && (need_miss - (scanned - c) > wstep) &&
+                             (nbase < da);
+            if (pre) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const int64_t idx = k0 + u * 32 + lane;
-              w[u] = idx < da ? __ldg(na + idx) : -1;
+              for (int u = 0; u < 4; ++u) {
+                const int32_t idx = nbase + u * 32 + lane;
+                nxt[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+              }
             }
+            const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
+            uint32_t hits = 0;
+            if (__all_sync(0xffffffffu, lo4 >= hub_lo)) {  // bitmap only, branch-free
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-              const bool hit = w[u] >= 0 && probe<GTAB>(table, T, (uint32_t)w[u]);
-              c += __popc(__ballot_sync(0xffffffffu, hit));
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t r = min(cur[u] - hub_lo, rmax);
+                hits += (bm[r >> 5] >> (r & 31)) & 1u;
+              }
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (cur[u] != kPast)
+                  hits += member<GTAB>(bm, hub_lo, C, cur[u], nstash, nb, nlo);
             }
-            scanned = k0 + 32 * U < da ? k0 + 32 * U : da;
+            c += (int32_t)__reduce_add_sync(0xffffffffu, hits);
+            scanned = nbase;
             if (c >= cmin) { res = true; break; }
-            if ((int64_t)c + (da - scanned) < cmin) { res = false; break; }
+            if (c + (da - scanned) < cmin) { res = false; break; }
+            if (pre) {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+            } else {
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int32_t idx = scanned + u * 32 + lane;
+                cur[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+              }
+            }
+            cu = 4;
           }
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
             lc.inters++;
             lc.bytes += 4ull * (unsigned long long)da;
-            record_edge(P, e0 + j, a, (int32_t)b, res, false, lc);
+            record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
           }
         }
@@ -310,7 +461,10 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
         apply_bounds(P.bounds, P.role, b, s_bsim, s_bdis, P.mu);
       __syncthreads();
     }
-    __syncthreads();  // everyone has read s_item before it is rewritten
+    if (built) {  // clear the bitmap words this b set (O(deg b), not O(R))
+      for (int64_t i = s_nlo + tid; i < db; i += NT) bm[((uint32_t)nb[i] - hub_lo) >> 5] = 0u;
+    }
+    __syncthreads();  // bitmap clean and s_item read by all before the next b
   }
   flush_ctr(P, lc);
 }
@@ -318,12 +472,18 @@ __global__ void __launch_bounds__(NT) k_sim_hash(SimParams P, int64_t rlo, int64
 // ---------------------------------------------------------------------------
 // host driver
 
-template <int NT, bool GTAB, int U>
+template <int NT, bool GTAB>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
-                       uint32_t tcap, int qi, int chunk) {
+                       uint32_t tcap, int qi, int chunk, uint32_t bm_bits) {
   if (rhi <= rlo) return GS_OK;
-  const size_t smem = (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
-  auto kern = k_sim_hash<NT, GTAB, U>;
+  // bitmap over the top bm_bits ranks (bm_bits a multiple of 32, <= n rounded up)
+  const int64_t n = e->g.n;
+  uint32_t bits = (uint32_t)std::min<int64_t>(bm_bits, ((n + 31) / 32) * 32);
+  const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, n - (int64_t)bits);
+  const uint32_t bm_words = (uint32_t)((n - hub_lo + 31) / 32);  // + 1 zero guard word
+  const size_t smem =
+      (size_t)(bm_words + 4) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
+  auto kern = k_sim_hash<NT, GTAB>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -331,7 +491,7 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   int64_t grid = (int64_t)occ * e->sms;
   if (grid > rhi - rlo) grid = rhi - rlo;
   if (GTAB && grid > e->sms * 2) grid = e->sms * 2;
-  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk);
+  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk, hub_lo, bm_words);
   e->launches++;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
@@ -363,18 +523,18 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   // huge b first (longest work items), with an L2-resident table per CTA
   const int64_t rhuge = rc[4];
   if (g.n > rhuge) {
-    const int64_t tcap_g = g.dmax / 2 + 1;  // buckets
+    const int64_t tcap_g = (g.dmax * 5) / 12 + 1;  // buckets
     const int64_t nblk = (int64_t)e->sms * 2;
     GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
     P.gtab_stride = 4 * tcap_g;
-    GS_TRY((launch_hash<1024, true, 4>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024)));
+    GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, 1u << 18)));
   }
-  // table capacities in 16-byte buckets: large 12544 (196 KB, <= 0.572
-  // keys/slot for deg < 28672), medium 2048 (32 KB), small 256 (4 KB);
-  // survivor lists take 24 B per candidate of a chunk
-  GS_TRY((launch_hash<1024, false, 4>(e, P, rc[3], rc[4], 12544, 3, 1024)));
-  GS_TRY((launch_hash<256, false, 4>(e, P, rc[2], rc[3], 2048, 2, 512)));
-  GS_TRY((launch_hash<128, false, 2>(e, P, rc[1], rc[2], 256, 1, 512)));
+  // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB; small class
+  // 2^16: 8 KB) + cuckoo table for the non-hub part of N(b) (16-byte buckets)
+  // + survivor lists (24 B per candidate of a chunk)
+  GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, 1u << 18)));
+  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 512, 1u << 18)));
+  GS_TRY((launch_hash<128, false>(e, P, rc[1], rc[2], 256, 1, 512, 1u << 16)));
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;

@@ -98,6 +98,7 @@ int main(int argc, char** argv) {
   for (int ie = 0; ie < 6; ie += 3) {
     double e2 = epss[ie] * epss[ie];
     double full = 0, asc = 0, desc = 0, sims = 0, tot = 0;
+    double hubfrac[4] = {0}, hubscan[4] = {0};
     for (int64_t t = 0; t < nsamp; ) {
       int64_t slot = xr() % (2 * m);
       int64_t lo = 0, hi = n;  // owner of slot: last v with off[v] <= slot
@@ -130,10 +131,23 @@ int main(int argc, char** argv) {
       cc = 0;
       for (i = 0; i < da; ++i) { cc += hit[da - 1 - i]; if (cc >= cmin || cc + (da - 1 - i) < cmin) { ++i; break; } }
       desc += i;
+      for (int r = 0; r < 4; ++r) {
+        int64_t lo_rank = n - (n >> (5 + r));   /* top n/32, n/64, n/128, n/256 */
+        int64_t inreg = 0, sc = 0; cc = 0;
+        for (i = 0; i < da; ++i) {
+          int32_t w = adj[off[a] + da - 1 - i];
+          inreg += (w >= lo_rank); ++sc;
+          cc += hit[da - 1 - i];
+          if (cc >= cmin || cc + (da - 1 - i) < cmin) break;
+        }
+        hubfrac[r] += inreg; hubscan[r] += sc;
+      }
       free(hit);
     }
     printf("eps %.1f sampled %lld intersect-edges: similar %.1f%%, mean da %.1f, early-exit asc %.1f%% desc %.1f%% of elements\n",
            epss[ie], (long long)nsamp, 100 * sims / tot, full / tot, 100 * asc / full, 100 * desc / full);
+    for (int r = 0; r < 4; ++r)
+      printf("   scanned elements (desc) inside top n/%d ranks: %.1f%%\n", 32 << r, 100 * hubfrac[r] / hubscan[r]);
   }
   return 0;
 }
