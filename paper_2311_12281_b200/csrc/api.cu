@@ -144,6 +144,8 @@ void gs_engine::free_state() {
   release(s.lmax);
   release(s.ctr);
   release(s.wq);
+  release(s.thr);
+  release(s.nlo);
   s = DevState();
 }
 

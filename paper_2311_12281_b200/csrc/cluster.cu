@@ -298,6 +298,7 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     e->launches++;
   }
   // ---- phase 1: identify cores (Alg. 2)
+  GS_TRY(prepare_similarity(e, eps));
   GS_TRY(run_similarity(e, MODE_IDENTIFY, eps, mu));
   tm.mark();  // 1
   // ---- cleanup (scan.py:415-449): resolve from bounds; re-evaluate if open

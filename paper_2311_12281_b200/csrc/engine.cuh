@@ -53,6 +53,8 @@ struct DevState {
   int32_t* lmin = nullptr;      // [n] min cluster label per clustered vertex
   int32_t* lmax = nullptr;      // [n] max cluster label per clustered vertex
   unsigned long long* ctr = nullptr;  // device counters (see Ctr)
+  int2* thr = nullptr;          // [dmax+1] per-degree O(1) thresholds for this epsilon
+  int32_t* nlo = nullptr;       // [n] hub split of each adjacency run
   int32_t* wq = nullptr;        // work-queue heads for persistent kernels
 };
 
@@ -94,6 +96,10 @@ struct SimParams {
   int32_t* wq;
   uint32_t* gtab;  // global hash scratch for very large lists
   int64_t gtab_stride;
+  const int2* thr;      // per degree d of b: {xmin, simmax} O(1) bounds (see sim.cu)
+  const int32_t* nlo;   // per vertex: neighbours below hub_lo (the non-hub prefix)
+  uint32_t hub_lo;      // first rank of the hub bitmap range
+  uint32_t bm_words;    // hub bitmap words (range [hub_lo, n))
   Eps2 eps;
   int32_t mu;
   int mode;
@@ -136,6 +142,7 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
                    const int32_t* adj_dev);
 // sim.cu
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
+int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split
 // cluster.cu
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
              int32_t* cluster_out, int out_on_device, gs_stats* st);

@@ -264,6 +264,32 @@ __device__ __forceinline__ void b_thresholds(int64_t db, const Eps2& e, int64_t&
   simmax = d;
 }
 
+// per-degree table of the O(1) thresholds, computed once per scan
+__global__ void k_thresholds(int64_t dmax, Eps2 e, int2* __restrict__ thr) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d <= dmax;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    int64_t xmin, simmax;
+    b_thresholds(d, e, xmin, simmax);
+    thr[d] = make_int2((int32_t)(xmin > 0x7fffffff ? 0x7fffffff : xmin),
+                       (int32_t)(simmax > 0x7fffffff ? 0x7fffffff : simmax));
+  }
+}
+
+// per-vertex split of the adjacency run at hub_lo (runs are sorted)
+__global__ void k_hubsplit(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                           int64_t n, uint32_t hub_lo, int32_t* __restrict__ nlo) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t l = off[v], h = off[v + 1];
+    const int64_t lo0 = l;
+    while (l < h) {
+      const int64_t mid = (l + h) >> 1;
+      if ((uint32_t)adj[mid] < hub_lo) l = mid + 1; else h = mid;
+    }
+    nlo[v] = (int32_t)(l - lo0);
+  }
+}
+
 // Membership structure for N(b), per CTA:
 //   * a direct-mapped bitmap over the top R ranks [hub_lo, n) in shared
 //     memory: the high-degree vertices hold almost every element a warp
@@ -278,6 +304,72 @@ __device__ __forceinline__ bool member(const uint32_t* bm, uint32_t hub_lo, cons
     return (bm[r >> 5] >> (r & 31)) & 1u;
   }
   return cuckoo_find<GTAB>(C, w, nstash, nb, nlo);
+}
+
+// Decide one surviving edge (a, b): a warp walks N(a) from its high-rank
+// end (hubs first).  The first step covers 32 elements -- a survivor near the
+// degree bound is rejected after one or two misses -- later steps 128 (4
+// coalesced loads per lane); the next step is prefetched only when this one
+// cannot decide the edge.  Steps whose elements all lie in the hub range
+// (warp vote) take a branch-free bitmap path; past-the-end slots hold a
+// sentinel >= n that lands on an always-zero bitmap guard word.
+template <bool GTAB>
+__device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run, int32_t da,
+                                              int32_t cmin, const uint32_t* bm, uint32_t hub_lo,
+                                              uint32_t rmax, const Cuckoo& C, int nstash,
+                                              const int32_t* __restrict__ nb, int64_t nlo,
+                                              int lane, int32_t& scanned) {
+  const int32_t* __restrict__ na = a_run + (da - 1);  // walk downwards
+  const int32_t need_miss = da - cmin + 1;            // misses that decide "dissimilar"
+  constexpr uint32_t kPast = 0x7fffffffu;             // sentinel, >= n
+  uint32_t cur[4], nxt[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
+  if (lane < da) cur[0] = (uint32_t)__ldg(na - lane);
+  int32_t cu = 1;  // loads per lane in the current step
+  int32_t c = 0;
+  scanned = 0;
+  for (;;) {
+    const int32_t wstep = min(32 * cu, da - scanned);
+    const int32_t nbase = scanned + wstep;
+    const bool pre =
+        (cmin - c > wstep) && (need_miss - (scanned - c) > wstep) && (nbase < da);
+    if (pre) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t idx = nbase + u * 32 + lane;
+        nxt[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+      }
+    }
+    const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
+    uint32_t hits = 0;
+    if (__all_sync(0xffffffffu, lo4 >= hub_lo)) {  // bitmap only, branch-free
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = min(cur[u] - hub_lo, rmax);
+        hits += (bm[r >> 5] >> (r & 31)) & 1u;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (cur[u] != kPast) hits += member<GTAB>(bm, hub_lo, C, cur[u], nstash, nb, nlo);
+    }
+    c += (int32_t)__reduce_add_sync(0xffffffffu, hits);
+    scanned = nbase;
+    if (c >= cmin) return true;
+    if (c + (da - scanned) < cmin) return false;
+    if (pre) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t idx = scanned + u * 32 + lane;
+        cur[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+      }
+    }
+    cu = 4;
+  }
 }
 
 template <int NT, bool GTAB>
@@ -311,8 +403,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
     const int32_t* __restrict__ nb = P.adj + ob;
-    int64_t xmin, simmax;
-    b_thresholds(db, P.eps, xmin, simmax);
+    const int2 th = P.thr[db];
+    const int64_t xmin = th.x, simmax = th.y;
     bool built = false;
     for (int64_t base = 0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
@@ -345,12 +437,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       if (ns > 0) {
         if (!built) {  // stage N(b) once per b: hub suffix -> bitmap, rest -> cuckoo
           if (tid == 0) {
-            int64_t l = 0, h = db;
-            while (l < h) {
-              const int64_t mid = (l + h) >> 1;
-              if ((uint32_t)nb[mid] < hub_lo) l = mid + 1; else h = mid;
-            }
-            s_nlo = l;
+            s_nlo = P.nlo[b];
             s_nstash = 0;
           }
           __syncthreads();
@@ -376,15 +463,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
         }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
-        // one warp per surviving a, dynamic.  N(a) is walked from its
-        // high-rank end (hubs first).  The first step covers 32 elements --
-        // a survivor near the degree bound is rejected after one or two
-        // misses -- later steps 128 (4 coalesced loads per lane); the next
-        // step is prefetched only when this one cannot decide the edge.
-        // Steps whose elements all lie in the hub range (warp vote) take a
-        // branch-free bitmap path; past-the-end slots hold a sentinel >= n
-        // that lands on an always-zero bitmap word.
         const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
+        // one warp per surviving a, dynamic (scan_survivor)
         for (;;) {
           int s = 0;
           if (lane == 0) s = atomicAdd(&s_next, 1);
@@ -392,64 +472,13 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           if (s >= ns) break;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
-          const int32_t cmin = jc.y;
-          const int32_t da = ad.y;
-          const int32_t* __restrict__ na = P.adj + surv_oa[s] + (da - 1);  // walk downwards
-          const int32_t need_miss = da - cmin + 1;  // misses that decide "dissimilar"
-          constexpr uint32_t kPast = 0x7fffffffu;   // sentinel, >= n
-          uint32_t cur[4], nxt[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
-          if (lane < da) cur[0] = (uint32_t)__ldg(na - lane);
-          int32_t cu = 1;  // loads per lane in the current step
-          int32_t c = 0, scanned = 0;
-          bool res = false;
-          for (;;) {
-            const int32_t wstep = min(32 * cu, da - scanned);
-            const int32_t nbase = scanned + wstep;
-            const bool pre = (cmin - c > wstep) && (need_miss - (scanned - c) > wstep) &&
-                             (nbase < da);
-            if (pre) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int32_t idx = nbase + u * 32 + lane;
-                nxt[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
-              }
-            }
-            const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
-            uint32_t hits = 0;
-            if (__all_sync(0xffffffffu, lo4 >= hub_lo)) {  // bitmap only, branch-free
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const uint32_t r = min(cur[u] - hub_lo, rmax);
-                hits += (bm[r >> 5] >> (r & 31)) & 1u;
-              }
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-                if (cur[u] != kPast)
-                  hits += member<GTAB>(bm, hub_lo, C, cur[u], nstash, nb, nlo);
-            }
-            c += (int32_t)__reduce_add_sync(0xffffffffu, hits);
-            scanned = nbase;
-            if (c >= cmin) { res = true; break; }
-            if (c + (da - scanned) < cmin) { res = false; break; }
-            if (pre) {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
-            } else {
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                const int32_t idx = scanned + u * 32 + lane;
-                cur[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
-              }
-            }
-            cu = 4;
-          }
+          int32_t scanned;
+          const bool res = scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo, rmax,
+                                               C, nstash, nb, nlo, lane, scanned);
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
             lc.inters++;
-            lc.bytes += 4ull * (unsigned long long)da;
+            lc.bytes += 4ull * (unsigned long long)ad.y;
             record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
           }
@@ -470,19 +499,110 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
 }
 
 // ---------------------------------------------------------------------------
+// small b (64 <= deg < 512): one warp per b, no CTA barriers.  Each warp owns
+// a private cuckoo table of N(b) in shared memory; the 32 lanes filter 32
+// candidates at a time (O(1) bounds), and the surviving edges are decided one
+// by one by the whole warp with scan_survivor (data broadcast by shuffles).
+static constexpr int kWarpBuckets = 256;  // 4 KB: deg < 512 -> <= 0.5 keys per slot
+static constexpr int kWarpWords = 4 * kWarpBuckets + kStash + 4;
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int64_t rlo,
+                                                               int64_t rhi, int qi) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* tab = smem + (size_t)wid * kWarpWords;
+  Cuckoo C;
+  C.tab = tab;
+  C.stash = tab + 4 * kWarpBuckets;
+  C.nstash = reinterpret_cast<int*>(C.stash + kStash);
+  LocalCtr lc;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    const int64_t b = rhi - 1 - (int64_t)item;
+    if (b < rlo) break;
+    const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
+    const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
+    const int32_t* __restrict__ nb = P.adj + ob;
+    const int2 th = P.thr[db];
+    bool built = false;
+    uint32_t bsim = 0, bdis = 0;
+    for (int64_t base = 0; base < nlow; base += 32) {
+      const int64_t j = base + lane;
+      int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
+      int32_t a = 0, da = 0, cmin = 0;
+      int64_t oa = 0;
+      if (j < nlow) {
+        a = nb[j];
+        if (edge_needed(P, e0 + j, a, (int32_t)b)) {
+          oa = P.off[a];
+          da = (int32_t)(P.off[a + 1] - oa);
+          if (da + 1 < th.x) st = 1;
+          else if (da <= th.y) st = 2;
+          else {
+            st = 3;
+            cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
+          }
+          if (st == 1 || st == 2) {
+            lc.bound++;
+            record_edge(P, e0 + j, a, (int32_t)b, st == 2, false, lc);
+          }
+        }
+      }
+      bdis += __popc(__ballot_sync(0xffffffffu, st == 1));
+      bsim += __popc(__ballot_sync(0xffffffffu, st == 2));
+      uint32_t smask = __ballot_sync(0xffffffffu, st == 3);
+      if (smask && !built) {  // stage N(b) once per b, warp-private
+        uint32_t T = (uint32_t)((db * 5) / 12 + 1);
+        if (T > kWarpBuckets) T = kWarpBuckets;
+        C.T = T;
+        for (uint32_t i = lane; i < T; i += 32)
+          reinterpret_cast<uint4*>(tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+        if (lane == 0) *C.nstash = 0;
+        __syncwarp();
+        for (int64_t i = lane; i < db; i += 32) cuckoo_insert(C, (uint32_t)nb[i]);
+        __syncwarp();
+        built = true;
+        if (lane == 0) lc.bytes += 4ull * (unsigned long long)db;
+      }
+      const int nstash = built ? *C.nstash : 0;
+      while (smask) {
+        const int src = __ffs(smask) - 1;
+        smask &= smask - 1;
+        const int32_t sa = __shfl_sync(0xffffffffu, a, src);
+        const int32_t sda = __shfl_sync(0xffffffffu, da, src);
+        const int32_t scm = __shfl_sync(0xffffffffu, cmin, src);
+        const int64_t soa = __shfl_sync(0xffffffffu, oa, src);
+        int32_t scanned;
+        const bool res = scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu, 0, C,
+                                              nstash, nb, db, lane, scanned);
+        if (res) ++bsim; else ++bdis;
+        if (lane == 0) {
+          lc.probes += (unsigned long long)scanned;
+          lc.inters++;
+          lc.bytes += 4ull * (unsigned long long)sda;
+          record_edge(P, e0 + base + src, sa, (int32_t)b, res, false, lc);
+        }
+      }
+    }
+    if (lane == 0 && (bsim | bdis) && (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP))
+      apply_bounds(P.bounds, P.role, b, bsim, bdis, P.mu);
+    __syncwarp();
+  }
+  flush_ctr(P, lc);
+}
+
+// ---------------------------------------------------------------------------
 // host driver
 
 template <int NT, bool GTAB>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
-                       uint32_t tcap, int qi, int chunk, uint32_t bm_bits) {
+                       uint32_t tcap, int qi, int chunk) {
   if (rhi <= rlo) return GS_OK;
-  // bitmap over the top bm_bits ranks (bm_bits a multiple of 32, <= n rounded up)
-  const int64_t n = e->g.n;
-  uint32_t bits = (uint32_t)std::min<int64_t>(bm_bits, ((n + 31) / 32) * 32);
-  const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, n - (int64_t)bits);
-  const uint32_t bm_words = (uint32_t)((n - hub_lo + 31) / 32);  // + 1 zero guard word
   const size_t smem =
-      (size_t)(bm_words + 4) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
+      (size_t)(P.bm_words + 4) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
   auto kern = k_sim_hash<NT, GTAB>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -491,8 +611,46 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   int64_t grid = (int64_t)occ * e->sms;
   if (grid > rhi - rlo) grid = rhi - rlo;
   if (GTAB && grid > e->sms * 2) grid = e->sms * 2;
-  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk, hub_lo, bm_words);
+  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk, P.hub_lo,
+                                                P.bm_words);
   e->launches++;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi, int qi) {
+  if (rhi <= rlo) return GS_OK;
+  constexpr int NT = 256;
+  const size_t smem = (size_t)(NT / 32) * kWarpWords * 4;
+  auto kern = k_sim_warp<NT>;
+  GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)occ * e->sms;
+  const int64_t nw = (rhi - rlo + NT / 32 - 1) / (NT / 32);
+  if (grid > nw) grid = nw;
+  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, qi);
+  e->launches++;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+// hub bitmap range: the top 2^18 ranks (32 KB of shared memory per CTA)
+static constexpr int64_t kHubBits = 1 << 18;
+
+int prepare_similarity(gs_engine* e, const Eps2& eps) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  GS_TRY(e->alloc_n(&s.thr, g.dmax + 1));
+  GS_TRY(e->alloc_n(&s.nlo, g.n));
+  k_thresholds<<<grid_for(g.dmax + 1, 256), 256, 0, e->stream>>>(g.dmax, eps, s.thr);
+  const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
+  const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
+  if (g.n > 0) {
+    k_hubsplit<<<grid_for(g.n, 256), 256, 0, e->stream>>>(g.off, g.adj, g.n, hub_lo, s.nlo);
+    e->launches += 2;
+  }
   GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
@@ -518,6 +676,13 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.mode = mode;
   P.gtab = nullptr;
   P.gtab_stride = 0;
+  P.thr = s.thr;
+  P.nlo = s.nlo;
+  {
+    const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
+    P.hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
+    P.bm_words = (uint32_t)((g.n - P.hub_lo + 31) / 32);
+  }
   GS_CUDA(cudaMemsetAsync(s.wq, 0, 8 * sizeof(int32_t), e->stream));
   const int64_t* rc = g.rclass;
   // huge b first (longest work items), with an L2-resident table per CTA
@@ -527,14 +692,14 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     const int64_t nblk = (int64_t)e->sms * 2;
     GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
     P.gtab_stride = 4 * tcap_g;
-    GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, 1u << 18)));
+    GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024)));
   }
-  // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB; small class
-  // 2^16: 8 KB) + cuckoo table for the non-hub part of N(b) (16-byte buckets)
-  // + survivor lists (24 B per candidate of a chunk)
-  GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, 1u << 18)));
-  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 512, 1u << 18)));
-  GS_TRY((launch_hash<128, false>(e, P, rc[1], rc[2], 256, 1, 512, 1u << 16)));
+  // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB) + cuckoo table
+  // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
+  // per candidate of a chunk); the small class runs warp-per-b
+  GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024)));
+  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024)));
+  GS_TRY(launch_warp(e, P, rc[1], rc[2], 1));
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
