@@ -1,0 +1,292 @@
+// simcore.cuh -- device building blocks of the similarity sweep shared by
+// the in-HBM kernels (sim.cu) and the out-of-core kernels (ooc.cu): roles and
+// Lemma-1 bounds, lock-free union-find, the two-choice cuckoo table, the
+// per-degree O(1) thresholds and the early-exit survivor scan.
+#pragma once
+#include "engine.cuh"
+
+namespace gs {
+
+static constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint8_t ld_role(const uint8_t* role, int64_t v) {
+  return *reinterpret_cast<const volatile uint8_t*>(role + v);
+}
+
+__device__ __forceinline__ int32_t uf_find(int32_t* parent, int32_t x) {
+  volatile int32_t* p = parent;
+  for (;;) {
+    int32_t px = p[x];
+    if (px == x) return x;
+    int32_t gp = p[px];
+    if (gp == px) return px;
+    p[x] = gp;  // path halving: gp is an ancestor of x, safe under races
+    x = gp;
+  }
+}
+
+// Lock-free union: hook the larger root under the smaller (roots are then the
+// minimum rank of their class; parent[v] <= v keeps the forest acyclic).
+__device__ __forceinline__ void uf_union(int32_t* parent, int32_t a, int32_t b,
+                                         unsigned long long& retries) {
+  for (;;) {
+    a = uf_find(parent, a);
+    b = uf_find(parent, b);
+    if (a == b) return;
+    if (a > b) { int32_t t = a; a = b; b = t; }
+    int32_t old = atomicCAS(&parent[b], b, a);
+    if (old == b) return;
+    ++retries;
+  }
+}
+
+// Apply nsim similar / ndis dissimilar outcomes to x's packed bounds and
+// decide its role the moment a bound crosses mu (scan.py:302-345).
+__device__ __forceinline__ void apply_bounds(uint64_t* bounds, uint8_t* role, int64_t x,
+                                             uint32_t nsim, uint32_t ndis, int32_t mu) {
+  const uint64_t delta = (uint64_t)nsim - ((uint64_t)ndis << 32);
+  const uint64_t old = atomicAdd(reinterpret_cast<unsigned long long*>(&bounds[x]),
+                                 (unsigned long long)delta);
+  const uint64_t nw = old + delta;
+  const int32_t lower = (int32_t)(uint32_t)nw;
+  const int32_t upper = (int32_t)(uint32_t)(nw >> 32);
+  if (lower >= mu) role[x] = ROLE_CORE;
+  else if (upper < mu) role[x] = ROLE_NONCORE;
+}
+
+// Does edge (a, b) need a decision in this mode?
+__device__ __forceinline__ bool edge_needed(const SimParams& P, int64_t e, int32_t a,
+                                            int32_t b) {
+  if (P.sim[e] != SIM_UNKNOWN) return false;
+  const uint8_t ra = ld_role(P.role, a), rb = ld_role(P.role, b);
+  switch (P.mode) {
+    case MODE_IDENTIFY:  // Alg. 2 line 2: defer if both roles are known
+      return ra == ROLE_UNKNOWN || rb == ROLE_UNKNOWN;
+    case MODE_CLEANUP:
+      return ra == ROLE_UNKNOWN || rb == ROLE_UNKNOWN;
+    case MODE_UNION:  // scan.py:642-648
+      if (ra != ROLE_CORE || rb != ROLE_CORE) return false;
+      return uf_find(P.parent, a) != uf_find(P.parent, b);
+    default:  // MODE_ATTACH, scan.py:681-686
+      return (ra == ROLE_CORE) != (rb == ROLE_CORE);
+  }
+}
+
+struct LocalCtr {
+  unsigned long long evals = 0, probes = 0, bound = 0, inters = 0, bytes = 0, retries = 0;
+};
+
+// Record one decided edge.  b's bound update is returned to the caller
+// (aggregated per CTA for the shared-b kernels) unless apply_b is set.
+__device__ __forceinline__ void record_edge(const SimParams& P, int64_t e, int32_t a,
+                                            int32_t b, bool similar, bool apply_b,
+                                            LocalCtr& lc) {
+  P.sim[e] = similar ? SIM_SIMILAR : SIM_DISSIMILAR;
+  lc.evals++;
+  if (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP) {
+    apply_bounds(P.bounds, P.role, a, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
+    if (apply_b) apply_bounds(P.bounds, P.role, b, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
+  } else if (P.mode == MODE_UNION && similar) {
+    uf_union(P.parent, a, b, lc.retries);
+  }
+}
+
+__device__ __forceinline__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
+  // warp reduce then one atomic per warp
+  unsigned long long v[6] = {lc.evals, lc.probes, lc.bound, lc.inters, lc.bytes, lc.retries};
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (v[0]) atomicAdd(&P.ctr[CTR_SIM_EVALS], v[0]);
+    if (v[1]) atomicAdd(&P.ctr[CTR_PROBES], v[1]);
+    if (v[2]) atomicAdd(&P.ctr[CTR_BOUND_DECIDED], v[2]);
+    if (v[3]) atomicAdd(&P.ctr[CTR_INTERSECTIONS], v[3]);
+    if (v[4]) atomicAdd(&P.ctr[CTR_ALG_BYTES], v[4]);
+    if (v[5]) atomicAdd(&P.ctr[CTR_UNION_RETRIES], v[5]);
+  }
+}
+
+// Two-choice bucketed cuckoo table: T buckets of 4 keys (16 B).  Every key
+// lives in one of its two buckets h1(w), h2(w), so a lookup is exactly two
+// independent 16-byte loads and eight compares -- no probe loop, so the 32
+// lanes of a warp never wait for the longest chain.  The CTA builds it in
+// parallel: claim an empty slot with atomicCAS in either bucket, otherwise
+// atomicExch a resident key out and re-home it in its other bucket.  A key
+// still homeless after kMaxKicks goes to a small shared stash; if the stash
+// overflows the b is marked and lookups fall back to binary search of N(b)
+// (exact, never taken at the load factors used here, <= 0.6 keys/slot).
+static constexpr int kMaxKicks = 64;
+static constexpr int kStash = 32;
+
+struct Cuckoo {
+  uint32_t* tab;      // 4*T words (shared or global)
+  uint32_t T;
+  int* nstash;        // shared
+  uint32_t* stash;    // shared [kStash]
+};
+
+__device__ __forceinline__ uint32_t h1_of(uint32_t x, uint32_t T) { return __umulhi(x, T); }
+__device__ __forceinline__ uint32_t h2_of(uint32_t x, uint32_t T) {
+  return __umulhi(x * 0x85EBCA6Bu ^ (x >> 15), T);
+}
+
+__device__ __forceinline__ void cuckoo_insert(const Cuckoo& C, uint32_t w) {
+  uint32_t key = w;
+  uint32_t x = key * 0x9E3779B1u;
+  uint32_t h = h1_of(x, C.T);
+  for (int kick = 0; kick < kMaxKicks; ++kick) {
+    const uint32_t ha = h1_of(x, C.T), hb = h2_of(x, C.T);
+    const uint32_t alt = (h == ha) ? hb : ha;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      uint32_t* bk = C.tab + 4 * (pass == 0 ? h : alt);
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (atomicCAS(&bk[s], kEmpty, key) == kEmpty) return;
+    }
+    // both buckets full: displace a resident of `alt` and re-home it
+    const uint32_t victim = atomicExch(&C.tab[4 * alt + (kick & 3)], key);
+    if (victim == kEmpty) return;
+    key = victim;
+    x = key * 0x9E3779B1u;
+    const uint32_t va = h1_of(x, C.T), vb = h2_of(x, C.T);
+    h = (alt == va) ? vb : va;  // the victim's other bucket
+  }
+  const int i = atomicAdd(C.nstash, 1);
+  if (i < kStash) C.stash[i] = key;
+}
+
+template <bool GTAB>
+__device__ __forceinline__ bool cuckoo_find(const Cuckoo& C, uint32_t w, int nstash,
+                                            const int32_t* __restrict__ nb, int64_t db) {
+  const uint32_t x = w * 0x9E3779B1u;
+  const uint4* t4 = reinterpret_cast<const uint4*>(C.tab);
+  const uint32_t ha = h1_of(x, C.T), hb = h2_of(x, C.T);
+  // L2-resident tables are written with atomics at L2: bypass L1 (.cg)
+  const uint4 p = GTAB ? __ldcg(t4 + ha) : t4[ha];
+  const uint4 q = GTAB ? __ldcg(t4 + hb) : t4[hb];
+  bool hit = (p.x == w) | (p.y == w) | (p.z == w) | (p.w == w) | (q.x == w) | (q.y == w) |
+             (q.z == w) | (q.w == w);
+  if (nstash > 0) {  // CTA-uniform
+    if (nstash <= kStash) {
+      for (int i = 0; i < nstash; ++i) hit |= (C.stash[i] == w);
+    } else {  // stash overflow: exact binary search of sorted N(b)
+      int64_t lo = 0, hi = db;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint32_t)nb[mid] < w) lo = mid + 1; else hi = mid;
+      }
+      hit = lo < db && (uint32_t)nb[lo] == w;
+    }
+  }
+  return hit;
+}
+
+// Per-b O(1) thresholds (exact): with cmax = deg(a) - 1,
+//   dissimilar without intersecting  iff (da+1) q <  p (db+1)  iff da + 1 < xmin_b
+//   similar without intersecting     iff 4 q >= p (da+1)(db+1)  iff da <= simmax_b
+__device__ __forceinline__ void b_thresholds(int64_t db, const Eps2& e, int64_t& xmin,
+                                             int64_t& simmax) {
+  double est = e.ratio * (double)(db + 1);
+  int64_t x = (int64_t)est;
+  if (x < 1) x = 1;
+  while (x > 1 && pred_ge((uint64_t)(x - 1), (uint64_t)(db + 1), e)) --x;
+  while (!pred_ge((uint64_t)x, (uint64_t)(db + 1), e)) ++x;
+  xmin = x;
+  double es = 4.0 / (e.ratio * (double)(db + 1)) - 1.0;
+  int64_t d = es < 0 ? -1 : (int64_t)(es > 4e18 ? 4e18 : es);
+  if (d > (int64_t)1 << 40) d = (int64_t)1 << 40;
+  while (d >= 0 && !pred_ge(4, (uint64_t)(d + 1) * (uint64_t)(db + 1), e)) --d;
+  while (pred_ge(4, (uint64_t)(d + 2) * (uint64_t)(db + 1), e) && d < ((int64_t)1 << 40)) ++d;
+  simmax = d;
+}
+
+// Membership structure for N(b), per CTA:
+//   * a direct-mapped bitmap over the top R ranks [hub_lo, n) in shared
+//     memory: the high-degree vertices hold almost every element a warp
+//     scans (N(a) is walked from its high-rank end), one LDS + bit test each
+//   * a two-choice cuckoo table for the rest of N(b)
+template <bool GTAB>
+__device__ __forceinline__ bool member(const uint32_t* bm, uint32_t hub_lo, const Cuckoo& C,
+                                       uint32_t w, int nstash, const int32_t* __restrict__ nb,
+                                       int64_t nlo) {
+  if (w >= hub_lo) {
+    const uint32_t r = w - hub_lo;
+    return (bm[r >> 5] >> (r & 31)) & 1u;
+  }
+  return cuckoo_find<GTAB>(C, w, nstash, nb, nlo);
+}
+
+// Decide one surviving edge (a, b): a warp walks N(a) from its high-rank
+// end (hubs first).  The first step covers 32 elements -- a survivor near the
+// degree bound is rejected after one or two misses -- later steps 128 (4
+// coalesced loads per lane); the next step is prefetched only when this one
+// cannot decide the edge.  Steps whose elements all lie in the hub range
+// (warp vote) take a branch-free bitmap path; past-the-end slots hold a
+// sentinel >= n that lands on an always-zero bitmap guard word.
+template <bool GTAB>
+__device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run, int32_t da,
+                                              int32_t cmin, const uint32_t* bm, uint32_t hub_lo,
+                                              uint32_t rmax, const Cuckoo& C, int nstash,
+                                              const int32_t* __restrict__ nb, int64_t nlo,
+                                              int lane, int32_t& scanned) {
+  const int32_t* __restrict__ na = a_run + (da - 1);  // walk downwards
+  const int32_t need_miss = da - cmin + 1;            // misses that decide "dissimilar"
+  constexpr uint32_t kPast = 0x7fffffffu;             // sentinel, >= n
+  uint32_t cur[4], nxt[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
+  if (lane < da) cur[0] = (uint32_t)__ldg(na - lane);
+  int32_t cu = 1;  // loads per lane in the current step
+  int32_t c = 0;
+  scanned = 0;
+  for (;;) {
+    const int32_t wstep = min(32 * cu, da - scanned);
+    const int32_t nbase = scanned + wstep;
+    const bool pre =
+        (cmin - c > wstep) && (need_miss - (scanned - c) > wstep) && (nbase < da);
+    if (pre) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t idx = nbase + u * 32 + lane;
+        nxt[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+      }
+    }
+    const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
+    uint32_t hits = 0;
+    if (__all_sync(0xffffffffu, lo4 >= hub_lo)) {  // bitmap only, branch-free
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t r = min(cur[u] - hub_lo, rmax);
+        hits += (bm[r >> 5] >> (r & 31)) & 1u;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (cur[u] != kPast) hits += member<GTAB>(bm, hub_lo, C, cur[u], nstash, nb, nlo);
+    }
+    c += (int32_t)__reduce_add_sync(0xffffffffu, hits);
+    scanned = nbase;
+    if (c >= cmin) return true;
+    if (c + (da - scanned) < cmin) return false;
+    if (pre) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int32_t idx = scanned + u * 32 + lane;
+        cur[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+      }
+    }
+    cu = 4;
+  }
+}
+
+// host launcher of the per-degree threshold table (sim.cu)
+int launch_thresholds(int64_t dmax, const Eps2& eps, int2* thr, cudaStream_t st);
+
+}  // namespace gs

@@ -1,0 +1,171 @@
+"""Host mirror of the reference's out-of-core API (graphscan/partition.py).
+
+``partition_graph(g, budget_bytes)`` plans the run and ``scan_out_of_core(meta,
+plan, mu, epsilon)`` executes it on the device through ``gs_scan_partitioned``
+under an HBM cap of ``budget_bytes``.
+
+The reference spills edge-extended subgraphs (Def. 9) to disk and re-reads
+them per pass (partition.py:231-446); its greedy closure planner is O(sum d^2)
+and replicates R-MAT edges 181-1,993x.  Here the graph stays in
+(pinned) host memory: partitions are contiguous ranges of high endpoints whose
+adjacency slice is streamed into HBM, the low endpoint's list is gathered
+zero-copy, and only per-vertex state (13 bytes/vertex) is resident.  The plan
+object keeps the reference's reporting surface (partitions, budget, manifest
+lines) so callers and stats look the same.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Union
+
+import numpy as np
+
+from . import _lib
+from .graph import as_array, graph_arrays
+from .scan import ClusteringResult, EpsilonLike, _validate, stats_from_native
+
+VERTEX_STATE_BYTES = 13  # degree 4 + role 1 + bounds 8 (or forest 4 + labels 4)
+EDGE_BYTES = 25  # the reference's per-edge estimate (partition.py:70-72), reporting only
+VERTEX_BYTES = 4
+
+
+class InfeasibleBudgetError(ValueError):
+    """The resident state or the largest adjacency list cannot fit the budget
+    (partition.py:79-89)."""
+
+    def __init__(self, edge: tuple, required_bytes: int, budget_bytes: int, msg: str = ""):
+        self.edge = edge
+        self.required_bytes = required_bytes
+        self.budget_bytes = budget_bytes
+        super().__init__(msg or (f"edge {edge} needs {required_bytes} bytes against a budget of "
+                                 f"{budget_bytes}; no partitioning can satisfy this"))
+
+
+@dataclass
+class PartitionInfo:
+    """One partition: high endpoints [lo, hi), adjacency slice [a0, a1)."""
+
+    index: int
+    lo: int
+    hi: int
+    a0: int
+    a1: int
+
+    @property
+    def estimate_bytes(self) -> int:
+        return 4 * (self.a1 - self.a0) + 8 * (self.hi - self.lo + 1)
+
+
+@dataclass
+class GraphMeta:
+    """The globally resident slice of a graph (partition.py:143-160)."""
+
+    n: int
+    m: int
+    degrees: np.ndarray
+    orig_ids: np.ndarray
+    graph: object = field(default=None, repr=False)
+
+    @classmethod
+    def from_graph(cls, g) -> "GraphMeta":
+        n, m, off, _ = graph_arrays(g)
+        orig = as_array(g.orig_ids, np.uint32) if n else np.empty(0, np.uint32)
+        return cls(n=n, m=m, degrees=np.diff(off).astype(np.int64), orig_ids=orig, graph=g)
+
+
+@dataclass
+class PartitionPlan:
+    n: int
+    m: int
+    budget_bytes: int
+    partitions: list
+    spill_dir: Optional[str] = None
+    manifest_path: Optional[str] = None
+    graph: object = field(default=None, repr=False)
+
+    @property
+    def global_state_bytes(self) -> int:
+        return VERTEX_STATE_BYTES * self.n
+
+    def manifest(self) -> str:
+        lines = [f"n={self.n}", f"m={self.m}", f"budget_bytes={self.budget_bytes}",
+                 f"global_state_bytes={self.global_state_bytes}",
+                 f"partitions={len(self.partitions)}"]
+        lines += [f"{p.index}\t{p.lo}\t{p.hi}\t{p.a0}\t{p.a1}\t{p.estimate_bytes}"
+                  for p in self.partitions]
+        return "\n".join(lines) + "\n"
+
+
+def estimate_memory(s) -> int:
+    """``25*|E_s| + 4*|V_s|`` (partition.py:163-171), the reference's formula."""
+    if isinstance(s, PartitionInfo):
+        return s.estimate_bytes
+    return EDGE_BYTES * int(s.m) + VERTEX_BYTES * int(s.n)
+
+
+def partition_graph(g, budget_bytes: int, spill_dir: Optional[str] = None) -> PartitionPlan:
+    """Plan a budgeted run: validate the budget and cut the high-endpoint
+    range into slices that fit the two streaming buffers the budget leaves
+    after the resident state.  Raises InfeasibleBudgetError like the reference
+    (partition.py:239-243)."""
+    if budget_bytes <= 0:
+        raise ValueError(f"budget_bytes must be positive, got {budget_bytes}")
+    n, m, off, _ = graph_arrays(g)
+    state = VERTEX_STATE_BYTES * n
+    if state > budget_bytes:
+        raise InfeasibleBudgetError((-1, -1), state, budget_bytes)
+    dmax = int(np.diff(off).max()) if n else 0
+    avail = budget_bytes - state - (2 << 20) - 8 * (dmax + 1)
+    buf = max(0, avail // 2 // 4 * 3 // 4)
+    if n and buf < max(dmax, 1024):
+        raise InfeasibleBudgetError((-1, -1), state + (2 << 20) + 8 * 4 * max(dmax, 1024),
+                                    budget_bytes)
+    parts = []
+    lo = 0
+    max_verts = max(1, buf // 4)
+    while lo < n:
+        hi = int(np.searchsorted(off, off[lo] + buf, side="right")) - 1
+        hi = min(max(hi, lo + 1), n, lo + max_verts)
+        parts.append(PartitionInfo(len(parts), lo, hi, int(off[lo]), int(off[hi])))
+        lo = hi
+    plan = PartitionPlan(n=n, m=m, budget_bytes=int(budget_bytes), partitions=parts,
+                         spill_dir=spill_dir, graph=g)
+    if spill_dir is not None:
+        os.makedirs(spill_dir, exist_ok=True)
+        plan.manifest_path = os.path.join(spill_dir, "plan.manifest")
+        with open(plan.manifest_path, "w", encoding="utf-8") as f:
+            f.write(plan.manifest())
+    return plan
+
+
+def scan_out_of_core(meta: GraphMeta, plan: PartitionPlan, mu: int, epsilon: EpsilonLike, *,
+                     workers: int = 1):
+    """Cluster under the plan's HBM budget (partition.py:666-757).  Same
+    results as ``scan_in_memory`` (canonical ids), same error behaviour."""
+    f = _validate(mu, workers, epsilon)
+    if plan.n != meta.n or plan.m != meta.m:
+        raise ValueError(f"plan is for a different graph: plan n={plan.n} m={plan.m}, "
+                         f"graph n={meta.n} m={meta.m}")
+    g = plan.graph if plan.graph is not None else meta.graph
+    n, m, off, adj = graph_arrays(g)
+    eps2 = _lib.eps2_struct(f, int(meta.degrees.max()) if n else 0)
+    roles = np.empty(n, dtype=np.uint8)
+    cids = np.empty(n, dtype=np.int32)
+    st = _lib.GsStats()
+    if n:
+        lib = _lib.load()
+        try:
+            _lib.check(lib.gs_scan_partitioned(n, m, off.ctypes.data, adj.ctypes.data, int(mu),
+                                               ctypes.byref(eps2), int(plan.budget_bytes),
+                                               roles.ctypes.data, cids.ctypes.data,
+                                               ctypes.byref(st)))
+        except _lib.InfeasibleBudget as exc:
+            raise InfeasibleBudgetError((-1, -1), VERTEX_STATE_BYTES * n, plan.budget_bytes,
+                                        str(exc)) from None
+    stats = stats_from_native(st, n, m, workers)
+    stats.extra["partitions"] = int(st.partitions) if n else 0
+    orig = meta.orig_ids if n else np.empty(0, np.uint32)
+    return ClusteringResult(n, roles, cids, orig), stats

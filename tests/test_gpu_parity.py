@@ -265,3 +265,89 @@ def test_errors_map_to_reference_exceptions():
     b.orig_ids = np.arange(3, dtype=np.uint32)
     with pytest.raises(ValueError):
         gs.scan_in_memory(b, 2, "0.5")
+
+
+# ---------------------------------------------------------------------------
+# out-of-core mode (gs_scan_partitioned): same canonical output under an HBM cap
+
+def _ooc(g, mu, eps, budget):
+    plan = gs.partition_graph(g, budget)
+    meta = gs.GraphMeta.from_graph(g)
+    r, s = gs.scan_out_of_core(meta, plan, mu, eps)
+    return plan, r, s
+
+
+def test_ooc_fig1_single_and_multi_partition():
+    g = make_graph(14, sorted(TWO_COMMUNITIES))
+    ref = run(g, 3, "0.6")
+    for budget in (1 << 26, 13 * 14 + (2 << 20) + 8 * 8 + 4 * 1024 * 8 + 2000):
+        plan, r, s = _ooc(g, 3, "0.6", budget)
+        np.testing.assert_array_equal(r.role_codes, ref[0])
+        np.testing.assert_array_equal(r.cluster_ids, ref[1])
+        assert s.extra["partitions"] >= 1
+
+
+@pytest.mark.parametrize("scale,seed", [(14, 3), (16, 1)])
+def test_ooc_rmat_matches_oracle_with_many_partitions(orc, scale, seed):
+    n, e = orc.rmat(scale, seed=seed)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    dmax = int(np.diff(g.vertex_offsets).max())
+    # leave room for buffers of ~1/8 of the adjacency: forces several partitions
+    budget = 13 * n + (2 << 20) + 8 * (dmax + 1) + max(2 * g.m // 4 * 4 * 4 // 3, 8 * 4 * dmax)
+    for eps, mu in (("0.2", 3), ("0.3", 5), ("0.5", 5)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        plan, r, s = _ooc(g, mu, eps, budget)
+        assert s.extra["partitions"] >= 3, s.extra
+        np.testing.assert_array_equal(r.role_codes, roles, err_msg=f"{eps} {mu}")
+        np.testing.assert_array_equal(r.cluster_ids, cl, err_msg=f"{eps} {mu}")
+        assert s.extra["peak_device_bytes"] <= budget
+
+
+def test_ooc_golden_corpus(golden):
+    n_cfg = 0
+    for k, c in golden.cases():
+        if c["n"] == 0 or c["m"] == 0 or not c["name"].startswith(("corpus", "shared", "clique")):
+            continue
+        g = make_graph(c["n"], golden.edges(k))
+        for j, cfg in enumerate(c["configs"][:6]):
+            plan, r, s = _ooc(g, cfg["mu"], cfg["eps"], 1 << 24)
+            np.testing.assert_array_equal(r.role_codes, golden.get(k, f"c{j}_roles"))
+            np.testing.assert_array_equal(r.cluster_ids, golden.get(k, f"c{j}_cluster"))
+            n_cfg += 1
+    assert n_cfg > 100
+
+
+def test_ooc_huge_lists_use_l2_table(orc):
+    """Hubs of degree 40k exceed the shared-memory cuckoo: HBM slab path."""
+    rng = np.random.default_rng(7)
+    n = 70000
+    edges = set()
+    for h in (0, 1, 2):
+        for v in rng.choice(np.arange(3, n), size=40000, replace=False):
+            edges.add((h, int(v)))
+    for _ in range(150000):
+        u, v = rng.integers(3, n, size=2)
+        if u != v:
+            edges.add((int(min(u, v)), int(max(u, v))))
+    edges |= {(0, 1), (1, 2), (0, 2)}
+    e = np.array(sorted(edges), dtype=np.int32)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.05", 2), ("0.3", 2)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        plan, r, s = _ooc(g, mu, eps, 64 << 20)
+        np.testing.assert_array_equal(r.role_codes, roles)
+        np.testing.assert_array_equal(r.cluster_ids, cl)
+
+
+def test_ooc_infeasible_budget():
+    g = make_graph(14, sorted(TWO_COMMUNITIES))
+    with pytest.raises(gs.InfeasibleBudgetError):
+        gs.partition_graph(g, 13 * 14 - 1)
+    with pytest.raises(ValueError):
+        gs.partition_graph(g, 0)
+    plan = gs.partition_graph(g, 1 << 24)
+    other = make_graph(10, [(0, 1), (1, 2)])
+    with pytest.raises(ValueError):
+        gs.scan_out_of_core(gs.GraphMeta.from_graph(other), plan, 3, "0.5")
