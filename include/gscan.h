@@ -136,6 +136,13 @@ int gs_scan_edges(int64_t n, int64_t m, const int32_t* edges_uv, int32_t mu,
 int gs_build_graph(int64_t n, int64_t m, const int32_t* edges_uv, int64_t* offsets,
                    int32_t* adjacency, int32_t* edge_ids, int32_t* edge_list);
 
+/* build_graph's CSR part (vertex_offsets, sorted adjacency) on the device,
+ * device in / device out: edges_dev = normalised pairs, off_dev [n+1] i64,
+ * adj_dev [2m] i32.  Used to prepare very large inputs for the partitioned
+ * scan (the CSR is then copied to pinned host memory). */
+int gs_build_csr_device(int64_t n, int64_t m, const int32_t* edges_dev, int64_t* off_dev,
+                        int32_t* adj_dev, void* stream);
+
 /* check_sim for k edges (u_i, v_i) of the loaded graph: out[i] = 1 similar,
  * 0 dissimilar, -1 not an edge. */
 int gs_engine_check_sim(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,

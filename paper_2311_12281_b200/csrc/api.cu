@@ -18,7 +18,7 @@ std::string cuda_msg(cudaError_t e, const char* what, const char* file, int line
 }
 int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv_dev,
                            int64_t* off_dev, int32_t* adj_dev, int32_t* eids_dev,
-                           int32_t* elist_dev);
+                           int32_t* elist_dev, bool csr_only);
 int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t* dst,
                   cudaStream_t st);
 int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32_t* dst,
@@ -188,6 +188,10 @@ void gs_engine_destroy(gs_engine* e) {
   for (auto& kv : e->cache) cudaFreeAsync(kv.second, e->stream);
   cudaStreamSynchronize(e->stream);
   cudaStreamDestroy(e->stream);
+  // hand the pool's reserved memory back (the release threshold keeps it
+  // across calls of a live engine, not beyond its lifetime)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, e->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
   delete e;
 }
 
@@ -351,7 +355,7 @@ int gs_build_graph(int64_t n, int64_t m, const int32_t* edges_uv, int64_t* offse
     set_error("host to device copy failed");
     rc = GS_ECUDA;
   }
-  if (rc == GS_OK) rc = build_reference_layout(e, n, m, d_uv, d_off, d_adj, d_eids, d_el);
+  if (rc == GS_OK) rc = build_reference_layout(e, n, m, d_uv, d_off, d_adj, d_eids, d_el, false);
   if (rc == GS_OK) {
     cudaMemcpyAsync(offsets, d_off, 8 * (size_t)(n + 1), cudaMemcpyDeviceToHost, e->stream);
     if (m > 0) {
@@ -365,6 +369,18 @@ int gs_build_graph(int64_t n, int64_t m, const int32_t* edges_uv, int64_t* offse
       rc = GS_ECUDA;
     }
   }
+  gs_engine_destroy(e);
+  return rc;
+}
+
+int gs_build_csr_device(int64_t n, int64_t m, const int32_t* edges_dev, int64_t* off_dev,
+                        int32_t* adj_dev, void* stream) {
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  if (stream) cudaStreamSynchronize((cudaStream_t)stream);
+  int rc = load_common(e, n, m);
+  if (rc == GS_OK)
+    rc = build_reference_layout(e, n, m, edges_dev, off_dev, adj_dev, nullptr, nullptr, true);
   gs_engine_destroy(e);
   return rc;
 }

@@ -443,7 +443,7 @@ __global__ void k_orient_emit(const int64_t* __restrict__ off, int64_t n,
 
 int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv_dev,
                            int64_t* off_dev, int32_t* adj_dev, int32_t* eids_dev,
-                           int32_t* elist_dev) {
+                           int32_t* elist_dev, bool csr_only) {
   cudaStream_t st = e->stream;
   int* d_bad = nullptr;
   GS_TRY(e->alloc_n(&d_bad, 1));
@@ -486,6 +486,18 @@ int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv
   }
   e->release(keys);
   e->release(keys2);
+  if (csr_only) {
+    GS_CUDA(cudaStreamSynchronize(st));
+    int h_bad = 0;
+    GS_CUDA(cudaMemcpy(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+    e->release(d_bad);
+    if (h_bad) {
+      set_error(h_bad == 1 ? "invalid edge list: id outside [0, n) or self-loop"
+                           : "invalid edge list: duplicate undirected edge");
+      return GS_EINVAL;
+    }
+    return GS_OK;
+  }
   int64_t* flag = nullptr;
   int64_t* pos = nullptr;
   GS_TRY(e->alloc_n(&flag, slots + 1));
