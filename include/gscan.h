@@ -124,6 +124,26 @@ int gs_engine_load_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edge
 int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_out,
                    int32_t* cluster_out, int out_on_device, gs_stats* stats);
 
+/* Sharded (multi-GPU) scan, SURVEY 8(e).  Every rank loads the same graph
+ * into its engine and owns the oriented edges whose high endpoint b (in the
+ * engine's degree-rank order) satisfies b % world == rank.  The phases below
+ * are the single-GPU scan cut where a collective is needed; the host runs,
+ * between them (paper_2311_12281_b200/dist.py, NCCL via torch.distributed):
+ *   counts  [2n] i32 (similar | dissimilar per vertex)  -> all-reduce SUM
+ *   pairs   [2*npairs] i32 (core, local root)            -> all-gather (merge forests)
+ *   labels  [2n] i32 (min | max member label)            -> all-reduce MIN | MAX
+ * Device buffers are caller-owned (capacity 2n).  With world = 1 and NULL
+ * buffers the phases reproduce gs_engine_scan exactly. */
+int gs_engine_set_shard(gs_engine* e, int rank, int world);
+int gs_engine_phase_begin(gs_engine* e, int32_t mu, const gs_eps2* eps2);
+int gs_engine_phase_identify(gs_engine* e, int32_t* counts_dev);
+int gs_engine_phase_resolve(gs_engine* e, const int32_t* counts_dev, int64_t* ncores);
+int gs_engine_phase_union(gs_engine* e, int32_t* pairs_dev, int64_t* npairs);
+int gs_engine_phase_merge(gs_engine* e, const int32_t* pairs_dev, int64_t npairs);
+int gs_engine_phase_attach(gs_engine* e, int32_t* labels_dev);
+int gs_engine_phase_finish(gs_engine* e, const int32_t* labels_dev, uint8_t* role_out,
+                           int32_t* cluster_out, int out_on_device, gs_stats* stats);
+
 /* One-shot calls (temporary engine on the current device). */
 int gs_scan_csr(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
                 int32_t mu, const gs_eps2* eps2, uint8_t* role_out,

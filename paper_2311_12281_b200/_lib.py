@@ -77,6 +77,15 @@ SIGNATURES = [
     ("gs_engine_load_edges", ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int]),
     ("gs_engine_scan", ctypes.c_int,
      [_P, _I32, ctypes.POINTER(GsEps2), _P, _P, ctypes.c_int, ctypes.POINTER(GsStats)]),
+    ("gs_engine_set_shard", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),
+    ("gs_engine_phase_begin", ctypes.c_int, [_P, _I32, ctypes.POINTER(GsEps2)]),
+    ("gs_engine_phase_identify", ctypes.c_int, [_P, _P]),
+    ("gs_engine_phase_resolve", ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    ("gs_engine_phase_union", ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    ("gs_engine_phase_merge", ctypes.c_int, [_P, _P, _I64]),
+    ("gs_engine_phase_attach", ctypes.c_int, [_P, _P]),
+    ("gs_engine_phase_finish", ctypes.c_int,
+     [_P, _P, _P, _P, ctypes.c_int, ctypes.POINTER(GsStats)]),
     ("gs_scan_csr", ctypes.c_int,
      [_I64, _I64, _P, _P, _I32, ctypes.POINTER(GsEps2), _P, _P, ctypes.POINTER(GsStats)]),
     ("gs_scan_edges", ctypes.c_int,

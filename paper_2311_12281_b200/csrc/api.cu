@@ -301,6 +301,117 @@ int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_
   return rc;
 }
 
+// ---- sharded (multi-GPU) scan: phases with the collectives in between
+static int phase_guard(gs_engine* e) {
+  if (!e) { set_error("engine is NULL"); return GS_EINVAL; }
+  if (!e->g.off && e->g.n > 0) { set_error("no graph loaded"); return GS_EINVAL; }
+  GS_CUDA(cudaSetDevice(e->device));
+  return GS_OK;
+}
+
+int gs_engine_set_shard(gs_engine* e, int rank, int world) {
+  if (!e || world < 1 || rank < 0 || rank >= world) { set_error("invalid shard"); return GS_EINVAL; }
+  e->shard_rank = rank;
+  e->shard_world = world;
+  return GS_OK;
+}
+
+int gs_engine_phase_begin(gs_engine* e, int32_t mu, const gs_eps2* eps2) {
+  GS_TRY(phase_guard(e));
+  if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
+  GS_TRY(check_eps(eps2));
+  e->launches = 0;
+  for (auto& x : e->phase_ms) x = 0;
+  return timed(e, GS_PH_IDENTIFY, [&] { return phase_begin(e, mu, to_eps(eps2)); });
+}
+
+// event-timed phase call (sharded path): adds the device time to e->phase_ms[ph]
+template <class F>
+static int timed(gs_engine* e, int ph, F&& f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, e->stream);
+  int rc = f();
+  cudaEventRecord(b, e->stream);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  e->phase_ms[ph] += ms;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return rc;
+}
+
+int gs_engine_phase_identify(gs_engine* e, int32_t* counts_dev) {
+  GS_TRY(phase_guard(e));
+  GS_TRY(timed(e, GS_PH_IDENTIFY, [&] { return phase_identify(e); }));
+  if (counts_dev) GS_TRY(phase_export_counts(e, counts_dev));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  return GS_OK;
+}
+
+int gs_engine_phase_resolve(gs_engine* e, const int32_t* counts_dev, int64_t* ncores) {
+  GS_TRY(phase_guard(e));
+  if (counts_dev) GS_TRY(phase_import_counts(e, counts_dev));
+  GS_TRY(timed(e, GS_PH_CLEANUP, [&] {
+    return phase_resolve(e, counts_dev == nullptr && e->shard_world == 1);
+  }));
+  if (ncores) *ncores = (int64_t)e->ncores;
+  return GS_OK;
+}
+
+int gs_engine_phase_union(gs_engine* e, int32_t* pairs_dev, int64_t* npairs) {
+  GS_TRY(phase_guard(e));
+  GS_TRY(timed(e, GS_PH_CLUSTER, [&] { return phase_union(e); }));
+  int64_t np = 0;
+  if (pairs_dev) GS_TRY(phase_export_pairs(e, pairs_dev, &np));
+  if (npairs) *npairs = np;
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  return GS_OK;
+}
+
+int gs_engine_phase_merge(gs_engine* e, const int32_t* pairs_dev, int64_t npairs) {
+  GS_TRY(phase_guard(e));
+  GS_TRY(timed(e, GS_PH_CLUSTER, [&] {
+    int rc = pairs_dev ? phase_merge_pairs(e, pairs_dev, npairs) : GS_OK;
+    return rc == GS_OK ? phase_labels(e) : rc;
+  }));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  return GS_OK;
+}
+
+int gs_engine_phase_attach(gs_engine* e, int32_t* labels_dev) {
+  GS_TRY(phase_guard(e));
+  GS_TRY(timed(e, GS_PH_CLUSTER, [&] { return phase_attach(e); }));
+  if (labels_dev) GS_TRY(phase_export_labels(e, labels_dev));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  return GS_OK;
+}
+
+int gs_engine_phase_finish(gs_engine* e, const int32_t* labels_dev, uint8_t* role_out,
+                           int32_t* cluster_out, int out_on_device, gs_stats* stats) {
+  GS_TRY(phase_guard(e));
+  if (stats) memset(stats, 0, sizeof(*stats));
+  if (labels_dev) GS_TRY(phase_import_labels(e, labels_dev));
+  GS_TRY(timed(e, GS_PH_CLASSIFY, [&] {
+    return phase_finish(e, role_out, cluster_out, out_on_device, stats);
+  }));
+  if (stats) {
+    stats->kernel_launches = e->launches;
+    stats->peak_device_bytes = (int64_t)e->peak;
+    const double d2h = stats->phase_ms[GS_PH_D2H];
+    for (int i = 0; i < GS_PH_COUNT; ++i) stats->phase_ms[i] = e->phase_ms[i];
+    stats->phase_ms[GS_PH_D2H] = d2h;
+    stats->phase_ms[GS_PH_CLASSIFY] -= d2h;
+    stats->phase_ms[GS_PH_H2D] = e->last_h2d_ms;
+    stats->phase_ms[GS_PH_BUILD] = e->last_build_ms;
+    stats->phase_ms[GS_PH_TOTAL] = e->phase_ms[GS_PH_IDENTIFY] + e->phase_ms[GS_PH_CLEANUP] +
+                                   e->phase_ms[GS_PH_CLUSTER] + e->phase_ms[GS_PH_CLASSIFY];
+  }
+  return GS_OK;
+}
+
 int gs_scan_csr(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
                 int32_t mu, const gs_eps2* eps2, uint8_t* role_out, int32_t* cluster_out,
                 gs_stats* stats) {

@@ -9,6 +9,8 @@
 // it is eligible for; shared members (eligible for >= 2 clusters, the
 // reference's ROLE_MEMBER_SHARED) are recognised by min != max, which is the
 // exact information classify_vertex_from_neighbors needs (scan.py:794-808).
+#include <algorithm>
+
 #include "engine.cuh"
 
 namespace gs {
@@ -59,7 +61,7 @@ __global__ void k_singletons(int64_t n, const uint8_t* __restrict__ role,
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cores += __shfl_xor_sync(0xffffffffu, cores, o);
-  if ((threadIdx.x & 31) == 0 && cores) atomicAdd(&ctr[CTR_CORES_PRE], cores);
+  if (ctr && (threadIdx.x & 31) == 0 && cores) atomicAdd(&ctr[CTR_CORES_PRE], cores);
 }
 
 __device__ __forceinline__ int32_t uf_find_h(int32_t* parent, int32_t x) {
@@ -78,12 +80,13 @@ __device__ __forceinline__ int32_t uf_find_h(int32_t* parent, int32_t x) {
 __global__ void k_union_known(int64_t m, const int32_t* __restrict__ elo,
                               const int32_t* __restrict__ ehi, const uint8_t* __restrict__ sim,
                               const uint8_t* __restrict__ role, int32_t* parent,
-                              unsigned long long* __restrict__ ctr) {
+                              unsigned long long* __restrict__ ctr, int rank, int world) {
   unsigned long long retries = 0;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
        e += (int64_t)gridDim.x * blockDim.x) {
     if (sim[e] != SIM_SIMILAR) continue;
     int32_t a = elo[e], b = ehi[e];
+    if (!owns(b, rank, world)) continue;
     if (role[a] != ROLE_CORE || role[b] != ROLE_CORE) continue;
     for (;;) {
       a = uf_find_h(parent, a);
@@ -134,11 +137,12 @@ __global__ void k_core_labels(int64_t n, const uint8_t* __restrict__ role,
 __global__ void k_attach(int64_t m, const int32_t* __restrict__ elo,
                          const int32_t* __restrict__ ehi, const uint8_t* __restrict__ sim,
                          const uint8_t* __restrict__ role, int32_t* __restrict__ lmin,
-                         int32_t* __restrict__ lmax) {
+                         int32_t* __restrict__ lmax, int rank, int world) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
        e += (int64_t)gridDim.x * blockDim.x) {
     if (sim[e] != SIM_SIMILAR) continue;
     const int32_t a = elo[e], b = ehi[e];
+    if (!owns(b, rank, world)) continue;
     const bool ca = role[a] == ROLE_CORE, cb = role[b] == ROLE_CORE;
     if (ca == cb) continue;
     const int32_t core = ca ? a : b, w = ca ? b : a;
@@ -240,6 +244,65 @@ __global__ void k_output(int64_t n, const int32_t* __restrict__ orig,
 }
 
 // ---------------------------------------------------------------------------
+// exchange kernels of the sharded scan (dist.py runs the collectives)
+
+// local Lemma-1 evidence -> per-vertex counts: [0,n) similar, [n,2n) dissimilar
+__global__ void k_export_counts(int64_t n, const uint64_t* __restrict__ bounds,
+                                const int64_t* __restrict__ off, int32_t* __restrict__ cnt) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = bounds[v];
+    cnt[v] = (int32_t)(uint32_t)b - 1;
+    cnt[n + v] = (int32_t)(off[v + 1] - off[v] + 1) - (int32_t)(uint32_t)(b >> 32);
+  }
+}
+
+// summed counts of all shards -> exact global bounds (then k_resolve)
+__global__ void k_import_counts(int64_t n, const int32_t* __restrict__ cnt,
+                                const int64_t* __restrict__ off, uint64_t* __restrict__ bounds) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t lower = (uint64_t)(1 + cnt[v]);
+    const uint64_t upper = (uint64_t)(off[v + 1] - off[v] + 1 - cnt[n + v]);
+    bounds[v] = lower | (upper << 32);
+  }
+}
+
+// the local forest as (core, root) pairs, roots excluded
+__global__ void k_export_pairs(int64_t n, const uint8_t* __restrict__ role,
+                               const int32_t* __restrict__ parent, int32_t* __restrict__ pairs,
+                               unsigned long long* __restrict__ count) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (role[v] != ROLE_CORE) continue;
+    const int32_t r = uf_root(parent, (int32_t)v);
+    if (r == (int32_t)v) continue;
+    const unsigned long long i = atomicAdd(count, 1ull);
+    pairs[2 * i] = (int32_t)v;
+    pairs[2 * i + 1] = r;
+  }
+}
+
+// every shard's pairs unioned into a fresh forest: the merged components
+__global__ void k_union_pairs(int64_t np, const int32_t* __restrict__ pairs, int32_t* parent,
+                              unsigned long long* __restrict__ ctr) {
+  unsigned long long retries = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t a = pairs[2 * i], b = pairs[2 * i + 1];
+    for (;;) {
+      a = uf_find_h(parent, a);
+      b = uf_find_h(parent, b);
+      if (a == b) break;
+      if (a > b) { int32_t t = a; a = b; b = t; }
+      if (atomicCAS(&parent[b], b, a) == b) break;
+      ++retries;
+    }
+  }
+  if (retries) atomicAdd(&ctr[CTR_UNION_RETRIES], retries);
+}
+
+// ---------------------------------------------------------------------------
 
 struct PhaseTimer {
   gs_engine* e;
@@ -259,15 +322,19 @@ struct PhaseTimer {
   }
 };
 
-int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
-             int32_t* cluster_out, int out_on_device, gs_stats* st) {
+static inline unsigned gridv(gs_engine* e, int64_t n) {
+  return (unsigned)std::min<int64_t>(grid_for(n, 256), (int64_t)e->sms * 32);
+}
+
+// state, thresholds, Alg. 1 lines 1-4
+int phase_begin(gs_engine* e, int32_t mu, const Eps2& eps) {
   DevGraph& g = e->g;
   DevState& s = e->s;
   cudaStream_t str = e->stream;
   const int64_t n = g.n, m = g.m;
-  const int T = 256;
-  const unsigned gv = (unsigned)std::min<int64_t>(grid_for(n, T), (int64_t)e->sms * 32);
-  const unsigned ge = (unsigned)std::min<int64_t>(grid_for(m, T), (int64_t)e->sms * 32);
+  e->mu = mu;
+  e->eps = eps;
+  e->ncores = 0;
   e->free_state();
   GS_TRY(e->alloc_n(&s.sim, m));
   GS_TRY(e->alloc_n(&s.bounds, n));
@@ -278,6 +345,170 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
   GS_TRY(e->alloc_n(&s.lmax, n));
   GS_TRY(e->alloc_n(&s.ctr, CTR_COUNT));
   GS_TRY(e->alloc_n(&s.wq, 8));
+  GS_CUDA(cudaMemsetAsync(s.sim, 0, (size_t)(m > 0 ? m : 1), str));
+  GS_CUDA(cudaMemsetAsync(s.ctr, 0, sizeof(unsigned long long) * CTR_COUNT, str));
+  GS_CUDA(cudaMemsetAsync(s.label, 0x7f, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), str));
+  if (n > 0) {
+    k_init_state<<<gridv(e, n), 256, 0, str>>>(g.off, n, mu, s.bounds, s.role);
+    e->launches++;
+  }
+  return prepare_similarity(e, eps);
+}
+
+// phase 1 on this shard's edges (Alg. 2)
+int phase_identify(gs_engine* e) { return run_similarity(e, MODE_IDENTIFY, e->eps, e->mu); }
+
+int phase_export_counts(gs_engine* e, int32_t* counts) {
+  if (e->g.n == 0) return GS_OK;
+  k_export_counts<<<gridv(e, e->g.n), 256, 0, e->stream>>>(e->g.n, e->s.bounds, e->g.off, counts);
+  e->launches++;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+int phase_import_counts(gs_engine* e, const int32_t* counts) {
+  if (e->g.n == 0) return GS_OK;
+  k_import_counts<<<gridv(e, e->g.n), 256, 0, e->stream>>>(e->g.n, counts, e->g.off, e->s.bounds);
+  e->launches++;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+// resolve_roles_from_bounds / _cleanup_unknown_roles (scan.py:390-449)
+int phase_resolve(gs_engine* e, bool allow_cleanup) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  cudaStream_t str = e->stream;
+  const int64_t n = g.n;
+  if (n > 0) {
+    k_resolve<<<gridv(e, n), 256, 0, str>>>(n, e->mu, s.bounds, s.role, s.ctr);
+    e->launches++;
+  }
+  unsigned long long unresolved = 0;
+  GS_CUDA(cudaMemcpyAsync(&unresolved, s.ctr + CTR_UNRESOLVED, sizeof(unresolved),
+                          cudaMemcpyDeviceToHost, str));
+  GS_CUDA(cudaStreamSynchronize(str));
+  if (unresolved && allow_cleanup) {
+    GS_CUDA(cudaMemsetAsync(s.ctr + CTR_UNRESOLVED, 0, sizeof(unsigned long long), str));
+    GS_TRY(run_similarity(e, MODE_CLEANUP, e->eps, e->mu));
+    k_resolve<<<gridv(e, n), 256, 0, str>>>(n, e->mu, s.bounds, s.role, s.ctr);
+    e->launches++;
+    GS_CUDA(cudaMemcpyAsync(&unresolved, s.ctr + CTR_UNRESOLVED, sizeof(unresolved),
+                            cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+  }
+  if (unresolved) {
+    set_error("role resolution incomplete after full edge sweep");
+    return GS_EINTERNAL;
+  }
+  // singletons (scan.py:725-727) and the core count
+  if (n > 0) {
+    k_singletons<<<gridv(e, n), 256, 0, str>>>(n, s.role, s.parent, s.ctr);
+    e->launches++;
+    GS_CUDA(cudaMemcpyAsync(&e->ncores, s.ctr + CTR_CORES_PRE, sizeof(e->ncores),
+                            cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+  }
+  return GS_OK;
+}
+
+// unions over this shard's similar core-core edges (Alg. 3 lines 1-18)
+int phase_union(gs_engine* e) {
+  if (e->ncores == 0) return GS_OK;  // no core, no cluster
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  if (g.m > 0) {
+    k_union_known<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.parent,
+                                                       s.ctr, e->shard_rank, e->shard_world);
+    e->launches++;
+  }
+  return run_similarity(e, MODE_UNION, e->eps, e->mu);
+}
+
+int phase_export_pairs(gs_engine* e, int32_t* pairs, int64_t* npairs) {
+  *npairs = 0;
+  if (e->ncores == 0 || e->g.n == 0) return GS_OK;
+  DevState& s = e->s;
+  unsigned long long* cnt = nullptr;
+  GS_TRY(e->alloc_n(&cnt, 1));
+  GS_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), e->stream));
+  k_export_pairs<<<gridv(e, e->g.n), 256, 0, e->stream>>>(e->g.n, s.role, s.parent, pairs, cnt);
+  e->launches++;
+  unsigned long long h = 0;
+  GS_CUDA(cudaMemcpyAsync(&h, cnt, sizeof(h), cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  e->release(cnt);
+  *npairs = (int64_t)h;
+  return GS_OK;
+}
+
+int phase_merge_pairs(gs_engine* e, const int32_t* pairs, int64_t npairs) {
+  if (e->ncores == 0 || e->g.n == 0) return GS_OK;
+  DevState& s = e->s;
+  k_singletons<<<gridv(e, e->g.n), 256, 0, e->stream>>>(e->g.n, s.role, s.parent, nullptr);
+  e->launches++;
+  if (npairs > 0) {
+    k_union_pairs<<<gridv(e, npairs), 256, 0, e->stream>>>(npairs, pairs, s.parent, s.ctr);
+    e->launches++;
+  }
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+// flatten + canonical labels (min caller id per class); member labels init
+int phase_labels(gs_engine* e) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  const int64_t n = g.n;
+  if (n == 0) return GS_OK;
+  if (e->ncores > 0) {
+    k_flatten<<<gridv(e, n), 256, 0, e->stream>>>(n, s.role, s.parent, g.orig, s.label, s.ctr);
+    e->launches++;
+  }
+  k_core_labels<<<gridv(e, n), 256, 0, e->stream>>>(n, s.role, s.parent, s.label, s.lmin, s.lmax);
+  e->launches++;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+// member attachment over this shard's similar core-noncore edges
+int phase_attach(gs_engine* e) {
+  if (e->ncores == 0) return GS_OK;
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  GS_TRY(run_similarity(e, MODE_ATTACH, e->eps, e->mu));
+  if (g.m > 0) {
+    k_attach<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax,
+                                                  e->shard_rank, e->shard_world);
+    e->launches++;
+  }
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+int phase_export_labels(gs_engine* e, int32_t* labels) {
+  const size_t b = sizeof(int32_t) * (size_t)e->g.n;
+  if (b == 0) return GS_OK;
+  GS_CUDA(cudaMemcpyAsync(labels, e->s.lmin, b, cudaMemcpyDeviceToDevice, e->stream));
+  GS_CUDA(cudaMemcpyAsync(labels + e->g.n, e->s.lmax, b, cudaMemcpyDeviceToDevice, e->stream));
+  return GS_OK;
+}
+
+int phase_import_labels(gs_engine* e, const int32_t* labels) {
+  const size_t b = sizeof(int32_t) * (size_t)e->g.n;
+  if (b == 0) return GS_OK;
+  GS_CUDA(cudaMemcpyAsync(e->s.lmin, labels, b, cudaMemcpyDeviceToDevice, e->stream));
+  GS_CUDA(cudaMemcpyAsync(e->s.lmax, labels + e->g.n, b, cudaMemcpyDeviceToDevice, e->stream));
+  return GS_OK;
+}
+
+// phase 3 (Alg. 4) and the result scatter to caller ids
+int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_on_device,
+                 gs_stats* st) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  cudaStream_t str = e->stream;
+  const int64_t n = g.n, m = g.m;
   uint8_t* fin = nullptr;
   GS_TRY(e->alloc_n(&fin, n));
   uint8_t* d_role_out = role_out;
@@ -288,90 +519,25 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     if (role_out) GS_TRY(e->alloc_n(&d_role_out, n));
     if (cluster_out) GS_TRY(e->alloc_n(&d_cluster_out, n));
   }
-  PhaseTimer tm(e);
-  tm.mark();  // 0
-  GS_CUDA(cudaMemsetAsync(s.sim, 0, (size_t)(m > 0 ? m : 1), str));
-  GS_CUDA(cudaMemsetAsync(s.ctr, 0, sizeof(unsigned long long) * CTR_COUNT, str));
-  GS_CUDA(cudaMemsetAsync(s.label, 0x7f, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), str));
-  if (n > 0) {
-    k_init_state<<<gv, T, 0, str>>>(g.off, n, mu, s.bounds, s.role);
-    e->launches++;
-  }
-  // ---- phase 1: identify cores (Alg. 2)
-  GS_TRY(prepare_similarity(e, eps));
-  GS_TRY(run_similarity(e, MODE_IDENTIFY, eps, mu));
-  tm.mark();  // 1
-  // ---- cleanup (scan.py:415-449): resolve from bounds; re-evaluate if open
-  if (n > 0) {
-    k_resolve<<<gv, T, 0, str>>>(n, mu, s.bounds, s.role, s.ctr);
-    e->launches++;
-  }
-  unsigned long long unresolved = 0;
-  GS_CUDA(cudaMemcpyAsync(&unresolved, s.ctr + CTR_UNRESOLVED, sizeof(unresolved),
-                          cudaMemcpyDeviceToHost, str));
-  GS_CUDA(cudaStreamSynchronize(str));
-  if (unresolved) {
-    GS_CUDA(cudaMemsetAsync(s.ctr + CTR_UNRESOLVED, 0, sizeof(unsigned long long), str));
-    GS_TRY(run_similarity(e, MODE_CLEANUP, eps, mu));
-    k_resolve<<<gv, T, 0, str>>>(n, mu, s.bounds, s.role, s.ctr);
-    e->launches++;
-    GS_CUDA(cudaMemcpyAsync(&unresolved, s.ctr + CTR_UNRESOLVED, sizeof(unresolved),
-                            cudaMemcpyDeviceToHost, str));
-    GS_CUDA(cudaStreamSynchronize(str));
-    if (unresolved) {
-      set_error("role resolution incomplete after full edge sweep");
-      return GS_EINTERNAL;
-    }
-  }
-  tm.mark();  // 2
-  // ---- phase 2: detect clusters (Alg. 3)
-  unsigned long long ncores = 0;
-  if (n > 0) {
-    k_singletons<<<gv, T, 0, str>>>(n, s.role, s.parent, s.ctr);
-    e->launches++;
-    GS_CUDA(cudaMemcpyAsync(&ncores, s.ctr + CTR_CORES_PRE, sizeof(ncores),
-                            cudaMemcpyDeviceToHost, str));
-    GS_CUDA(cudaStreamSynchronize(str));
-  }
-  if (ncores > 0) {  // no core, no cluster: the union / attach passes have no edge
-    if (m > 0) {
-      k_union_known<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.parent, s.ctr);
-      e->launches++;
-    }
-    GS_TRY(run_similarity(e, MODE_UNION, eps, mu));
-    k_flatten<<<gv, T, 0, str>>>(n, s.role, s.parent, g.orig, s.label, s.ctr);
-    e->launches++;
-  }
-  if (n > 0) {
-    k_core_labels<<<gv, T, 0, str>>>(n, s.role, s.parent, s.label, s.lmin, s.lmax);
-    e->launches++;
-  }
-  if (ncores > 0) {
-    GS_TRY(run_similarity(e, MODE_ATTACH, eps, mu));
-    if (m > 0) {
-      k_attach<<<ge, T, 0, str>>>(m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax);
-      e->launches++;
-    }
-  }
-  tm.mark();  // 3
-  // ---- phase 3: hubs and outliers (Alg. 4)
-  const int64_t rsplit = ncores > 0 ? g.rclass[1] : 0;
-  if (ncores == 0 && n > 0)  // nothing is clustered: every vertex is an outlier
+  const int64_t rsplit = e->ncores > 0 ? g.rclass[1] : 0;
+  if (e->ncores == 0 && n > 0)  // nothing is clustered: every vertex is an outlier
     GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
   if (rsplit > 0) {
-    k_classify_thread<<<(unsigned)std::min<int64_t>(grid_for(rsplit, T), (int64_t)e->sms * 32),
-                        T, 0, str>>>(0, rsplit, g.off, g.adj, s.role, s.lmin, s.lmax, fin);
+    k_classify_thread<<<gridv(e, rsplit), 256, 0, str>>>(0, rsplit, g.off, g.adj, s.role, s.lmin,
+                                                        s.lmax, fin);
     e->launches++;
   }
-  if (ncores > 0 && n > rsplit) {
-    const int64_t nwarps = n - rsplit;
-    k_classify_warp<<<(unsigned)std::min<int64_t>(grid_for(nwarps * 32, T), (int64_t)e->sms * 32),
-                      T, 0, str>>>(rsplit, n, g.off, g.adj, s.role, s.lmin, s.lmax, fin);
+  if (e->ncores > 0 && n > rsplit) {
+    k_classify_warp<<<gridv(e, (n - rsplit) * 32), 256, 0, str>>>(rsplit, n, g.off, g.adj, s.role,
+                                                                 s.lmin, s.lmax, fin);
     e->launches++;
   }
-  tm.mark();  // 4
+  cudaEvent_t c0, c1;
+  cudaEventCreate(&c0);
+  cudaEventCreate(&c1);
+  cudaEventRecord(c0, str);
   if (n > 0) {
-    k_output<<<gv, T, 0, str>>>(n, g.orig, fin, s.lmin, d_role_out, d_cluster_out, s.ctr);
+    k_output<<<gridv(e, n), 256, 0, str>>>(n, g.orig, fin, s.lmin, d_role_out, d_cluster_out, s.ctr);
     e->launches++;
   }
   if (!out_on_device) {
@@ -381,7 +547,7 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
       GS_CUDA(cudaMemcpyAsync(cluster_out, d_cluster_out, (size_t)n * 4, cudaMemcpyDeviceToHost,
                               str));
   }
-  tm.mark();  // 5
+  cudaEventRecord(c1, str);
   unsigned long long h[CTR_COUNT];
   GS_CUDA(cudaMemcpyAsync(h, s.ctr, sizeof(h), cudaMemcpyDeviceToHost, str));
   GS_CUDA(cudaStreamSynchronize(str));
@@ -392,6 +558,8 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
   }
   e->release(fin);
   if (st) {
+    float d2h = 0;
+    cudaEventElapsedTime(&d2h, c0, c1);
     st->n = n;
     st->m = m;
     st->sim_evals = (int64_t)h[CTR_SIM_EVALS];
@@ -406,11 +574,36 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     st->n_hub = (int64_t)h[CTR_N_HUB];
     st->n_outlier = (int64_t)h[CTR_N_OUTLIER];
     st->n_clusters = (int64_t)h[CTR_N_CLUSTERS];
+    st->phase_ms[GS_PH_D2H] = d2h;
+  }
+  cudaEventDestroy(c0);
+  cudaEventDestroy(c1);
+  return GS_OK;
+}
+
+// the single-GPU scan: every phase in a row, no exchange
+int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
+             int32_t* cluster_out, int out_on_device, gs_stats* st) {
+  PhaseTimer tm(e);
+  tm.mark();  // 0
+  GS_TRY(phase_begin(e, mu, eps));
+  GS_TRY(phase_identify(e));
+  tm.mark();  // 1
+  GS_TRY(phase_resolve(e, e->shard_world == 1));
+  tm.mark();  // 2
+  GS_TRY(phase_union(e));
+  GS_TRY(phase_labels(e));
+  GS_TRY(phase_attach(e));
+  tm.mark();  // 3
+  tm.mark();  // 4 (classify is timed inside finish with the output scatter)
+  GS_TRY(phase_finish(e, role_out, cluster_out, out_on_device, st));
+  tm.mark();  // 5
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  if (st) {
     st->phase_ms[GS_PH_IDENTIFY] = tm.ms(0, 1);
     st->phase_ms[GS_PH_CLEANUP] = tm.ms(1, 2);
     st->phase_ms[GS_PH_CLUSTER] = tm.ms(2, 3);
-    st->phase_ms[GS_PH_CLASSIFY] = tm.ms(3, 4);
-    st->phase_ms[GS_PH_D2H] = tm.ms(4, 5);
+    st->phase_ms[GS_PH_CLASSIFY] = tm.ms(4, 5) - st->phase_ms[GS_PH_D2H];
   }
   return GS_OK;
 }

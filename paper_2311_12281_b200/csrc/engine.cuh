@@ -100,6 +100,8 @@ struct SimParams {
   const int32_t* nlo;   // per vertex: neighbours below hub_lo (the non-hub prefix)
   uint32_t hub_lo;      // first rank of the hub bitmap range
   uint32_t bm_words;    // hub bitmap words (range [hub_lo, n))
+  int shard_rank;       // this process owns the edges whose high endpoint
+  int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;
   int32_t mu;
   int mode;
@@ -121,6 +123,11 @@ struct gs_engine {
   int sms = 148;
   int64_t launches = 0;
   float last_h2d_ms = 0, last_build_ms = 0;
+  int shard_rank = 0, shard_world = 1;  // multi-GPU edge ownership (b % world == rank)
+  int32_t mu = 0;                       // parameters of the scan in progress
+  gs::Eps2 eps{};
+  unsigned long long ncores = 0;
+  float phase_ms[GS_PH_COUNT] = {0};    // timings of the sharded phase calls
   // host-side pinned staging for counters
   unsigned long long* h_ctr = nullptr;
   std::vector<cudaEvent_t> ev;
@@ -143,9 +150,36 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
 // sim.cu
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
 int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split
-// cluster.cu
+// cluster.cu: the scan as phases (single GPU: all of them in a row; sharded:
+// the host layer runs the collectives between them, see dist.py)
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
              int32_t* cluster_out, int out_on_device, gs_stats* st);
+int phase_begin(gs_engine* e, int32_t mu, const Eps2& eps);
+int phase_identify(gs_engine* e);
+int phase_export_counts(gs_engine* e, int32_t* counts);
+int phase_import_counts(gs_engine* e, const int32_t* counts);
+int phase_resolve(gs_engine* e, bool allow_cleanup);
+int phase_union(gs_engine* e);
+int phase_export_pairs(gs_engine* e, int32_t* pairs, int64_t* npairs);
+int phase_merge_pairs(gs_engine* e, const int32_t* pairs, int64_t npairs);
+int phase_labels(gs_engine* e);
+int phase_attach(gs_engine* e);
+int phase_export_labels(gs_engine* e, int32_t* labels);
+int phase_import_labels(gs_engine* e, const int32_t* labels);
+int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_on_device,
+                 gs_stats* st);
+// owner of the edges of high endpoint b
+__host__ __device__ __forceinline__ bool owns(int64_t b, int rank, int world) {
+  return world == 1 || (int)(b % world) == rank;
+}
+// the item-th owned high endpoint from the top of [rlo, rhi) (< rlo: done)
+__host__ __device__ __forceinline__ int64_t shard_top(int64_t rlo, int64_t rhi, int64_t item,
+                                                      int rank, int world) {
+  if (world == 1) return rhi - 1 - item;
+  int64_t top = rhi - 1;
+  top -= ((top - rank) % world + world) % world;
+  return top - item * world;
+}
 // launch helper: grid for n items
 inline unsigned grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;

@@ -28,8 +28,10 @@ namespace gs {
 
 __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int64_t rhi) {
   LocalCtr lc;
-  for (int64_t b = rlo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < rhi;
-       b += (int64_t)gridDim.x * blockDim.x) {
+  const int w = P.shard_world;
+  const int64_t first = rlo + ((P.shard_rank - rlo) % w + w) % w;  // first owned b >= rlo
+  for (int64_t b = first + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * w; b < rhi;
+       b += (int64_t)gridDim.x * blockDim.x * w) {
     const int64_t e0 = P.eoff[b], e1 = P.eoff[b + 1];
     if (e0 == e1) continue;
     const int64_t ob = P.off[b], eb = P.off[b + 1], db = eb - ob;
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&P.wq[qi], 1);
     __syncthreads();
-    const int64_t b = rhi - 1 - (int64_t)s_item;
+    const int64_t b = shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
@@ -248,7 +250,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
     int item = 0;
     if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
     item = __shfl_sync(0xffffffffu, item, 0);
-    const int64_t b = rhi - 1 - (int64_t)item;
+    const int64_t b = shard_top(rlo, rhi, item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
@@ -405,6 +407,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.gtab_stride = 0;
   P.thr = s.thr;
   P.nlo = s.nlo;
+  P.shard_rank = e->shard_rank;
+  P.shard_world = e->shard_world;
   {
     const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
     P.hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);

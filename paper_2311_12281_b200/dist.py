@@ -1,0 +1,107 @@
+"""Sharded multi-GPU scan: one process per GPU, NCCL over
+NVLink through torch.distributed for the three exchanges, the engine's
+sm_100a kernels for everything else.
+
+Every rank loads the same graph (degree-rank layout is deterministic, so
+rank-space vertex ids agree across ranks) and owns the oriented edges whose
+high endpoint b satisfies ``b % world == rank`` (round-robin over the
+degree-sorted order, which balances the heavy tail).  Lemma-1 bounds built
+from a subset of the edges are still valid bounds, so each rank prunes with
+its own counts during identify; the exact global state is then rebuilt by
+
+  1. all-reduce(SUM) of per-vertex similar / dissimilar counts  -> roles
+  2. all-gather of each rank's (core, local root) pairs           -> merged
+     union-find forest (identical on every rank), canonical labels
+  3. all-reduce(MIN / MAX) of member labels                       -> members,
+     shared members, then hub / outlier classification
+
+With world = 1 the same phases run with no exchange and reproduce
+``scan_in_memory`` exactly (tests/test_gpu_shards.py checks world 2 and 3).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def all_gather_varlen(t: torch.Tensor, n_valid: int, group=None) -> torch.Tensor:
+    """Concatenate the first ``n_valid`` rows of ``t`` from every rank (rank
+    order).  Pads to the longest contribution so NCCL sees equal sizes."""
+    world = dist.get_world_size(group)
+    cnt = torch.tensor([n_valid], dtype=torch.int64, device=t.device)
+    cnts = [torch.zeros_like(cnt) for _ in range(world)]
+    dist.all_gather(cnts, cnt, group=group)
+    sizes = [int(c.item()) for c in cnts]
+    mx = max(sizes)
+    if mx == 0:
+        return t[:0]
+    buf = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    buf[:n_valid] = t[:n_valid]
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[:s] for o, s in zip(out, sizes)])
+
+
+def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
+    """Sum the per-rank counters, max the timings (whole-job view)."""
+    ints = ["sim_evals", "adj_probes", "union_retries", "probe_bound_violations",
+            "sim_decided_by_bound", "sim_intersections", "alg_bytes_sim", "kernel_launches"]
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([getattr(st, k) for k in ints], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    ph = torch.tensor(list(st.phase_ms), dtype=torch.float64, device=dev)
+    dist.all_reduce(ph, op=dist.ReduceOp.MAX, group=group)
+    for k, v in zip(ints, t.tolist()):
+        setattr(st, k, int(v))
+    for i, v in enumerate(ph.tolist()):
+        st.phase_ms[i] = v
+    return st
+
+
+class ShardedScan:
+    """Run the phases of one engine as this rank's shard of a scan."""
+
+    def __init__(self, engine: _lib.Engine, n: int, group=None):
+        self.eng = engine
+        self.n = int(n)
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.lib = _lib.load()
+        _lib.check(self.lib.gs_engine_set_shard(engine.handle, self.rank, self.world))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.counts = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
+        self.pairs = torch.empty((max(self.n, 1), 2), dtype=torch.int32, device=dev)
+        self.labels = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
+
+    def run(self, mu: int, eps2: _lib.GsEps2, role_out: int, cluster_out: int,
+            out_on_device: int, stats: Optional[_lib.GsStats] = None) -> _lib.GsStats:
+        lib, h, n, g = self.lib, self.eng.handle, self.n, self.group
+        st = stats if stats is not None else _lib.GsStats()
+        _lib.check(lib.gs_engine_phase_begin(h, int(mu), ctypes.byref(eps2)))
+        _lib.check(lib.gs_engine_phase_identify(h, self.counts.data_ptr()))
+        dist.all_reduce(self.counts[: 2 * n], op=dist.ReduceOp.SUM, group=g)    # exchange 1
+        nc = ctypes.c_int64(0)
+        _lib.check(lib.gs_engine_phase_resolve(h, self.counts.data_ptr(), ctypes.byref(nc)))
+        labels_ptr = None
+        if nc.value > 0:  # no core anywhere: nothing to merge or attach
+            npairs = ctypes.c_int64(0)
+            _lib.check(lib.gs_engine_phase_union(h, self.pairs.data_ptr(), ctypes.byref(npairs)))
+            allp = all_gather_varlen(self.pairs, npairs.value, g).contiguous()  # exchange 2
+            _lib.check(lib.gs_engine_phase_merge(h, allp.data_ptr() if len(allp) else None,
+                                                 len(allp)))
+            _lib.check(lib.gs_engine_phase_attach(h, self.labels.data_ptr()))
+            dist.all_reduce(self.labels[:n], op=dist.ReduceOp.MIN, group=g)      # exchange 3
+            dist.all_reduce(self.labels[n: 2 * n], op=dist.ReduceOp.MAX, group=g)
+            labels_ptr = self.labels.data_ptr()
+        else:
+            _lib.check(lib.gs_engine_phase_merge(h, None, 0))
+        _lib.check(lib.gs_engine_phase_finish(h, labels_ptr, role_out, cluster_out,
+                                              out_on_device, ctypes.byref(st)))
+        return reduce_stats(st, g)
