@@ -56,6 +56,25 @@ static int check_eps(const gs_eps2* p) {
 
 using namespace gs;
 
+// event-timed phase call (sharded path): adds the device time to e->phase_ms[ph]
+template <class F>
+static int timed(gs_engine* e, int ph, F&& f) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, e->stream);
+  int rc = f();
+  cudaEventRecord(b, e->stream);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  e->phase_ms[ph] += ms;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return rc;
+}
+
+
 // Engine allocations are cached: a released block goes to a size-keyed free
 // list and the next request of a similar size reuses it, so repeated calls
 // (the same build + scan sequence every time) never touch the driver
@@ -323,24 +342,6 @@ int gs_engine_phase_begin(gs_engine* e, int32_t mu, const gs_eps2* eps2) {
   e->launches = 0;
   for (auto& x : e->phase_ms) x = 0;
   return timed(e, GS_PH_IDENTIFY, [&] { return phase_begin(e, mu, to_eps(eps2)); });
-}
-
-// event-timed phase call (sharded path): adds the device time to e->phase_ms[ph]
-template <class F>
-static int timed(gs_engine* e, int ph, F&& f) {
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  cudaEventRecord(a, e->stream);
-  int rc = f();
-  cudaEventRecord(b, e->stream);
-  cudaEventSynchronize(b);
-  float ms = 0;
-  cudaEventElapsedTime(&ms, a, b);
-  e->phase_ms[ph] += ms;
-  cudaEventDestroy(a);
-  cudaEventDestroy(b);
-  return rc;
 }
 
 int gs_engine_phase_identify(gs_engine* e, int32_t* counts_dev) {
