@@ -40,17 +40,31 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo,
 // ---------------------------------------------------------------------------
 // kernels
 
+// Degrees of a normalised edge list.  Sets bad[0] for invalid pairs and
+// bad[1] when the list is not strictly increasing with u < v (informational:
+// the sort-based build checks duplicates itself).  Consecutive edges of a
+// sorted list share u, so the u-side increments are warp-aggregated.
 __global__ void k_count_deg_edges(const int32_t* __restrict__ uv, int64_t m, int64_t n,
                                   uint32_t* __restrict__ deg, int* __restrict__ bad) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < m;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    int2 p = reinterpret_cast<const int2*>(uv)[k];
-    if (p.x < 0 || p.y < 0 || p.x >= n || p.y >= n || p.x == p.y) {
-      atomicExch(bad, 1);
-      continue;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t mm = (m + 31) / 32 * 32;  // whole warps iterate together
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < mm; k += stride) {
+    const bool in = k < m;
+    int2 p = in ? reinterpret_cast<const int2*>(uv)[k] : make_int2(-1, -1);
+    bool ok = in && !(p.x < 0 || p.y < 0 || p.x >= n || p.y >= n || p.x == p.y);
+    if (in && !ok) atomicExch(&bad[0], 1);
+    if (in && !(p.x < p.y)) bad[1] = 1;
+    if (in && k > 0) {
+      const int2 q = reinterpret_cast<const int2*>(uv)[k - 1];
+      if (q.x > p.x || (q.x == p.x && q.y >= p.y)) bad[1] = 1;
     }
-    atomicAdd(&deg[p.x], 1u);
-    atomicAdd(&deg[p.y], 1u);
+    const unsigned act = __ballot_sync(0xffffffffu, ok);
+    const int key = ok ? p.x : -1 - (int)(threadIdx.x & 31);
+    const unsigned grp = __match_any_sync(0xffffffffu, key) & act;
+    if (ok) {
+      if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&deg[p.x], (unsigned)__popc(grp));
+      atomicAdd(&deg[p.y], 1u);
+    }
   }
 }
 
@@ -196,38 +210,29 @@ __global__ void k_class_bounds(const int64_t* __restrict__ ndeg, int64_t n,
 // ---------------------------------------------------------------------------
 // shared tail of both builds: given rank[] (or null) and arc keys, finish CSR
 
-static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int B,
-                        uint64_t* keys_alt, int64_t* ndeg, int* d_bad) {
+// offsets (rank space) from rank-ordered degrees, class bounds, dmax
+static int finish_offsets(gs_engine* e, int64_t n, int64_t* ndeg, int64_t* h_cls) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
-  const int64_t slots = 2 * m;
-  // sort the 2m arc keys (rank_u, rank_v) -> CSR order
-  cub::DoubleBuffer<uint64_t> db(keys, keys_alt);
-  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, db, slots, 0, 2 * B, st);
-  }));
-  uint64_t* sorted = db.Current();
-  GS_TRY(e->alloc_n(&g.adj, slots));
-  if (slots > 0) {
-    k_extract_adj<<<e->sms * 16, 256, 0, st>>>(sorted, slots, B, g.adj, d_bad);
-    e->launches++;
-  }
-  e->release(keys);
-  e->release(keys_alt);
-  // offsets from the rank-ordered degrees
   GS_TRY(e->alloc_n(&g.off, n + 1));
   GS_TRY(cub_call(e, [&](void* t, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(t, b, ndeg, g.off, n + 1, st);
   }));
-  // class bounds + dmax
   int64_t* d_cls = nullptr;
   GS_TRY(e->alloc_n(&d_cls, DevGraph::kClasses + 1));
   k_class_bounds<<<1, 32, 0, st>>>(ndeg, n, d_cls);
   e->launches++;
-  int64_t h_cls[DevGraph::kClasses + 1];
-  GS_CUDA(cudaMemcpyAsync(h_cls, d_cls, sizeof(h_cls), cudaMemcpyDeviceToHost, st));
-  e->release(ndeg);
-  // oriented edge offsets
+  GS_CUDA(cudaMemcpyAsync(h_cls, d_cls, sizeof(int64_t) * (DevGraph::kClasses + 1),
+                          cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(d_cls);
+  return GS_OK;
+}
+
+// oriented-edge offsets, validation, endpoint arrays
+static int finish_rest(gs_engine* e, int64_t n, int64_t m, const int64_t* h_cls, int* d_bad) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
   int64_t* cnt = nullptr;
   GS_TRY(e->alloc_n(&cnt, n + 1));
   if (n > 0) {
@@ -239,10 +244,9 @@ static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int 
     return cub::DeviceScan::ExclusiveSum(t, b, cnt, g.eoff, n + 1, st);
   }));
   e->release(cnt);
-  GS_CUDA(cudaStreamSynchronize(st));
-  e->release(d_cls);
   int h_bad = 0;
-  GS_CUDA(cudaMemcpy(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  GS_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_bad);
   if (h_bad) {
     const char* why = h_bad == 1   ? "edge has an id outside [0, n) or is a self-loop"
@@ -281,13 +285,37 @@ static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int 
   return GS_OK;
 }
 
+// generic build tail: sort the 2m arc keys (rank_u, rank_v) -> CSR order
+static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int B,
+                        uint64_t* keys_alt, int64_t* ndeg, int* d_bad) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  const int64_t slots = 2 * m;
+  cub::DoubleBuffer<uint64_t> db(keys, keys_alt);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, slots, 0, 2 * B, st);
+  }));
+  uint64_t* sorted = db.Current();
+  GS_TRY(e->alloc_n(&g.adj, slots));
+  if (slots > 0) {
+    k_extract_adj<<<e->sms * 16, 256, 0, st>>>(sorted, slots, B, g.adj, d_bad);
+    e->launches++;
+  }
+  e->release(keys);
+  e->release(keys_alt);
+  int64_t h_cls[DevGraph::kClasses + 1];
+  GS_TRY(finish_offsets(e, n, ndeg, h_cls));
+  e->release(ndeg);
+  return finish_rest(e, n, m, h_cls, d_bad);
+}
+
 int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
   cudaStream_t st = e->stream;
   DevGraph& g = e->g;
   e->free_graph();
   int* d_bad = nullptr;
-  GS_TRY(e->alloc_n(&d_bad, 1));
-  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  GS_TRY(e->alloc_n(&d_bad, 2));
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(int), st));
   uint32_t* deg = nullptr;
   GS_TRY(e->alloc_n(&deg, n));
   GS_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1), st));
@@ -446,8 +474,8 @@ int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv
                            int32_t* elist_dev, bool csr_only) {
   cudaStream_t st = e->stream;
   int* d_bad = nullptr;
-  GS_TRY(e->alloc_n(&d_bad, 1));
-  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  GS_TRY(e->alloc_n(&d_bad, 2));
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, 2 * sizeof(int), st));
   uint32_t* deg = nullptr;
   GS_TRY(e->alloc_n(&deg, n));
   GS_CUDA(cudaMemsetAsync(deg, 0, sizeof(uint32_t) * (size_t)(n > 0 ? n : 1), st));
