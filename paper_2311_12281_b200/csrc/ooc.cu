@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
         oa = __shfl_sync(0xffffffffu, oa, 0);
         int32_t scanned;
         const bool res = scan_survivor<false>(P.hadj + oa, sda, scm, nullptr, 0xffffffffu, 0, C,
-                                              nstash, nb, db, lane, scanned);
+                                              nstash, nb, db, lane, scanned,
+                                              first_element(P.hadj + oa, sda, lane));
         if (P.mode == OOC_IDENTIFY) { if (res) ++bsim; else ++bdis; }
         if (lane == 0) {
           lc.probes += (unsigned long long)scanned;
@@ -315,7 +316,8 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
           const int2 ad = surv_ad[s];
           int32_t scanned;
           const bool res = scan_survivor<GTAB>(P.hadj + surv_oa[s], ad.y, jc.y, nullptr,
-                                               0xffffffffu, 0, C, nstash, nb, db, lane, scanned);
+                                               0xffffffffu, 0, C, nstash, nb, db, lane, scanned,
+                                               first_element(P.hadj + surv_oa[s], ad.y, lane));
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
             lc.inters++;

@@ -193,17 +193,23 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
         const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
-        // one warp per surviving a, dynamic (scan_survivor)
-        for (;;) {
-          int s = 0;
-          if (lane == 0) s = atomicAdd(&s_next, 1);
-          s = __shfl_sync(0xffffffffu, s, 0);
-          if (s >= ns) break;
+        // one warp per surviving a, dynamic (scan_survivor), software-pipelined:
+        // survivor s+1 is claimed and its first load issued before s is scanned
+        int s = 0;
+        if (lane == 0) s = atomicAdd(&s_next, 1);
+        s = __shfl_sync(0xffffffffu, s, 0);
+        uint32_t first = s < ns ? first_element(P.adj + surv_oa[s], surv_ad[s].y, lane) : kPast;
+        while (s < ns) {
+          int s2 = 0;
+          if (lane == 0) s2 = atomicAdd(&s_next, 1);
+          s2 = __shfl_sync(0xffffffffu, s2, 0);
+          const uint32_t first2 =
+              s2 < ns ? first_element(P.adj + surv_oa[s2], surv_ad[s2].y, lane) : kPast;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
           int32_t scanned;
           const bool res = scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo, rmax,
-                                               C, nstash, nb, nlo, lane, scanned);
+                                               C, nstash, nb, nlo, lane, scanned, first);
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
             lc.inters++;
@@ -211,6 +217,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
           }
+          s = s2;
+          first = first2;
         }
       }
       __syncthreads();
@@ -297,16 +305,27 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
         if (lane == 0) lc.bytes += 4ull * (unsigned long long)db;
       }
       const int nstash = built ? *C.nstash : 0;
+      // survivors of this batch, software-pipelined like the CTA kernel
+      int src = smask ? __ffs(smask) - 1 : 0;
+      uint32_t first = kPast;
+      if (smask) {
+        const int32_t da0 = __shfl_sync(0xffffffffu, da, src);
+        const int64_t oa0 = __shfl_sync(0xffffffffu, oa, src);
+        first = first_element(P.adj + oa0, da0, lane);
+      }
       while (smask) {
-        const int src = __ffs(smask) - 1;
         smask &= smask - 1;
+        const int src2 = smask ? __ffs(smask) - 1 : 0;
         const int32_t sa = __shfl_sync(0xffffffffu, a, src);
         const int32_t sda = __shfl_sync(0xffffffffu, da, src);
         const int32_t scm = __shfl_sync(0xffffffffu, cmin, src);
         const int64_t soa = __shfl_sync(0xffffffffu, oa, src);
+        const int32_t da2 = __shfl_sync(0xffffffffu, da, src2);
+        const int64_t oa2 = __shfl_sync(0xffffffffu, oa, src2);
+        const uint32_t first2 = smask ? first_element(P.adj + oa2, da2, lane) : kPast;
         int32_t scanned;
         const bool res = scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu, 0, C,
-                                              nstash, nb, db, lane, scanned);
+                                              nstash, nb, db, lane, scanned, first);
         if (res) ++bsim; else ++bdis;
         if (lane == 0) {
           lc.probes += (unsigned long long)scanned;
@@ -314,6 +333,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
           lc.bytes += 4ull * (unsigned long long)sda;
           record_edge(P, e0 + base + src, sa, (int32_t)b, res, false, lc);
         }
+        src = src2;
+        first = first2;
       }
     }
     if (lane == 0 && (bsim | bdis) && (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP))

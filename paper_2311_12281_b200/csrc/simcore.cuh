@@ -227,32 +227,51 @@ __device__ __forceinline__ bool member(const uint32_t* bm, uint32_t hub_lo, cons
 // cannot decide the edge.  Steps whose elements all lie in the hub range
 // (warp vote) take a branch-free bitmap path; past-the-end slots hold a
 // sentinel >= n that lands on an always-zero bitmap guard word.
+static constexpr uint32_t kPast = 0x7fffffffu;  // scan sentinel, >= n
+
+// The first step's element of this lane (the top 32 of N(a)); issued early so
+// the load of survivor s+1 overlaps the scan of survivor s.
+__device__ __forceinline__ uint32_t first_element(const int32_t* __restrict__ a_run, int32_t da,
+                                                  int lane) {
+  return lane < da ? (uint32_t)__ldg(a_run + (da - 1 - lane)) : kPast;
+}
+
 template <bool GTAB>
 __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run, int32_t da,
                                               int32_t cmin, const uint32_t* bm, uint32_t hub_lo,
                                               uint32_t rmax, const Cuckoo& C, int nstash,
                                               const int32_t* __restrict__ nb, int64_t nlo,
-                                              int lane, int32_t& scanned) {
+                                              int lane, int32_t& scanned, uint32_t first) {
   const int32_t* __restrict__ na = a_run + (da - 1);  // walk downwards
   const int32_t need_miss = da - cmin + 1;            // misses that decide "dissimilar"
-  constexpr uint32_t kPast = 0x7fffffffu;             // sentinel, >= n
+  // Any decision reads at least min(need_miss - misses, cmin - hits) more
+  // elements, so a step of that many (rounded up to 32, at most 128) never
+  // over-reads except in its last 31 slots; the next step is prefetched only
+  // when this one cannot decide the edge.
   uint32_t cur[4], nxt[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
-  if (lane < da) cur[0] = (uint32_t)__ldg(na - lane);
-  int32_t cu = 1;  // loads per lane in the current step
+  cur[0] = first;
+  int32_t cu = min(4, max(1, (min(need_miss, cmin) + 31) >> 5));
+#pragma unroll
+  for (int u = 1; u < 4; ++u) {
+    const int32_t idx = u * 32 + lane;
+    if (u < cu && idx < da) cur[u] = (uint32_t)__ldg(na - idx);
+  }
   int32_t c = 0;
   scanned = 0;
   for (;;) {
     const int32_t wstep = min(32 * cu, da - scanned);
     const int32_t nbase = scanned + wstep;
-    const bool pre =
-        (cmin - c > wstep) && (need_miss - (scanned - c) > wstep) && (nbase < da);
+    const int32_t rest = min(need_miss - (scanned - c), cmin - c) - wstep;  // still certain
+    const bool pre = rest > 0 && nbase < da;
+    int32_t nu = 0;
     if (pre) {
+      nu = min(4, max(1, (rest + 31) >> 5));
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int32_t idx = nbase + u * 32 + lane;
-        nxt[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+        nxt[u] = (u < nu && idx < da) ? (uint32_t)__ldg(na - idx) : kPast;
       }
     }
     const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
@@ -275,14 +294,15 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
     if (pre) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
+      cu = nu;
     } else {
+      cu = min(4, max(1, (min(need_miss - (scanned - c), cmin - c) + 31) >> 5));
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int32_t idx = scanned + u * 32 + lane;
-        cur[u] = idx < da ? (uint32_t)__ldg(na - idx) : kPast;
+        cur[u] = (u < cu && idx < da) ? (uint32_t)__ldg(na - idx) : kPast;
       }
     }
-    cu = 4;
   }
 }
 
