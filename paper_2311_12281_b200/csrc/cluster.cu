@@ -348,11 +348,8 @@ int phase_begin(gs_engine* e, int32_t mu, const Eps2& eps) {
   GS_CUDA(cudaMemsetAsync(s.sim, 0, (size_t)(m > 0 ? m : 1), str));
   GS_CUDA(cudaMemsetAsync(s.ctr, 0, sizeof(unsigned long long) * CTR_COUNT, str));
   GS_CUDA(cudaMemsetAsync(s.label, 0x7f, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), str));
-  if (n > 0) {
-    k_init_state<<<gridv(e, n), 256, 0, str>>>(g.off, n, mu, s.bounds, s.role);
-    e->launches++;
-  }
-  return prepare_similarity(e, eps);
+  GS_TRY(prepare_similarity(e, eps));
+  return run_prepass(e, mu);  // initial Lemma-1 bounds incl. every O(1)-decided edge
 }
 
 // phase 1 on this shard's edges (Alg. 2)

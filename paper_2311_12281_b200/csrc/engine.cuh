@@ -150,6 +150,7 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
 // sim.cu
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
 int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split
+int run_prepass(gs_engine* e, int32_t mu);  // O(1)-decided edges -> initial bounds
 // cluster.cu: the scan as phases (single GPU: all of them in a row; sharded:
 // the host layer runs the collectives between them, see dist.py)
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,

@@ -78,11 +78,13 @@ struct LocalCtr {
 
 // Record one decided edge.  b's bound update is returned to the caller
 // (aggregated per CTA for the shared-b kernels) unless apply_b is set.
+// `count` is false for O(1)-decided edges re-met by the union / attach passes:
+// the identify pre-pass already counted their decision (sim_evals).
 __device__ __forceinline__ void record_edge(const SimParams& P, int64_t e, int32_t a,
                                             int32_t b, bool similar, bool apply_b,
-                                            LocalCtr& lc) {
+                                            LocalCtr& lc, bool count = true) {
   P.sim[e] = similar ? SIM_SIMILAR : SIM_DISSIMILAR;
-  lc.evals++;
+  lc.evals += count;
   if (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP) {
     apply_bounds(P.bounds, P.role, a, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
     if (apply_b) apply_bounds(P.bounds, P.role, b, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
