@@ -181,6 +181,11 @@ int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets,
  * the CPU generator in oracle/): raw samples, device pointers. */
 int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,
                      int32_t* dst_dev, void* stream);
+/* Chung-Lu (expected-degree power law, exponent gamma) workload: `count` raw
+ * samples over 2^logn vertices, the largest expected degree ~max_degree;
+ * device pointers, deterministic in seed. */
+int gs_chunglu_generate(int logn, double gamma, double max_degree, int64_t count,
+                        uint64_t seed, int32_t* src_dev, int32_t* dst_dev, void* stream);
 /* Normalise raw device samples in place (drop loops, orient, sort, dedupe);
  * writes the unique count to *m_out and interleaved pairs to edges_dev. */
 int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev,

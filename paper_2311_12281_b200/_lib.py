@@ -97,6 +97,8 @@ SIGNATURES = [
      [_I64, _I64, _P, _P, _I32, ctypes.POINTER(GsEps2), ctypes.c_uint64, _P, _P,
       ctypes.POINTER(GsStats)]),
     ("gs_rmat_generate", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _P, _P, _P]),
+    ("gs_chunglu_generate", ctypes.c_int,
+     [ctypes.c_int, ctypes.c_double, ctypes.c_double, _I64, ctypes.c_uint64, _P, _P, _P]),
     ("gs_normalize_edges", ctypes.c_int, [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P]),
     ("gs_last_error", ctypes.c_char_p, []),
     ("gs_version", ctypes.c_int, []),

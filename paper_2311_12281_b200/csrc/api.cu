@@ -21,6 +21,8 @@ int build_reference_layout(gs_engine* e, int64_t n, int64_t m, const int32_t* uv
                            int32_t* elist_dev, bool csr_only);
 int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t* dst,
                   cudaStream_t st);
+int chunglu_generate(int logn, double gamma, double wmax, int64_t count, uint64_t seed,
+                     int32_t* src, int32_t* dst, cudaStream_t st);
 int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32_t* dst,
                     int32_t* uv, int64_t* m_out);
 int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
@@ -530,6 +532,16 @@ int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,
   }
   return rmat_generate(scale, seed, (int64_t)edgefactor << scale, src_dev, dst_dev,
                        (cudaStream_t)stream);
+}
+
+int gs_chunglu_generate(int logn, double gamma, double max_degree, int64_t count,
+                        uint64_t seed, int32_t* src_dev, int32_t* dst_dev, void* stream) {
+  if (logn < 1 || logn > 31 || gamma <= 1.5 || max_degree <= 1 || count < 0) {
+    set_error("invalid Chung-Lu parameters");
+    return GS_EINVAL;
+  }
+  return chunglu_generate(logn, gamma, max_degree, count, seed, src_dev, dst_dev,
+                          (cudaStream_t)stream);
 }
 
 int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev, int32_t* edges_dev,

@@ -621,6 +621,56 @@ __global__ void k_unpack_pairs(const uint64_t* __restrict__ keys, int64_t count,
   }
 }
 
+// Chung-Lu (expected-degree) workload: vertex i has weight
+// w_i ~ (i + i0)^-alpha, alpha = 1/(gamma-1); both endpoints of every sample
+// are drawn with probability ~ w by the closed-form inverse CDF of the
+// continuous power law, then ids are scrambled like the R-MAT ones.
+// i0 is chosen so that the largest expected degree is ~wmax.
+__global__ void k_chunglu(int logn, double alpha, double i0, double span_lo, double span,
+                          uint64_t sm, int64_t count, int32_t* __restrict__ src,
+                          int32_t* __restrict__ dst) {
+  const double n = (double)(1ull << logn);
+  const double inv = 1.0 / (1.0 - alpha);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix64(sm ^ ((uint64_t)t * 0x9E3779B97F4A7C15ULL));
+    const double ru = ((r >> 11) & ((1ull << 26) - 1)) * (1.0 / 67108864.0) +
+                      (r >> 37) * (1.0 / 67108864.0 / 134217728.0);
+    const uint64_t r2 = mix64(r ^ 0xD1B54A32D192ED03ULL);
+    const double rv = ((r2 >> 11) & ((1ull << 26) - 1)) * (1.0 / 67108864.0) +
+                      (r2 >> 37) * (1.0 / 67108864.0 / 134217728.0);
+    double xu = pow(span_lo + ru * span, inv) - i0;
+    double xv = pow(span_lo + rv * span, inv) - i0;
+    uint32_t u = (uint32_t)fmin(fmax(xu, 0.0), n - 1.0);
+    uint32_t v = (uint32_t)fmin(fmax(xv, 0.0), n - 1.0);
+    src[t] = (int32_t)rmat_scramble(u, logn, sm);
+    dst[t] = (int32_t)rmat_scramble(v, logn, sm);
+  }
+}
+
+int chunglu_generate(int logn, double gamma, double wmax, int64_t count, uint64_t seed,
+                     int32_t* src, int32_t* dst, cudaStream_t st) {
+  const double alpha = 1.0 / (gamma - 1.0);
+  const double n = (double)(1ull << logn);
+  // expected degree of i: 2*count * w_i / sum(w); pick i0 so that i = 0 gets ~wmax
+  // (bisection on i0; sum(w) by the integral of the continuous law)
+  auto mass = [&](double i0) {
+    return (pow(n + i0, 1.0 - alpha) - pow(i0, 1.0 - alpha)) / (1.0 - alpha);
+  };
+  double lo = 1e-3, hi = n;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = sqrt(lo * hi);
+    const double d0 = 2.0 * (double)count * pow(mid, -alpha) / mass(mid);
+    if (d0 > wmax) lo = mid; else hi = mid;
+  }
+  const double i0 = sqrt(lo * hi);
+  const double a = pow(i0, 1.0 - alpha), b = pow(n + i0, 1.0 - alpha);
+  if (count > 0)
+    k_chunglu<<<148 * 16, 256, 0, st>>>(logn, alpha, i0, a, b - a, mix64(seed), count, src, dst);
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
 int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t* dst,
                   cudaStream_t st) {
   if (count > 0) k_rmat<<<148 * 16, 256, 0, st>>>(scale, mix64(seed), count, src, dst);

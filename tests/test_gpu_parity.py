@@ -351,3 +351,46 @@ def test_ooc_infeasible_budget():
     other = make_graph(10, [(0, 1), (1, 2)])
     with pytest.raises(ValueError):
         gs.scan_out_of_core(gs.GraphMeta.from_graph(other), plan, 3, "0.5")
+
+
+def _chunglu(logn, gamma, wmax, count, seed):
+    import ctypes
+
+    import torch
+
+    from paper_2311_12281_b200 import _lib
+
+    lib = _lib.load()
+    src = torch.empty(count, dtype=torch.int32, device="cuda")
+    dst = torch.empty(count, dtype=torch.int32, device="cuda")
+    _lib.check(lib.gs_chunglu_generate(logn, gamma, wmax, count, seed, src.data_ptr(),
+                                       dst.data_ptr(), None))
+    uv = torch.empty(2 * count, dtype=torch.int32, device="cuda")
+    m = ctypes.c_int64(0)
+    _lib.check(lib.gs_normalize_edges(count, src.data_ptr(), dst.data_ptr(), uv.data_ptr(),
+                                      ctypes.byref(m), None))
+    torch.cuda.synchronize()
+    return 1 << logn, uv[: 2 * m.value].cpu().numpy().reshape(-1, 2).copy()
+
+
+@pytest.mark.parametrize("logn,wmax,seed", [(14, 3000, 1), (16, 20000, 2)])
+def test_chunglu_against_oracle(orc, logn, wmax, seed):
+    """BASELINE configs[2] shape at test size: power-law (gamma 2.1) degrees
+    with a few vertices near wmax -> hub bitmap, L2 tables, early exits."""
+    n, e = _chunglu(logn, 2.1, wmax, 12 << logn, seed)
+    deg = np.bincount(e.ravel(), minlength=n)
+    assert deg.max() > wmax // 4 and len(e) > 4 << logn
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.1", 3), ("0.3", 5), ("0.5", 2), ("0.7", 4)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        r_roles, r_cl, _, s = run(g, mu, eps)
+        np.testing.assert_array_equal(r_roles, roles, err_msg=f"{eps} {mu}")
+        np.testing.assert_array_equal(r_cl, cl, err_msg=f"{eps} {mu}")
+        assert s.sim_evals <= g.m and s.probe_bound_violations == 0
+        dmax = int(deg.max())
+        budget = 13 * n + (2 << 20) + 8 * (dmax + 1) + max(2 * g.m // 3 * 4, 8 * 4 * dmax)
+        _, rr, ss = _ooc(g, mu, eps, budget)
+        assert ss.extra["partitions"] >= 2
+        np.testing.assert_array_equal(rr.role_codes, roles, err_msg=f"ooc {eps} {mu}")
+        np.testing.assert_array_equal(rr.cluster_ids, cl, err_msg=f"ooc {eps} {mu}")
