@@ -3,6 +3,9 @@
 // synthetic R-MAT workload generator.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <vector>
+
 #include "engine.cuh"
 
 namespace gs {
@@ -285,28 +288,339 @@ static int finish_rest(gs_engine* e, int64_t n, int64_t m, const int64_t* h_cls,
   return GS_OK;
 }
 
-// generic build tail: sort the 2m arc keys (rank_u, rank_v) -> CSR order
-static int finish_build(gs_engine* e, int64_t n, int64_t m, uint64_t* keys, int B,
-                        uint64_t* keys_alt, int64_t* ndeg, int* d_bad) {
+// ---------------------------------------------------------------------------
+// CSR assembly without a global sort: every arc is scattered straight into its
+// rank-space run (offsets are known from the degrees), then each run is sorted
+// on its own (segmented sort over 4-byte ranks).  This moves 4 B per arc per
+// pass instead of the 8-byte (rank_u, rank_v) keys of a 6-pass global radix
+// sort, and needs 2 x 4 B x 2m of scratch instead of 2 x 8 B x 2m.
+
+// Edge input: rank-space arcs (ru -> rv) and (rv -> ru) of every valid pair.
+// Sorted input puts consecutive pairs on the same u, so the u-side cursor
+// increments are warp-aggregated (match_any + one atomic per group).
+__global__ void k_scatter_edges(const int32_t* __restrict__ uv, int64_t m, int64_t n,
+                                const int32_t* __restrict__ rank,
+                                unsigned long long* __restrict__ cur,
+                                int32_t* __restrict__ out) {
+  // cur[r] starts at off[r]: the atomic returns the absolute slot
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t mm = (m + 31) / 32 * 32;
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < mm; k += stride) {
+    const bool in = k < m;
+    const int2 p = in ? reinterpret_cast<const int2*>(uv)[k] : make_int2(-1, -1);
+    const bool ok = in && !(p.x < 0 || p.y < 0 || p.x >= n || p.y >= n || p.x == p.y);
+    const int32_t ru = ok ? rank[p.x] : -1 - lane;
+    const int32_t rv = ok ? rank[p.y] : -1 - lane;
+    const unsigned gu = __match_any_sync(0xffffffffu, ru);
+    const unsigned gv = __match_any_sync(0xffffffffu, rv);
+    unsigned long long bu = 0, bv = 0;
+    if (ok && lane == __ffs(gu) - 1) bu = atomicAdd(&cur[ru], (unsigned long long)__popc(gu));
+    if (ok && lane == __ffs(gv) - 1) bv = atomicAdd(&cur[rv], (unsigned long long)__popc(gv));
+    bu = __shfl_sync(0xffffffffu, bu, __ffs(gu) - 1);
+    bv = __shfl_sync(0xffffffffu, bv, __ffs(gv) - 1);
+    if (ok) {
+      out[bu + __popc(gu & below)] = rv;
+      out[bv + __popc(gv & below)] = ru;
+    }
+  }
+}
+
+// CSR input: slot i of caller vertex u lands at the same position of u's
+// rank-space run (no atomics); validates ids and the strictly increasing runs.
+__global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n,
+                              const int32_t* __restrict__ adj, int64_t slots,
+                              const int32_t* __restrict__ rank,
+                              const int64_t* __restrict__ noff, int32_t* __restrict__ out,
+                              int* __restrict__ bad) {
+  const int64_t base = blockIdx.x * (int64_t)blockDim.x;
+  const int64_t i = base + threadIdx.x;
+  __shared__ int64_t vlo, vhi;
+  if (threadIdx.x == 0) {
+    int64_t last = base + blockDim.x - 1;
+    if (last >= slots) last = slots - 1;
+    vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
+    vhi = upper_bound_i64(off, 0, n + 1, last);
+  }
+  __syncthreads();
+  if (i >= slots) return;
+  const int64_t u = upper_bound_i64(off, vlo, vhi, i) - 1;
+  int32_t v = adj[i];
+  if (v < 0 || v >= n || v == u) { atomicExch(bad, 3); v = (int32_t)u; }
+  if (i > off[u] && adj[i - 1] >= v) atomicExch(bad, 4);  // runs strictly increasing
+  const int32_t ru = rank[u];
+  out[noff[ru] + (i - off[u])] = rank[v];
+}
+
+// ---------------------------------------------------------------------------
+// Per-run sorts, in place.  Degrees ascend with the rank, so each size class
+// is a contiguous rank range: [2, 32] one warp per run (register bitonic
+// network over shuffles), (32, 256] one warp per run (bitonic in a 1 KB
+// shared-memory slice), (256, 4096) one CTA per run (bitonic in shared
+// memory), >= 4096 (a few thousand hub runs holding a large share of the
+// arcs) one radix sort over (run, neighbour) keys.  A repeated neighbour
+// after sorting is a duplicate undirected edge (bad = 5).
+
+static constexpr int32_t kPad = 0x7fffffff;
+
+// first rank whose degree is >= x (degrees are non-decreasing in rank)
+__device__ __forceinline__ int64_t rank_of_degree(const int64_t* off, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid + 1] - off[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t n,
+                               int64_t* __restrict__ out) {
+  const int64_t th[5] = {2, 33, 257, 1025, 4096};
+  const int c = threadIdx.x;
+  if (c < 5) out[c] = rank_of_degree(off, n, th[c]);
+}
+
+__global__ void __launch_bounds__(256) k_sort_runs_reg(const int64_t* __restrict__ off,
+                                                       int64_t rlo, int64_t rhi,
+                                                       int32_t* __restrict__ arcs,
+                                                       int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = rlo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); v < rhi;
+       v += nw) {
+    const int64_t o = off[v];
+    const int d = (int)(off[v + 1] - o);
+    int32_t x = lane < d ? arcs[o + lane] : kPad;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        const bool up = (lane & k) == 0, low = (lane & j) == 0;
+        x = (low == up) ? min(x, y) : max(x, y);
+      }
+    }
+    const int32_t nx = __shfl_down_sync(0xffffffffu, x, 1);
+    if (lane < d) {
+      arcs[o + lane] = x;
+      if (lane + 1 < d && nx == x) atomicExch(bad, 5);
+    }
+  }
+}
+
+// bitonic sort of s[0, P) (P a power of two) by the `nt` threads of a group
+template <bool BLOCK>
+__device__ __forceinline__ void bitonic_smem(int32_t* s, int P, int t, int nt) {
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = t; i < (P >> 1); i += nt) {
+        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
+        const int32_t a = s[lo], b = s[hi];
+        if ((a > b) == ((lo & k) == 0)) { s[lo] = b; s[hi] = a; }
+      }
+      if (BLOCK) __syncthreads(); else __syncwarp();
+    }
+  }
+}
+
+template <bool BLOCK, int CAP>
+__global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restrict__ off,
+                                                        int64_t rlo, int64_t rhi,
+                                                        int32_t* __restrict__ arcs,
+                                                        int* __restrict__ bad) {
+  __shared__ int32_t buf[BLOCK ? CAP : 8 * CAP];
+  const int nt = BLOCK ? blockDim.x : 32;
+  const int t = BLOCK ? threadIdx.x : (threadIdx.x & 31);
+  int32_t* s = BLOCK ? buf : buf + (threadIdx.x >> 5) * CAP;
+  const int64_t groups = BLOCK ? gridDim.x : ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t g0 = BLOCK ? blockIdx.x : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  for (int64_t v = rlo + g0; v < rhi; v += groups) {
+    const int64_t o = off[v];
+    const int d = (int)(off[v + 1] - o);
+    int P = 1;
+    while (P < d) P <<= 1;
+    for (int i = t; i < P; i += nt) s[i] = i < d ? arcs[o + i] : kPad;
+    if (BLOCK) __syncthreads(); else __syncwarp();
+    bitonic_smem<BLOCK>(s, P, t, nt);
+    bool dup = false;
+    for (int i = t; i < d; i += nt) {
+      arcs[o + i] = s[i];
+      dup |= (i + 1 < d && s[i + 1] == s[i]);
+    }
+    if (dup) atomicExch(bad, 5);
+    if (BLOCK) __syncthreads(); else __syncwarp();
+  }
+}
+
+// one CTA per run of up to 256*ITEMS neighbours: block radix sort over the
+// rank bits (+ one bit that sends the padding to the end)
+template <int ITEMS>
+__global__ void __launch_bounds__(256) k_sort_runs_block(const int64_t* __restrict__ off,
+                                                         int64_t rlo, int64_t rhi, int endbit,
+                                                         int32_t* __restrict__ arcs,
+                                                         int* __restrict__ bad) {
+  using Sort = cub::BlockRadixSort<uint32_t, 256, ITEMS>;
+  __shared__ typename Sort::TempStorage tmp;
+  __shared__ int s_dup;
+  const int t = threadIdx.x;
+  if (t == 0) s_dup = 0;
+  for (int64_t v = rlo + blockIdx.x; v < rhi; v += gridDim.x) {
+    const int64_t o = off[v];
+    const int d = (int)(off[v + 1] - o);
+    uint32_t k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {  // striped load; the sort ignores input order
+      const int idx = i * 256 + t;
+      k[i] = idx < d ? (uint32_t)arcs[o + idx] : 0xFFFFFFFFu;
+    }
+    Sort(tmp).SortBlockedToStriped(k, 0, endbit);
+    bool dup = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * 256 + t;
+      if (idx < d) arcs[o + idx] = (int32_t)k[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * 256 + t;
+      if (idx + 1 < d) dup |= arcs[o + idx] == arcs[o + idx + 1];
+    }
+    if (dup) s_dup = 1;
+    __syncthreads();
+  }
+  if (t == 0 && s_dup) atomicExch(bad, 5);
+}
+
+// composite keys (run index within the tail, neighbour) of the long runs
+__global__ void k_tail_keys(const int64_t* __restrict__ off, int64_t rlo, int64_t rhi,
+                            const int32_t* __restrict__ arcs, int B,
+                            uint64_t* __restrict__ keys) {
+  const int64_t base = off[rlo];
+  for (int64_t v = rlo + blockIdx.x; v < rhi; v += gridDim.x) {
+    const uint64_t hi = (uint64_t)(v - rlo) << B;
+    for (int64_t i = off[v] + threadIdx.x; i < off[v + 1]; i += blockDim.x)
+      keys[i - base] = hi | (uint64_t)(uint32_t)arcs[i];
+  }
+}
+
+__global__ void k_tail_extract(const uint64_t* __restrict__ keys, int64_t cnt, int B,
+                               int32_t* __restrict__ out, int* __restrict__ bad) {
+  const uint64_t mask = (uint64_t(1) << B) - 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    out[i] = (int32_t)(k & mask);
+    if (i > 0 && keys[i - 1] == k) atomicExch(bad, 5);
+  }
+}
+
+// Sort every run of `arcs` (offsets g.off) in place.
+static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
-  const int64_t slots = 2 * m;
-  cub::DoubleBuffer<uint64_t> db(keys, keys_alt);
-  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, db, slots, 0, 2 * B, st);
-  }));
-  uint64_t* sorted = db.Current();
-  GS_TRY(e->alloc_n(&g.adj, slots));
-  if (slots > 0) {
-    k_extract_adj<<<e->sms * 16, 256, 0, st>>>(sorted, slots, B, g.adj, d_bad);
+  if (slots == 0 || n == 0) return GS_OK;
+  int64_t* d_cls = nullptr;
+  GS_TRY(e->alloc_n(&d_cls, 5));
+  k_sort_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
+  int64_t r[5], hbig = 0;
+  GS_CUDA(cudaMemcpyAsync(r, d_cls, sizeof(r), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(d_cls);
+  e->launches++;
+  const int64_t r2 = r[0], r33 = r[1], r257 = r[2], r1025 = r[3], rbig = r[4];
+  auto warps_grid = [&](int64_t runs) {
+    const int64_t gr = (runs + 7) / 8;
+    return (unsigned)(gr < (int64_t)e->sms * 64 ? gr : (int64_t)e->sms * 64);
+  };
+  auto blocks_grid = [&](int64_t runs) {
+    return (unsigned)(runs < (int64_t)e->sms * 16 ? runs : (int64_t)e->sms * 16);
+  };
+  const int endbit = std::min(32, bits_for(n - 1) + 1);
+  if (r33 > r2) {
+    k_sort_runs_reg<<<warps_grid(r33 - r2), 256, 0, st>>>(g.off, r2, r33, arcs, d_bad);
     e->launches++;
   }
-  e->release(keys);
-  e->release(keys_alt);
-  int64_t h_cls[DevGraph::kClasses + 1];
+  if (r257 > r33) {
+    k_sort_runs_smem<false, 256><<<warps_grid(r257 - r33), 256, 0, st>>>(g.off, r33, r257, arcs,
+                                                                        d_bad);
+    e->launches++;
+  }
+  if (r1025 > r257) {
+    k_sort_runs_block<4><<<blocks_grid(r1025 - r257), 256, 0, st>>>(g.off, r257, r1025, endbit,
+                                                                   arcs, d_bad);
+    e->launches++;
+  }
+  if (rbig > r1025) {
+    k_sort_runs_block<16><<<blocks_grid(rbig - r1025), 256, 0, st>>>(g.off, r1025, rbig, endbit,
+                                                                    arcs, d_bad);
+    e->launches++;
+  }
+  GS_CUDA(cudaGetLastError());
+  // long runs
+  GS_CUDA(cudaMemcpyAsync(&hbig, g.off + rbig, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  const int64_t cnt = slots - hbig;
+  if (cnt > 0) {
+    const int B = bits_for(n - 1);
+    const int R = bits_for(n - 1 - rbig);
+    uint64_t *k1 = nullptr, *k2 = nullptr;
+    GS_TRY(e->alloc_n(&k1, cnt));
+    GS_TRY(e->alloc_n(&k2, cnt));
+    const int64_t nv = n - rbig;
+    k_tail_keys<<<(unsigned)(nv < 65535 * 4 ? nv : 65535 * 4), 256, 0, st>>>(g.off, rbig, n, arcs,
+                                                                            B, k1);
+    cub::DoubleBuffer<uint64_t> db(k1, k2);
+    GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, B + R, st);
+    }));
+    k_tail_extract<<<e->sms * 16, 256, 0, st>>>(db.Current(), cnt, B, arcs + hbig, d_bad);
+    e->launches += 3;
+    e->release(k1);
+    e->release(k2);
+  }
+  return GS_OK;
+}
+
+// shared tail: arcs scattered into their runs (`arcs`, 2m) -> sorted CSR
+static int finish_scatter_build(gs_engine* e, int64_t n, int64_t m, int32_t* arcs,
+                                const int64_t* h_cls, int* d_bad) {
+  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad));
+  e->g.adj = arcs;
+  return finish_rest(e, n, m, h_cls, d_bad);
+}
+
+// degrees -> (degree, id) order: orig[rank], rank[orig], rank-space offsets
+static int rank_and_offsets(gs_engine* e, int64_t n, uint32_t* deg, int64_t* h_cls) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  uint64_t *vk = nullptr, *vk2 = nullptr;
+  GS_TRY(e->alloc_n(&vk, n));
+  GS_TRY(e->alloc_n(&vk2, n));
+  if (n > 0) {
+    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
+    e->launches++;
+  }
+  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
+  }));
+  int64_t* ndeg = nullptr;
+  GS_TRY(e->alloc_n(&g.orig, n));
+  GS_TRY(e->alloc_n(&g.rank, n));
+  GS_TRY(e->alloc_n(&ndeg, n + 1));
+  if (n > 0) {
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, g.rank, ndeg);
+    e->launches++;
+  } else {
+    GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
+  }
+  e->release(vk);
+  e->release(vk2);
   GS_TRY(finish_offsets(e, n, ndeg, h_cls));
   e->release(ndeg);
-  return finish_rest(e, n, m, h_cls, d_bad);
+  return GS_OK;
 }
 
 int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
@@ -323,40 +637,21 @@ int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
     k_count_deg_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, n, deg, d_bad);
     e->launches++;
   }
-  uint64_t *vk = nullptr, *vk2 = nullptr;
-  GS_TRY(e->alloc_n(&vk, n));
-  GS_TRY(e->alloc_n(&vk2, n));
-  if (n > 0) {
-    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
-    e->launches++;
-  }
-  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
-  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
-  }));
-  int64_t* ndeg = nullptr;
-  GS_TRY(e->alloc_n(&g.orig, n));
-  GS_TRY(e->alloc_n(&g.rank, n));
-  int32_t* rank = g.rank;
-  GS_TRY(e->alloc_n(&ndeg, n + 1));
-  if (n > 0) {
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, rank, ndeg);
-    e->launches++;
-  } else {
-    GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
-  }
-  e->release(vk);
-  e->release(vk2);
+  int64_t h_cls[DevGraph::kClasses + 1];
+  GS_TRY(rank_and_offsets(e, n, deg, h_cls));
   e->release(deg);
-  const int B = bits_for(n > 0 ? n - 1 : 0);
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  GS_TRY(e->alloc_n(&keys, 2 * m));
-  GS_TRY(e->alloc_n(&keys2, 2 * m));
+  unsigned long long* cur = nullptr;
+  GS_TRY(e->alloc_n(&cur, n));
+  if (n > 0)
+    GS_CUDA(cudaMemcpyAsync(cur, g.off, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, st));
+  int32_t* arcs = nullptr;
+  GS_TRY(e->alloc_n(&arcs, 2 * m));
   if (m > 0) {
-    k_arc_keys_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, rank, B, keys);
+    k_scatter_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, n, g.rank, cur, arcs);
     e->launches++;
   }
-  return finish_build(e, n, m, keys, B, keys2, ndeg, d_bad);
+  e->release(cur);
+  return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
 }
 
 int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
@@ -373,41 +668,17 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     k_deg_from_off<<<grid_for(n, 256), 256, 0, st>>>(off, n, deg, d_bad);
     e->launches++;
   }
-  uint64_t *vk = nullptr, *vk2 = nullptr;
-  GS_TRY(e->alloc_n(&vk, n));
-  GS_TRY(e->alloc_n(&vk2, n));
-  if (n > 0) {
-    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
-    e->launches++;
-  }
-  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
-  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
-  }));
-  int64_t* ndeg = nullptr;
-  GS_TRY(e->alloc_n(&g.orig, n));
-  GS_TRY(e->alloc_n(&g.rank, n));
-  int32_t* rank = g.rank;
-  GS_TRY(e->alloc_n(&ndeg, n + 1));
-  if (n > 0) {
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, rank, ndeg);
-    e->launches++;
-  } else {
-    GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
-  }
-  e->release(vk);
-  e->release(vk2);
+  int64_t h_cls[DevGraph::kClasses + 1];
+  GS_TRY(rank_and_offsets(e, n, deg, h_cls));
   e->release(deg);
-  const int B = bits_for(n > 0 ? n - 1 : 0);
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  GS_TRY(e->alloc_n(&keys, 2 * m));
-  GS_TRY(e->alloc_n(&keys2, 2 * m));
+  int32_t* arcs = nullptr;
+  GS_TRY(e->alloc_n(&arcs, 2 * m));
   if (m > 0) {
-    k_arc_keys_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 2 * m, rank, B, keys,
-                                                         d_bad);
+    k_scatter_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 2 * m, g.rank, g.off, arcs,
+                                                        d_bad);
     e->launches++;
   }
-  return finish_build(e, n, m, keys, B, keys2, ndeg, d_bad);
+  return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ d, int64_t n, int64_t* __restrict__ o) {
