@@ -244,8 +244,11 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
                                               uint32_t rmax, const Cuckoo& C, int nstash,
                                               const int32_t* __restrict__ nb, int64_t nlo,
                                               int lane, int32_t& scanned, uint32_t first) {
-  const int32_t* __restrict__ na = a_run + (da - 1);  // walk downwards
-  const int32_t need_miss = da - cmin + 1;            // misses that decide "dissimilar"
+  // Element j (0 = the top of N(a)) is a_run[da - 1 - j]; in a step based at
+  // element s, lane l reads j = s + 32u + l for u < cu: one base pointer per
+  // step, the four loads use immediate offsets.
+  const int32_t* __restrict__ top = a_run + (da - 1 - lane);
+  const int32_t need_miss = da - cmin + 1;  // misses that decide "dissimilar"
   // Any decision reads at least min(need_miss - misses, cmin - hits) more
   // elements, so a step of that many (rounded up to 32, at most 128) never
   // over-reads except in its last 31 slots; the next step is prefetched only
@@ -255,10 +258,11 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
   for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
   cur[0] = first;
   int32_t cu = min(4, max(1, (min(need_miss, cmin) + 31) >> 5));
+  {
+    const int32_t rem = da - lane;
 #pragma unroll
-  for (int u = 1; u < 4; ++u) {
-    const int32_t idx = u * 32 + lane;
-    if (u < cu && idx < da) cur[u] = (uint32_t)__ldg(na - idx);
+    for (int u = 1; u < 4; ++u)
+      if (u < cu && 32 * u < rem) cur[u] = (uint32_t)__ldg(top - 32 * u);
   }
   int32_t c = 0;
   scanned = 0;
@@ -269,12 +273,12 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
     const bool pre = rest > 0 && nbase < da;
     int32_t nu = 0;
     if (pre) {
-      nu = min(4, max(1, (rest + 31) >> 5));
+      nu = min(4, (rest + 31) >> 5);
+      const int32_t* __restrict__ q = top - nbase;
+      const int32_t rem = da - nbase - lane;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int32_t idx = nbase + u * 32 + lane;
-        nxt[u] = (u < nu && idx < da) ? (uint32_t)__ldg(na - idx) : kPast;
-      }
+      for (int u = 0; u < 4; ++u)
+        nxt[u] = (u < nu && 32 * u < rem) ? (uint32_t)__ldg(q - 32 * u) : kPast;
     }
     const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
     uint32_t hits = 0;
@@ -299,11 +303,11 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
       cu = nu;
     } else {
       cu = min(4, max(1, (min(need_miss - (scanned - c), cmin - c) + 31) >> 5));
+      const int32_t* __restrict__ q = top - scanned;
+      const int32_t rem = da - scanned - lane;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int32_t idx = scanned + u * 32 + lane;
-        cur[u] = (u < cu && idx < da) ? (uint32_t)__ldg(na - idx) : kPast;
-      }
+      for (int u = 0; u < 4; ++u)
+        cur[u] = (u < cu && 32 * u < rem) ? (uint32_t)__ldg(q - 32 * u) : kPast;
     }
   }
 }
