@@ -92,7 +92,7 @@ typedef struct gs_stats {
   int64_t alg_bytes_sim;          /* SURVEY 8(d) W_sim of the similarity pass */
   int64_t n_core, n_member, n_hub, n_outlier, n_clusters;
   int64_t partitions;             /* out-of-core / sharded passes */
-  int64_t kernel_launches;        /* kernels launched by this call */
+  int64_t kernel_launches;        /* kernels launched (gs_engine_scan: load + scan) */
   int64_t peak_device_bytes;      /* high-water mark of engine allocations */
   double phase_ms[GS_PH_COUNT];
 } gs_stats;

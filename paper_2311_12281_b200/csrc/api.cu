@@ -302,7 +302,6 @@ int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_
   GS_TRY(check_eps(eps2));
   GS_CUDA(cudaSetDevice(e->device));
   if (stats) memset(stats, 0, sizeof(*stats));
-  const int64_t launches0 = e->launches;
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0); cudaEventCreate(&t1);
   cudaEventRecord(t0, e->stream);
@@ -315,7 +314,7 @@ int gs_engine_scan(gs_engine* e, int32_t mu, const gs_eps2* eps2, uint8_t* role_
     stats->phase_ms[GS_PH_TOTAL] = ms;
     stats->phase_ms[GS_PH_H2D] = e->last_h2d_ms;
     stats->phase_ms[GS_PH_BUILD] = e->last_build_ms;
-    stats->kernel_launches = e->launches - launches0;
+    stats->kernel_launches = e->launches;  // since the last load: build + scan
     stats->peak_device_bytes = (int64_t)e->peak;
   }
   cudaEventDestroy(t0); cudaEventDestroy(t1);
