@@ -144,6 +144,24 @@ int gs_engine_phase_attach(gs_engine* e, int32_t* labels_dev);
 int gs_engine_phase_finish(gs_engine* e, const int32_t* labels_dev, uint8_t* role_out,
                            int32_t* cluster_out, int out_on_device, gs_stats* stats);
 
+/* The engine's scan state in the reference ClusterState layout (scan.py:87-134),
+ * host buffers indexed by caller ids (any may be NULL): lower/upper [n] i32
+ * (Lemma-1 bounds incl. the vertex itself), role [n] u8 (internal codes
+ * 0..6), parent [n] i32 (canonical cluster label, -1 hub, -2 none), and per
+ * oriented edge sim [m] u8 (SIM_*) with its caller-id pair edge_pairs [2m]
+ * (low-(degree, id) endpoint first; the host maps them onto the reference
+ * edge_list order).  stage: 0 after the identify phase (gs_engine_phase_
+ * resolve), 1 after the cluster phases (gs_engine_phase_attach), 2 after
+ * gs_engine_phase_finish.  Replaces direct access to ClusterState fields
+ * (scan.py:87-107) for callers of identify_core / detect_clusters /
+ * classify_hub_outlier (scan.py:452, 701, 832). */
+int gs_engine_export_state(gs_engine* e, int stage, int32_t* lower, int32_t* upper,
+                           uint8_t* role, int32_t* parent, uint8_t* sim, int32_t* edge_pairs);
+/* Counters and per-phase device times of the engine's scan so far (the
+ * StatsReport of identify_core / detect_clusters / classify_hub_outlier
+ * called one at a time, scan.py:488-492). */
+int gs_engine_phase_stats(gs_engine* e, gs_stats* stats);
+
 /* One-shot calls (temporary engine on the current device). */
 int gs_scan_csr(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
                 int32_t mu, const gs_eps2* eps2, uint8_t* role_out,

@@ -92,6 +92,8 @@ SIGNATURES = [
      [_I64, _I64, _P, _I32, ctypes.POINTER(GsEps2), _P, _P, ctypes.POINTER(GsStats)]),
     ("gs_build_graph", ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P]),
     ("gs_build_csr_device", ctypes.c_int, [_I64, _I64, _P, _P, _P, _P]),
+    ("gs_engine_phase_stats", ctypes.c_int, [_P, ctypes.POINTER(GsStats)]),
+    ("gs_engine_export_state", ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P, _P]),
     ("gs_engine_check_sim", ctypes.c_int, [_P, _I64, _P, _P, ctypes.POINTER(GsEps2), _P]),
     ("gs_scan_partitioned", ctypes.c_int,
      [_I64, _I64, _P, _P, _I32, ctypes.POINTER(GsEps2), ctypes.c_uint64, _P, _P,

@@ -498,6 +498,26 @@ int gs_build_csr_device(int64_t n, int64_t m, const int32_t* edges_dev, int64_t*
   return rc;
 }
 
+int gs_engine_phase_stats(gs_engine* e, gs_stats* stats) {
+  GS_TRY(phase_guard(e));
+  if (!stats) return GS_OK;
+  memset(stats, 0, sizeof(*stats));
+  GS_TRY(read_counters(e, stats));
+  stats->kernel_launches = e->launches;
+  stats->peak_device_bytes = (int64_t)e->peak;
+  for (int i = 0; i < GS_PH_COUNT; ++i) stats->phase_ms[i] = e->phase_ms[i];
+  stats->phase_ms[GS_PH_H2D] = e->last_h2d_ms;
+  stats->phase_ms[GS_PH_BUILD] = e->last_build_ms;
+  return GS_OK;
+}
+
+int gs_engine_export_state(gs_engine* e, int stage, int32_t* lower, int32_t* upper,
+                           uint8_t* role, int32_t* parent, uint8_t* sim, int32_t* edge_pairs) {
+  GS_TRY(phase_guard(e));
+  if (stage < 0 || stage > 2) { set_error("stage must be 0, 1 or 2"); return GS_EINVAL; }
+  return export_state(e, stage, lower, upper, role, parent, sim, edge_pairs);
+}
+
 int gs_engine_check_sim(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,
                         const gs_eps2* eps2, int8_t* out) {
   if (!e) { set_error("engine is NULL"); return GS_EINVAL; }

@@ -553,10 +553,22 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     if (d_role_out) e->release(d_role_out);
     if (d_cluster_out) e->release(d_cluster_out);
   }
+  if (n > 0)  // final roles stay on the device (state export, scan.py ClusterState.role)
+    GS_CUDA(cudaMemcpyAsync(s.role, fin, (size_t)n, cudaMemcpyDeviceToDevice, str));
+  GS_CUDA(cudaStreamSynchronize(str));
   e->release(fin);
   if (st) {
     float d2h = 0;
     cudaEventElapsedTime(&d2h, c0, c1);
+    fill_counters(st, n, m, h);
+    st->phase_ms[GS_PH_D2H] = d2h;
+  }
+  cudaEventDestroy(c0);
+  cudaEventDestroy(c1);
+  return GS_OK;
+}
+
+void fill_counters(gs_stats* st, int64_t n, int64_t m, const unsigned long long* h) {
     st->n = n;
     st->m = m;
     st->sim_evals = (int64_t)h[CTR_SIM_EVALS];
@@ -571,10 +583,15 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     st->n_hub = (int64_t)h[CTR_N_HUB];
     st->n_outlier = (int64_t)h[CTR_N_OUTLIER];
     st->n_clusters = (int64_t)h[CTR_N_CLUSTERS];
-    st->phase_ms[GS_PH_D2H] = d2h;
+}
+
+int read_counters(gs_engine* e, gs_stats* st) {
+  unsigned long long h[CTR_COUNT] = {0};
+  if (e->s.ctr) {
+    GS_CUDA(cudaMemcpyAsync(h, e->s.ctr, sizeof(h), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
   }
-  cudaEventDestroy(c0);
-  cudaEventDestroy(c1);
+  fill_counters(st, e->g.n, e->g.m, h);
   return GS_OK;
 }
 
@@ -602,6 +619,111 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     st->phase_ms[GS_PH_CLUSTER] = tm.ms(2, 3);
     st->phase_ms[GS_PH_CLASSIFY] = tm.ms(4, 5) - st->phase_ms[GS_PH_D2H];
   }
+  return GS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// ClusterState export (scan.py:87-134): the device state re-expressed in the
+// reference's per-vertex layout, indexed by caller ids.
+//   stage 0 (after identify_core): lower/upper, role core|noncore, parent -2
+//   stage 1 (after detect_clusters): + members (3, shared 4), parent = the
+//            canonical cluster label (a core id; its own parent)
+//   stage 2 (after classify_hub_outlier): + hubs (5, parent -1), outliers (6)
+__global__ void k_export_vertices(int64_t n, int stage, const int32_t* __restrict__ orig,
+                                  const uint64_t* __restrict__ bounds,
+                                  const uint8_t* __restrict__ role,
+                                  const int32_t* __restrict__ lmin,
+                                  const int32_t* __restrict__ lmax, int32_t* __restrict__ lower,
+                                  int32_t* __restrict__ upper, uint8_t* __restrict__ role_out,
+                                  int32_t* __restrict__ parent_out) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t o = orig[v];
+    const uint64_t b = bounds[v];
+    lower[o] = (int32_t)(uint32_t)b;
+    upper[o] = (int32_t)(uint32_t)(b >> 32);
+    uint8_t r = role[v];
+    int32_t par = -2;
+    if (stage >= 1) {
+      const bool clustered = lmin[v] != 0x7fffffff;
+      if (stage == 1 && r == ROLE_NONCORE && clustered) r = ROLE_MEMBER;
+      if (r == ROLE_MEMBER && lmin[v] != lmax[v]) r = 4;  // ROLE_MEMBER_SHARED
+      if (r == ROLE_CORE || r == ROLE_MEMBER || r == 4) par = lmin[v];
+      else if (r == ROLE_HUB) par = -1;
+    }
+    role_out[o] = r;
+    parent_out[o] = par;
+  }
+}
+
+// per oriented edge: status (O(1)-decided edges, folded into the initial
+// bounds by the pre-pass, get their status here) and the caller-id pair
+__global__ void k_export_edges(int64_t m, const int32_t* __restrict__ elo,
+                               const int32_t* __restrict__ ehi, const int32_t* __restrict__ orig,
+                               const int64_t* __restrict__ off, const int2* __restrict__ thr,
+                               const uint8_t* __restrict__ sim, uint8_t* __restrict__ sim_out,
+                               int32_t* __restrict__ pairs) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = elo[e], b = ehi[e];
+    uint8_t st = sim[e];
+    if (st == SIM_UNKNOWN && thr) {
+      const int64_t da = off[a + 1] - off[a], db = off[b + 1] - off[b];
+      const int2 t = thr[db];
+      if (da + 1 < t.x) st = SIM_DISSIMILAR;
+      else if (da <= t.y) st = SIM_SIMILAR;
+    }
+    if (sim_out) sim_out[e] = st;
+    if (pairs) {
+      pairs[2 * e] = orig[a];
+      pairs[2 * e + 1] = orig[b];
+    }
+  }
+}
+
+int export_state(gs_engine* e, int stage, int32_t* lower, int32_t* upper, uint8_t* role,
+                 int32_t* parent, uint8_t* sim, int32_t* pairs) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  cudaStream_t str = e->stream;
+  const int64_t n = g.n, m = g.m;
+  if (!s.bounds) { set_error("no scan state: run the identify phase first"); return GS_EINVAL; }
+  if (n > 0 && (lower || upper || role || parent)) {
+    int32_t *dl = nullptr, *du = nullptr, *dp = nullptr;
+    uint8_t* dr = nullptr;
+    GS_TRY(e->alloc_n(&dl, n));
+    GS_TRY(e->alloc_n(&du, n));
+    GS_TRY(e->alloc_n(&dp, n));
+    GS_TRY(e->alloc_n(&dr, n));
+    k_export_vertices<<<gridv(e, n), 256, 0, str>>>(n, stage, g.orig, s.bounds, s.role, s.lmin,
+                                                    s.lmax, dl, du, dr, dp);
+    e->launches++;
+    if (lower) GS_CUDA(cudaMemcpyAsync(lower, dl, 4 * (size_t)n, cudaMemcpyDeviceToHost, str));
+    if (upper) GS_CUDA(cudaMemcpyAsync(upper, du, 4 * (size_t)n, cudaMemcpyDeviceToHost, str));
+    if (parent) GS_CUDA(cudaMemcpyAsync(parent, dp, 4 * (size_t)n, cudaMemcpyDeviceToHost, str));
+    if (role) GS_CUDA(cudaMemcpyAsync(role, dr, (size_t)n, cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+    e->release(dl);
+    e->release(du);
+    e->release(dp);
+    e->release(dr);
+  }
+  if (m > 0 && (sim || pairs)) {
+    uint8_t* ds = nullptr;
+    int32_t* dpairs = nullptr;
+    if (sim) GS_TRY(e->alloc_n(&ds, m));
+    if (pairs) GS_TRY(e->alloc_n(&dpairs, 2 * m));
+    k_export_edges<<<gridv(e, m), 256, 0, str>>>(m, g.elo, g.ehi, g.orig, g.off, s.thr, s.sim, ds,
+                                                 dpairs);
+    e->launches++;
+    if (sim) GS_CUDA(cudaMemcpyAsync(sim, ds, (size_t)m, cudaMemcpyDeviceToHost, str));
+    if (pairs) GS_CUDA(cudaMemcpyAsync(pairs, dpairs, 8 * (size_t)m, cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+    if (ds) e->release(ds);
+    if (dpairs) e->release(dpairs);
+  }
+  GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
 

@@ -169,6 +169,10 @@ int phase_export_labels(gs_engine* e, int32_t* labels);
 int phase_import_labels(gs_engine* e, const int32_t* labels);
 int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_on_device,
                  gs_stats* st);
+void fill_counters(gs_stats* st, int64_t n, int64_t m, const unsigned long long* h);
+int read_counters(gs_engine* e, gs_stats* st);
+int export_state(gs_engine* e, int stage, int32_t* lower, int32_t* upper, uint8_t* role,
+                 int32_t* parent, uint8_t* sim, int32_t* pairs);
 // owner of the edges of high endpoint b
 __host__ __device__ __forceinline__ bool owns(int64_t b, int rank, int world) {
   return world == 1 || (int)(b % world) == rank;

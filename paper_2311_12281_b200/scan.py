@@ -341,3 +341,259 @@ def structural_similarity(g, u: int, v: int) -> float:
     adjacent = bool(np.any(nu == v))
     inter = common + (2 if adjacent else 0)
     return inter / ((len(nu) + 1) * (len(nv) + 1)) ** 0.5
+
+
+# --- phase-level API (scan.py:87-134, 390-412, 452-564, 701-852, 950-962) -----
+#
+# The reference exposes its three phases over a mutable ClusterState.  Here
+# the state lives on the device (the engine that ran the phase); the host
+# arrays of ClusterState are a snapshot exported after each phase
+# (gs_engine_export_state) in the reference layout, indexed by caller ids.
+# find_root / union_roots are the reference's host utilities over those
+# arrays (the device clustering uses its own lock-free union-find).
+
+
+class SimilarityStatus(int, Enum):
+    UNKNOWN = SIM_UNKNOWN
+    SIMILAR = SIM_SIMILAR
+    DISSIMILAR = SIM_DISSIMILAR
+
+
+@dataclass
+class ClusterState:
+    """Working state shared by the phases (scan.py:87-107): ``lower``/``upper``
+    bound the similar-neighbourhood size (both include the vertex), ``parent``
+    is the cluster forest (vertex id; -1 hub; -2 none), ``height`` the
+    union-by-height rank, ``sim`` one status byte per edge of ``edge_list``."""
+
+    n: int
+    m: int
+    lower: np.ndarray
+    upper: np.ndarray
+    role: np.ndarray
+    parent: np.ndarray
+    height: np.ndarray
+    sim: np.ndarray
+    _engine: Optional[_lib.Engine] = field(default=None, repr=False, compare=False)
+    _stage: int = field(default=-1, repr=False, compare=False)  # last finished phase
+    _mu: int = field(default=0, repr=False, compare=False)
+    _eps: Optional[Fraction] = field(default=None, repr=False, compare=False)
+
+
+def init_vertex_state(n: int, degrees, m: int, with_sim: bool) -> ClusterState:
+    """scan.py:117-134: lower=1, upper=deg+1, role/sim unknown, parent=-2."""
+    deg = np.asarray(degrees, dtype=np.int64).reshape(-1)
+    if deg.shape[0] != n:
+        raise ValueError(f"{deg.shape[0]} degrees for {n} vertices")
+    return ClusterState(
+        n=int(n), m=int(m),
+        lower=np.ones(n, dtype=np.int32),
+        upper=(deg + 1).astype(np.int32),
+        role=np.zeros(n, dtype=np.uint8),
+        parent=np.full(n, PARENT_NONE, dtype=np.int32),
+        height=np.ones(n, dtype=np.int32),
+        sim=np.zeros(m if with_sim else 0, dtype=np.uint8),
+    )
+
+
+def init_state(g) -> ClusterState:
+    """scan.py:110-114: fresh state for graph ``g``."""
+    n, m, off, _ = graph_arrays(g)
+    return init_vertex_state(n, np.diff(off) if n else np.empty(0, np.int64), m, True)
+
+
+def _export(g, st: ClusterState, stage: int) -> None:
+    """Device state -> the host arrays of ``st`` (reference layout)."""
+    n, m = st.n, st.m
+    lib = _lib.load()
+    lower = np.empty(n, np.int32)
+    upper = np.empty(n, np.int32)
+    role = np.empty(n, np.uint8)
+    parent = np.empty(n, np.int32)
+    sim = np.empty(m, np.uint8)
+    pairs = np.empty((m, 2), np.int32)
+    if n:
+        _lib.check(lib.gs_engine_export_state(st._engine.handle, stage, lower.ctypes.data,
+                                              upper.ctypes.data, role.ctypes.data,
+                                              parent.ctypes.data, sim.ctypes.data,
+                                              pairs.ctypes.data))
+    st.lower, st.upper, st.role, st.parent = lower, upper, role, parent
+    if m and len(st.sim) == m:
+        # reference edge k = the k-th (a, b) pair in (a, b) order (graph.py:218-231)
+        order = np.lexsort((pairs[:, 1], pairs[:, 0]))
+        st.sim[:] = sim[order]
+    st._stage = stage
+
+
+def identify_core(g, mu: int, epsilon: EpsilonLike, st: ClusterState, *, workers: int = 1,
+                  stats: Optional[StatsReport] = None, on_edge=None) -> None:
+    """scan.py:452-492: decide Core/NonCore for every vertex on the device
+    (pre-pass, bound-pruned sweep, then the cleanup sweep of unresolved roles).
+
+    ``on_edge`` is the reference's observability hook; the device sweep has no
+    per-edge host callback, so it is called once after the sweep and once
+    after the cleanup, each time with ``-1`` and ``st`` holding a consistent
+    snapshot (the bounds sandwich |N_eps| at every step of the sweep)."""
+    f = _validate(mu, workers, epsilon)
+    n, m, off, adj = graph_arrays(g)
+    if st.n != n or st.m != m:
+        raise ValueError("state does not belong to this graph")
+    if n == 0:
+        st._stage = 0
+        return
+    lib = _lib.load()
+    if st._engine is None:
+        st._engine = _lib.Engine()
+    h = st._engine.handle
+    _lib.check(lib.gs_engine_load_csr(h, n, m, off.ctypes.data, adj.ctypes.data, 0))
+    eps2 = _lib.eps2_struct(f, _dmax(off))
+    _lib.check(lib.gs_engine_phase_begin(h, int(mu), ctypes.byref(eps2)))
+    _lib.check(lib.gs_engine_phase_identify(h, None))
+    if on_edge is not None:
+        _export(g, st, 0)
+        on_edge(-1)
+    ncores = ctypes.c_int64(0)
+    _lib.check(lib.gs_engine_phase_resolve(h, None, ctypes.byref(ncores)))
+    st._mu, st._eps = int(mu), f
+    _export(g, st, 0)
+    if on_edge is not None:
+        on_edge(-1)
+    if stats is not None:
+        _phase_stats(st, stats, ("identify", "cleanup"))
+
+
+def _phase_stats(st: ClusterState, stats: StatsReport, names) -> None:
+    """Counters and the device phase times of the engine's scan so far."""
+    tmp = _lib.GsStats()
+    lib = _lib.load()
+    _lib.check(lib.gs_engine_phase_stats(st._engine.handle, ctypes.byref(tmp)))
+    rep = stats_from_native(tmp, st.n, st.m, stats.workers)
+    stats.sim_evals = rep.sim_evals
+    stats.adj_probes = rep.adj_probes
+    stats.union_retries = rep.union_retries
+    stats.probe_bound_violations = rep.probe_bound_violations
+    for k in names:
+        stats.phases[k] = rep.phases[k]
+
+
+def _require_stage(st: ClusterState, stage: int, what: str) -> None:
+    if st._engine is None or st._stage < stage:
+        raise RuntimeError(f"{what}: run the previous phases on this state first")
+
+
+def detect_clusters(g, epsilon: EpsilonLike, st: ClusterState, *, workers: int = 1,
+                    stats: Optional[StatsReport] = None) -> None:
+    """scan.py:701-773: cluster forest over similar core-core edges, flatten,
+    canonical labels, member attachment -- on the device."""
+    f = epsilon_fraction(epsilon)
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if st.n == 0:
+        st._stage = 1
+        return
+    _require_stage(st, 0, "detect_clusters")
+    if f != st._eps:
+        raise ValueError("detect_clusters must use the epsilon of identify_core")
+    lib = _lib.load()
+    h = st._engine.handle
+    _lib.check(lib.gs_engine_phase_union(h, None, None))
+    _lib.check(lib.gs_engine_phase_merge(h, None, 0))
+    _lib.check(lib.gs_engine_phase_attach(h, None))
+    _export(g, st, 1)
+    if stats is not None:
+        _phase_stats(st, stats, ("cluster",))
+
+
+def classify_hub_outlier(g, st: ClusterState, *, workers: int = 1,
+                         stats: Optional[StatsReport] = None) -> None:
+    """scan.py:832-852: every unclustered vertex becomes Hub or Outlier."""
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    if st.n == 0:
+        st._stage = 2
+        return
+    _require_stage(st, 1, "classify_hub_outlier")
+    if st._stage >= 2:  # idempotent (scan.py:832)
+        return
+    lib = _lib.load()
+    tmp = _lib.GsStats()
+    _lib.check(lib.gs_engine_phase_finish(st._engine.handle, None, None, None, 0,
+                                          ctypes.byref(tmp)))
+    _export(g, st, 2)
+    if stats is not None:
+        _phase_stats(st, stats, ("classify",))
+
+
+def resolve_roles_from_bounds(st: ClusterState, mu: int, strict: bool = False) -> bool:
+    """scan.py:390-412 over the host snapshot: Core if lower >= mu, NonCore if
+    upper < mu; True when no role is left open (``strict`` raises instead)."""
+    open_ = st.role == ROLE_UNKNOWN
+    st.role[open_ & (st.lower >= mu)] = ROLE_CORE
+    st.role[open_ & (st.lower < mu) & (st.upper < mu)] = ROLE_NONCORE
+    left = int(np.count_nonzero(st.role == ROLE_UNKNOWN))
+    if left and strict:
+        raise RuntimeError(f"{left} vertices have unresolved roles")
+    return left == 0
+
+
+def _chase(parent, u: int) -> int:
+    r = u
+    nxt = parent[r]
+    while nxt != r:
+        r = int(nxt)
+        nxt = parent[r]
+    return int(r)
+
+
+def find_root(st: ClusterState, u: int) -> int:
+    """scan.py:507-511: root of u's cluster tree (read-only)."""
+    if st.parent[u] < 0:
+        raise ValueError(f"vertex {u} is not in any cluster tree")
+    return _chase(st.parent, u)
+
+
+def union_roots(st: ClusterState, u: int, v: int, *, lock=None, counters=None) -> None:
+    """scan.py:514-564: union by height on the host forest of ``st`` (a tie
+    links v's root under u's and bumps its height); with ``lock`` the link is
+    validated under the lock and a lost race retries (counted)."""
+    parent, height = st.parent, st.height
+    while True:
+        ru, rv = _chase(parent, u), _chase(parent, v)
+        if ru == rv:
+            return
+        if lock is None:
+            _link(parent, height, ru, rv)
+            return
+        with lock:
+            if parent[ru] == ru and parent[rv] == rv:
+                _link(parent, height, ru, rv)
+                return
+        if counters is not None:
+            counters.union_retries += 1
+        u, v = ru, rv
+
+
+def _link(parent, height, ru: int, rv: int) -> None:
+    hu, hv = int(height[ru]), int(height[rv])
+    if hu < hv:
+        parent[ru] = rv
+    elif hv < hu:
+        parent[rv] = ru
+    else:
+        parent[rv] = ru
+        height[ru] = hu + 1
+
+
+def build_result(st: ClusterState, orig_ids) -> ClusteringResult:
+    """scan.py:950-962: freeze the state; MEMBER_SHARED reads as MEMBER,
+    cluster_id = parent if >= 0 else -1."""
+    role = np.asarray(st.role, dtype=np.uint8)
+    bad = ~np.isin(role, [ROLE_CORE, ROLE_MEMBER, ROLE_MEMBER_SHARED, ROLE_HUB, ROLE_OUTLIER])
+    if st.n and bad.any():
+        v = int(np.flatnonzero(bad)[0])
+        raise RuntimeError(f"vertex {v} finished with unresolved role {_PUBLIC_ROLE[int(role[v])]}")
+    codes = np.where(role == ROLE_MEMBER_SHARED, ROLE_MEMBER, role).astype(np.uint8)
+    par = np.asarray(st.parent, dtype=np.int32)
+    cids = np.where(par >= 0, par, -1).astype(np.int32)
+    orig = np.asarray(orig_ids, dtype=np.uint32) if st.n else np.empty(0, np.uint32)
+    return ClusteringResult(st.n, codes, cids, orig)
