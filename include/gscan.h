@@ -55,6 +55,7 @@ extern "C" {
 #define GS_ECUDA 3
 #define GS_ENOMEM 4
 #define GS_EINTERNAL 5
+#define GS_EPARSE 6 /* input outside the native grammar; err_line says where */
 
 #define GS_ROLE_CORE 1
 #define GS_ROLE_MEMBER 3
@@ -208,6 +209,22 @@ int gs_chunglu_generate(int logn, double gamma, double max_degree, int64_t count
  * writes the unique count to *m_out and interleaved pairs to edges_dev. */
 int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev,
                        int32_t* edges_dev, int64_t* m_out, void* stream);
+
+/* Native ingest (parse_edge_list, graph.py:63-118), host memory in and out.
+ * gs_parse_edge_text: ASCII edge-list text -> raw (u, v) pairs in input order
+ * (self-loops kept), multi-threaded; u_out/v_out hold `cap` pairs (one per
+ * line at most).  GS_EPARSE + *err_line for anything outside the native
+ * grammar (the caller then applies the reference parser to report or accept).
+ * gs_normalize_sparse (device): dense ids = rank of the sorted distinct
+ * endpoint ids (ids_out [n], capacity 2*count), self-loops dropped, pairs
+ * oriented u < v, sorted, deduplicated (edges_out [2m], capacity 2*count). */
+int gs_parse_edge_text(const char* buf, int64_t len, int threads, uint32_t* u_out,
+                       uint32_t* v_out, int64_t cap, int64_t* count, int64_t* err_line);
+int gs_normalize_sparse(int64_t count, const uint32_t* u, const uint32_t* v, uint32_t* ids_out,
+                        int64_t* n_out, int32_t* edges_out, int64_t* m_out);
+
+/* Number of visible CUDA devices (0 when there is no usable driver/device). */
+int gs_device_count(void);
 
 const char* gs_last_error(void);
 int gs_version(void);

@@ -21,6 +21,7 @@ GS_EBUDGET = 2
 GS_ECUDA = 3
 GS_ENOMEM = 4
 GS_EINTERNAL = 5
+GS_EPARSE = 6
 
 GS_PH_H2D, GS_PH_BUILD, GS_PH_IDENTIFY, GS_PH_CLEANUP = 0, 1, 2, 3
 GS_PH_CLUSTER, GS_PH_CLASSIFY, GS_PH_D2H, GS_PH_TOTAL = 4, 5, 6, 7
@@ -102,6 +103,12 @@ SIGNATURES = [
     ("gs_chunglu_generate", ctypes.c_int,
      [ctypes.c_int, ctypes.c_double, ctypes.c_double, _I64, ctypes.c_uint64, _P, _P, _P]),
     ("gs_normalize_edges", ctypes.c_int, [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P]),
+    ("gs_parse_edge_text", ctypes.c_int,
+     [ctypes.c_char_p, _I64, ctypes.c_int, _P, _P, _I64, ctypes.POINTER(_I64),
+      ctypes.POINTER(_I64)]),
+    ("gs_normalize_sparse", ctypes.c_int,
+     [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P, ctypes.POINTER(_I64)]),
+    ("gs_device_count", ctypes.c_int, []),
     ("gs_last_error", ctypes.c_char_p, []),
     ("gs_version", ctypes.c_int, []),
 ]

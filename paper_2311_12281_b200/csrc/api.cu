@@ -23,6 +23,8 @@ int rmat_generate(int scale, uint64_t seed, int64_t count, int32_t* src, int32_t
                   cudaStream_t st);
 int chunglu_generate(int logn, double gamma, double wmax, int64_t count, uint64_t seed,
                      int32_t* src, int32_t* dst, cudaStream_t st);
+int normalize_sparse(gs_engine* e, int64_t count, uint32_t* src, uint32_t* dst, uint32_t* ids,
+                     int64_t* n_out, int32_t* uv, int64_t* m_out);
 int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32_t* dst,
                     int32_t* uv, int64_t* m_out);
 int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
@@ -173,6 +175,11 @@ void gs_engine::free_state() {
 extern "C" {
 
 int gs_version(void) { return GS_ABI_VERSION; }
+int gs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n;
+}
 const char* gs_last_error(void) { return g_err.c_str(); }
 
 int gs_engine_create(int device, uint64_t hbm_cap_bytes, gs_engine** out) {
@@ -571,6 +578,32 @@ int gs_normalize_edges(int64_t count, int32_t* src_dev, int32_t* dst_dev, int32_
   int rc = normalize_edges(e, count, src_dev, dst_dev, edges_dev, m_out);
   gs_engine_destroy(e);
   return rc;
+}
+
+int gs_normalize_sparse(int64_t count, const uint32_t* u, const uint32_t* v, uint32_t* ids_out,
+                        int64_t* n_out, int32_t* edges_out, int64_t* m_out) {
+  if (count < 0 || !n_out || !m_out) { set_error("invalid arguments"); return GS_EINVAL; }
+  *n_out = 0;
+  *m_out = 0;
+  if (count == 0) return GS_OK;
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(-1, 0, &e));
+  struct Guard { gs_engine* e; ~Guard() { gs_engine_destroy(e); } } guard{e};
+  uint32_t *du = nullptr, *dv = nullptr, *dids = nullptr;
+  int32_t* duv = nullptr;
+  GS_TRY(e->alloc_n(&du, count));
+  GS_TRY(e->alloc_n(&dv, count));
+  GS_TRY(e->alloc_n(&dids, 2 * count));
+  GS_TRY(e->alloc_n(&duv, 2 * count));
+  GS_CUDA(cudaMemcpyAsync(du, u, 4 * (size_t)count, cudaMemcpyHostToDevice, e->stream));
+  GS_CUDA(cudaMemcpyAsync(dv, v, 4 * (size_t)count, cudaMemcpyHostToDevice, e->stream));
+  GS_TRY(normalize_sparse(e, count, du, dv, dids, n_out, duv, m_out));
+  if (*n_out > 0)
+    GS_CUDA(cudaMemcpyAsync(ids_out, dids, 4 * (size_t)*n_out, cudaMemcpyDeviceToHost, e->stream));
+  if (*m_out > 0)
+    GS_CUDA(cudaMemcpyAsync(edges_out, duv, 8 * (size_t)*m_out, cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  return GS_OK;
 }
 
 }  // extern "C"

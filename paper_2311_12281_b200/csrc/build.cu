@@ -990,4 +990,66 @@ int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32
   return GS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// sparse input ids -> dense ranks (parse_edge_list's remap, graph.py:114-117)
+
+__global__ void k_concat_ids(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                             int64_t count, uint32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = a[i];
+    out[count + i] = b[i];
+  }
+}
+
+__global__ void k_remap_ids(const uint32_t* __restrict__ ids, int64_t n, uint32_t* __restrict__ x,
+                            int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = x[i];
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ids[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    x[i] = (uint32_t)lo;
+  }
+}
+
+int normalize_sparse(gs_engine* e, int64_t count, uint32_t* src, uint32_t* dst, uint32_t* ids,
+                     int64_t* n_out, int32_t* uv, int64_t* m_out) {
+  cudaStream_t st = e->stream;
+  *n_out = 0;
+  *m_out = 0;
+  if (count == 0) return GS_OK;
+  uint32_t *k1 = nullptr, *k2 = nullptr;
+  GS_TRY(e->alloc_n(&k1, 2 * count));
+  GS_TRY(e->alloc_n(&k2, 2 * count));
+  k_concat_ids<<<e->sms * 8, 256, 0, st>>>(src, dst, count, k1);
+  cub::DoubleBuffer<uint32_t> db(k1, k2);
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, db, 2 * count, 0, 32, st);
+  }));
+  int64_t* d_num = nullptr;
+  GS_TRY(e->alloc_n(&d_num, 1));
+  GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, db.Current(), ids, d_num, 2 * count, st);
+  }));
+  int64_t n = 0;
+  GS_CUDA(cudaMemcpyAsync(&n, d_num, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(k1);
+  e->release(k2);
+  e->release(d_num);
+  if (n > 0x7fffffffLL) { set_error("vertex count exceeds the 4-byte id range"); return GS_EINVAL; }
+  k_remap_ids<<<e->sms * 8, 256, 0, st>>>(ids, n, src, count);
+  k_remap_ids<<<e->sms * 8, 256, 0, st>>>(ids, n, dst, count);
+  e->launches += 5;
+  GS_CUDA(cudaGetLastError());
+  *n_out = n;
+  return normalize_edges(e, count, reinterpret_cast<const int32_t*>(src),
+                         reinterpret_cast<const int32_t*>(dst), uv, m_out);
+}
+
 }  // namespace gs

@@ -10,6 +10,7 @@ the device (``gs_build_graph``); ``parse_edge_list`` is host ingest.
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 from typing import BinaryIO, Optional, Union
 
@@ -56,15 +57,71 @@ class EdgeList:
 def parse_edge_list(source: Union[bytes, str, BinaryIO]) -> EdgeList:
     """Text edge list -> EdgeList, the reference's rules (graph.py:63-118):
     '#' comments and blank lines skipped, self-loops dropped (vertex kept),
-    duplicates merged, sparse ids remapped order-preservingly."""
+    duplicates merged, sparse ids remapped order-preservingly.
+
+    Native ingest: libgscan's multi-threaded parser (gs_parse_edge_text) reads
+    the text, the device remaps and deduplicates (gs_normalize_sparse; host
+    numpy when no CUDA device is visible).  Input outside the parser's ASCII
+    grammar -- malformed lines included -- goes through the reference-exact
+    Python parser below, so errors (ParseError with the line number) and
+    exotic-but-valid inputs behave exactly as in the reference."""
     data = source.read() if hasattr(source, "read") else source
-    if isinstance(data, bytes):
-        try:
-            text = data.decode("utf-8")
-        except UnicodeDecodeError as exc:
-            raise ParseError(f"input is not valid UTF-8 text: {exc}") from None
-    else:
-        text = data
+    if isinstance(data, str):
+        data = data.encode("utf-8")
+    raw = _parse_native(bytes(data))
+    if raw is None:
+        return _parse_exact(data)
+    return _normalize(*raw)
+
+
+def _parse_native(data: bytes):
+    lib = _lib.load()
+    cap = data.count(b"\n") + data.count(b"\r") + 1
+    u = np.empty(cap, dtype=np.uint32)
+    v = np.empty(cap, dtype=np.uint32)
+    cnt = ctypes.c_int64(0)
+    err = ctypes.c_int64(-1)
+    rc = lib.gs_parse_edge_text(data, len(data), 0, u.ctypes.data, v.ctypes.data, cap,
+                                ctypes.byref(cnt), ctypes.byref(err))
+    if rc == _lib.GS_EPARSE:
+        return None
+    _lib.check(rc)
+    return u[: cnt.value], v[: cnt.value]
+
+
+def _normalize(u: np.ndarray, v: np.ndarray) -> EdgeList:
+    count = int(len(u))
+    lib = _lib.load()
+    if count and lib.gs_device_count() > 0:
+        ids = np.empty(2 * count, dtype=np.uint32)
+        edges = np.empty((count, 2), dtype=np.int32)
+        n = ctypes.c_int64(0)
+        m = ctypes.c_int64(0)
+        _lib.check(lib.gs_normalize_sparse(count, u.ctypes.data, v.ctypes.data, ids.ctypes.data,
+                                           ctypes.byref(n), edges.ctypes.data, ctypes.byref(m)))
+        return EdgeList(n_hint=n.value, edges=edges[: m.value].copy(),
+                        orig_ids=ids[: n.value].copy())
+    return _normalize_host(u.astype(np.int64), v.astype(np.int64))
+
+
+def _normalize_host(u: np.ndarray, v: np.ndarray) -> EdgeList:
+    ids = np.unique(np.concatenate([u, v]))
+    du = np.searchsorted(ids, u)
+    dv = np.searchsorted(ids, v)
+    keep = du != dv
+    lo = np.minimum(du, dv)[keep]
+    hi = np.maximum(du, dv)[keep]
+    key = np.unique(lo * (len(ids) + 1) + hi)
+    edges = np.stack([key // (len(ids) + 1), key % (len(ids) + 1)], axis=1).astype(np.int32)
+    return EdgeList(n_hint=len(ids), edges=edges, orig_ids=ids.astype(np.uint32))
+
+
+def _parse_exact(data: bytes) -> EdgeList:
+    """graph.py:63-118 rule for rule (str.splitlines / strip / split / int)."""
+    try:
+        text = data.decode("utf-8")
+    except UnicodeDecodeError as exc:
+        raise ParseError(f"input is not valid UTF-8 text: {exc}") from None
     us: list[int] = []
     vs: list[int] = []
     for lineno, raw in enumerate(text.splitlines(), 1):
@@ -85,17 +142,7 @@ def parse_edge_list(source: Union[bytes, str, BinaryIO]) -> EdgeList:
             raise ParseError(f"vertex id exceeds 4-byte unsigned range in {line!r}", lineno)
         us.append(u)
         vs.append(v)
-    u = np.asarray(us, dtype=np.int64)
-    v = np.asarray(vs, dtype=np.int64)
-    ids = np.unique(np.concatenate([u, v]))
-    du = np.searchsorted(ids, u)
-    dv = np.searchsorted(ids, v)
-    keep = du != dv
-    lo = np.minimum(du, dv)[keep]
-    hi = np.maximum(du, dv)[keep]
-    key = np.unique(lo * (len(ids) + 1) + hi)
-    edges = np.stack([key // (len(ids) + 1), key % (len(ids) + 1)], axis=1).astype(np.int32)
-    return EdgeList(n_hint=len(ids), edges=edges, orig_ids=ids.astype(np.uint32))
+    return _normalize_host(np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64))
 
 
 @dataclass
@@ -196,3 +243,73 @@ def graph_arrays(g) -> tuple[int, int, np.ndarray, np.ndarray]:
 
 def _ptr(a: np.ndarray) -> int:
     return a.ctypes.data_as(ctypes.c_void_p).value or 0
+
+
+# --- binary graph cache (graph.py:279-350): the GSCG format, byte-compatible -
+#
+#   magic "GSCG" | version u32 | n u64 | m u64      (little-endian)
+#   vertex_offsets (n+1) x i64 | adjacency 2m x i32 | edge_ids 2m x i32
+#   edge_list 2m x i32 | orig_ids n x u32
+#
+# Arrays are read with one bulk read each (np.fromfile), so a cached s24 graph
+# (6.5 GB) loads at disk speed instead of through per-element Python code.
+
+_GRAPH_MAGIC = b"GSCG"
+_GRAPH_VERSION = 1
+_HEADER = struct.Struct("<4sIQQ")
+_LAYOUT = (("vertex_offsets", "<i8", 1, 0), ("adjacency", "<i4", 0, 2),
+           ("edge_ids", "<i4", 0, 2), ("edge_list", "<i4", 0, 2), ("orig_ids", "<u4", 0, 0))
+
+
+def _count(n: int, m: int, plus_one: int, per_edge: int) -> int:
+    return (n + plus_one) if per_edge == 0 else per_edge * m
+
+
+def save_graph(g, path: str) -> None:
+    """graph.py:313-321: write the five layout arrays to a GSCG cache."""
+    n, m = int(g.n), int(g.m)
+    with open(path, "wb") as f:
+        f.write(_HEADER.pack(_GRAPH_MAGIC, _GRAPH_VERSION, n, m))
+        for name, dt, plus, per in _LAYOUT:
+            a = np.ascontiguousarray(as_array(getattr(g, name), np.dtype(dt).newbyteorder("=")),
+                                     dtype=dt)
+            want = _count(n, m, plus, per)
+            if len(a) != want:
+                raise ValueError(f"{name} has {len(a)} entries, expected {want}")
+            a.tofile(f)
+
+
+def load_graph(path: str) -> Graph:
+    """graph.py:324-350: read a GSCG cache written by save_graph (or by the
+    reference); the same validation and error messages."""
+    with open(path, "rb") as f:
+        header = f.read(_HEADER.size)
+        if len(header) != _HEADER.size:
+            raise ValueError("truncated graph cache header")
+        magic, version, n, m = _HEADER.unpack(header)
+        if magic != _GRAPH_MAGIC:
+            raise ValueError("not a graph cache file (bad magic)")
+        if version != _GRAPH_VERSION:
+            raise ValueError(f"unsupported graph cache version {version}")
+        arrs = {}
+        for name, dt, plus, per in _LAYOUT:
+            cnt = (n + plus) if per == 0 else per * m
+            a = np.fromfile(f, dtype=dt, count=cnt)
+            if len(a) != cnt:
+                raise ValueError("truncated graph cache")
+            arrs[name] = a.astype(np.dtype(dt).newbyteorder("="), copy=False)
+    off = arrs["vertex_offsets"]
+    if off[0] != 0 or off[n] != 2 * m:
+        raise ValueError("corrupt graph cache: bad offset bounds")
+    if n and np.any(np.diff(off) < 0):
+        raise ValueError("corrupt graph cache: offsets not monotone")
+    return Graph(n=int(n), m=int(m), **arrs)
+
+
+def is_graph_cache(path: str) -> bool:
+    """graph.py:353-359: True if ``path`` starts with the GSCG magic."""
+    try:
+        with open(path, "rb") as f:
+            return f.read(4) == _GRAPH_MAGIC
+    except OSError:
+        return False
