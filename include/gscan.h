@@ -223,6 +223,12 @@ int gs_parse_edge_text(const char* buf, int64_t len, int threads, uint32_t* u_ou
 int gs_normalize_sparse(int64_t count, const uint32_t* u, const uint32_t* v, uint32_t* ids_out,
                         int64_t* n_out, int32_t* edges_out, int64_t* m_out);
 
+/* ClusteringResult.to_text (scan.py:892-904), host, multi-threaded: n lines
+ * "orig[v]\t{C|M|H|O}\t orig[cluster[v]] or -1\n" into out (capacity cap;
+ * 25 bytes per vertex always suffice); *len = bytes written. */
+int gs_format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
+                     const uint32_t* orig, int threads, char* out, int64_t cap, int64_t* len);
+
 /* Number of visible CUDA devices (0 when there is no usable driver/device). */
 int gs_device_count(void);
 

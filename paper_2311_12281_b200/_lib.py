@@ -108,6 +108,8 @@ SIGNATURES = [
       ctypes.POINTER(_I64)]),
     ("gs_normalize_sparse", ctypes.c_int,
      [_I64, _P, _P, _P, ctypes.POINTER(_I64), _P, ctypes.POINTER(_I64)]),
+    ("gs_format_result", ctypes.c_int,
+     [_I64, _P, _P, _P, ctypes.c_int, _P, _I64, ctypes.POINTER(_I64)]),
     ("gs_device_count", ctypes.c_int, []),
     ("gs_last_error", ctypes.c_char_p, []),
     ("gs_version", ctypes.c_int, []),

@@ -151,3 +151,86 @@ extern "C" int gs_parse_edge_text(const char* buf, int64_t len, int threads, uin
   }
   return GS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Result writer (ClusteringResult.to_text, scan.py:892-904): one line per
+// vertex "orig<TAB>letter<TAB>orig(cluster) | -1", multi-threaded.  role codes
+// are the public ones (1 C, 3/4 M, 5 H, 6 O); cluster ids index orig_ids.
+
+namespace {
+
+inline int ulen(uint64_t x) {
+  int k = 1;
+  while (x >= 10) { x /= 10; ++k; }
+  return k;
+}
+
+inline char* put_u(char* p, uint64_t x) {
+  const int k = ulen(x);
+  for (int i = k - 1; i >= 0; --i) { p[i] = (char)('0' + x % 10); x /= 10; }
+  return p + k;
+}
+
+inline char letter(uint8_t r) {
+  switch (r) {
+    case 1: return 'C';
+    case 3: case 4: return 'M';
+    case 5: return 'H';
+    case 6: return 'O';
+    default: return '?';
+  }
+}
+
+}  // namespace
+
+extern "C" int gs_format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
+                                const uint32_t* orig, int threads, char* out, int64_t cap,
+                                int64_t* len) {
+  *len = 0;
+  if (n <= 0) return GS_OK;
+  if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(threads, std::max<int64_t>(1, n / 65536));
+  auto line_len = [&](int64_t v) -> int64_t {
+    const int32_t c = cluster[v];
+    if (c >= n) return -1;
+    return ulen(orig[v]) + 3 + (c >= 0 ? ulen(orig[c]) : 2) + 1;
+  };
+  std::vector<int64_t> part(nt + 1, 0);
+  std::vector<int> bad(nt, 0);
+  {
+    std::vector<std::thread> ts;
+    for (int t = 0; t < nt; ++t)
+      ts.emplace_back([&, t] {
+        int64_t s = 0;
+        for (int64_t v = n * t / nt; v < n * (t + 1) / nt; ++v) {
+          const int64_t l = line_len(v);
+          if (l < 0) { bad[t] = 1; return; }
+          s += l;
+        }
+        part[t + 1] = s;
+      });
+    for (auto& t : ts) t.join();
+  }
+  for (int t = 0; t < nt; ++t)
+    if (bad[t]) return GS_EINVAL;
+  for (int t = 0; t < nt; ++t) part[t + 1] += part[t];
+  *len = part[nt];
+  if (part[nt] > cap) return GS_EINVAL;
+  std::vector<std::thread> ts;
+  for (int t = 0; t < nt; ++t)
+    ts.emplace_back([&, t] {
+      char* p = out + part[t];
+      for (int64_t v = n * t / nt; v < n * (t + 1) / nt; ++v) {
+        p = put_u(p, orig[v]);
+        *p++ = '\t';
+        *p++ = letter(role[v]);
+        *p++ = '\t';
+        const int32_t c = cluster[v];
+        if (c >= 0) p = put_u(p, orig[c]);
+        else { *p++ = '-'; *p++ = '1'; }
+        *p++ = '\n';
+      }
+    });
+  for (auto& t : ts) t.join();
+  return GS_OK;
+}

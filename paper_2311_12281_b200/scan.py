@@ -54,7 +54,6 @@ _PUBLIC_ROLE = {
     ROLE_OUTLIER: Role.OUTLIER,
 }
 ROLE_LETTERS = {Role.CORE: "C", Role.MEMBER: "M", Role.HUB: "H", Role.OUTLIER: "O"}
-_CODE_LETTER = np.array([b"?", b"C", b"N", b"M", b"M", b"H", b"O"], dtype="S1")
 
 
 def epsilon_fraction(epsilon: EpsilonLike) -> Fraction:
@@ -159,21 +158,29 @@ class ClusteringResult:
             classes.setdefault(int(ids[v]), set()).add(v)
         return {frozenset(s) for s in classes.values()}
 
+    def to_bytes(self) -> bytes:
+        """to_text() as ASCII bytes, formatted by libgscan (gs_format_result)."""
+        if self.n == 0:
+            return b""
+        codes = np.ascontiguousarray(self._codes(), dtype=np.uint8)
+        ids = np.ascontiguousarray(self._ids(), dtype=np.int32)
+        orig = np.ascontiguousarray(self._orig, dtype=np.uint32)
+        cap = 25 * self.n
+        buf = np.empty(cap, dtype=np.uint8)
+        ln = ctypes.c_int64(0)
+        lib = _lib.load()
+        _lib.check(lib.gs_format_result(self.n, codes.ctypes.data, ids.ctypes.data,
+                                        orig.ctypes.data, 0, buf.ctypes.data, cap,
+                                        ctypes.byref(ln)))
+        return buf[: ln.value].tobytes()
+
     def to_text(self) -> str:
         """``orig<TAB>role<TAB>orig(cluster)|-1`` per vertex (scan.py:892-904)."""
-        if self.n == 0:
-            return ""
-        codes, ids = self._codes(), self._ids()
-        orig = np.asarray(self._orig, dtype=np.int64)
-        shown = np.where(ids >= 0, orig[np.clip(ids, 0, None)], -1)
-        letters = _CODE_LETTER[codes].astype(str)
-        lines = [f"{o}\t{r}\t{c}" for o, r, c in zip(orig.tolist(), letters.tolist(),
-                                                   shown.tolist())]
-        return "\n".join(lines) + "\n"
+        return self.to_bytes().decode("ascii")
 
     def write(self, path: str) -> None:
-        with open(path, "w", encoding="utf-8") as f:
-            f.write(self.to_text())
+        with open(path, "wb") as f:
+            f.write(self.to_bytes())
 
 
 @dataclass

@@ -103,3 +103,21 @@ def test_gscg_cache_errors(tmp_path):
 def test_parse_matches_reference_device_normaliser():
     assert _lib.load().gs_device_count() > 0
     _check_all()
+
+
+def test_native_result_writer_matches_reference_format(tmp_path):
+    """ClusteringResult.to_text via gs_format_result == scan.py:892-904's lines."""
+    rng = np.random.default_rng(11)
+    n = 200_003
+    codes = rng.choice(np.array([1, 3, 4, 5, 6], np.uint8), n)
+    cid = np.where(np.isin(codes, [1, 3, 4]), rng.integers(0, n, n), -1).astype(np.int32)
+    orig = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    r = gs.ClusteringResult(n, codes, cid, orig)
+    letter = {1: "C", 3: "M", 4: "M", 5: "H", 6: "O"}
+    want = "".join(f"{orig[v]}\t{letter[int(codes[v])]}\t{orig[cid[v]] if cid[v] >= 0 else -1}\n"
+                   for v in range(n))
+    assert r.to_text() == want
+    p = tmp_path / "r.txt"
+    r.write(str(p))
+    assert p.read_text() == want
+    assert gs.ClusteringResult(0, codes[:0], cid[:0], orig[:0]).to_text() == ""
