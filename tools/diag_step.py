@@ -48,7 +48,8 @@ def main():
         t2 = time.perf_counter()
         ph = [round(st.phase_ms[k], 2) for k in range(9)]
         print(f"step {i}: load {1e3 * (t1 - t0):.1f} ms (build ev {ph[1]}), scan {1e3 * (t2 - t1):.1f} ms "
-              f"(phases {ph[2:8]}), launches {st.kernel_launches}", flush=True)
+              f"(phases {ph[2:8]}), launches {st.kernel_launches}, evals {st.sim_evals} "
+              f"inters {st.sim_intersections} probes {st.adj_probes}", flush=True)
 
 
 if __name__ == "__main__":

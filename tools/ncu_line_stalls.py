@@ -18,7 +18,10 @@ for r in csv.reader(io.StringIO(out)):
     if hdr and r[0] and len(r) >= 8:  # a CUDA line row: aggregated metrics
         key = f"{fname}:{r[0]}"
         f = lambda x: float(x) if x not in ("", "-") else 0.0
-        st, ex = f(r[4]), f(r[7])
+        try:
+            st, ex = f(r[4]), f(r[7])
+        except ValueError:
+            continue
         agg[key] = (st, ex, r[1].strip()[:80])
 ts = sum(v[0] for v in agg.values()) or 1
 te = sum(v[1] for v in agg.values()) or 1
