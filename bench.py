@@ -3,16 +3,21 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-One step = one full clustering call of the hot path (device CSR build with
-degree-rank relabel + identify + cluster + classify) over the synthetic
-R-MAT s24 edge list (BASELINE.json configs[1], the in-HBM config the metric is
-quoted on).  Inputs exceed L2 (2.1 GB edge list vs 126 MB), so no flush is
-needed between steps.
+One step = one clustering call of the hot path, exactly what
+scan_in_memory(g, mu, eps) does through the C-ABI (gs_engine_load_csr +
+gs_engine_scan): the reference Graph's CSR (vertex_offsets i64, adjacency
+i32) in, degree-rank relabel + identify + cluster + classify, roles and
+cluster ids out -- over the synthetic R-MAT s24 graph (BASELINE.json
+configs[1], the in-HBM config the metric is quoted on).  Inputs exceed L2
+(2.2 GB CSR vs 126 MB), so no flush is needed between steps.
 
-  value   edges/s = m / device time per step, edge list resident in HBM,
-          results left in HBM (CUDA events on the engine stream)
-  e2e     same metric through the C-ABI with HOST buffers: pinned edge list
-          H2D + build + scan + roles/cluster ids D2H inside the timed region
+  value   edges/s = m / device time per step, CSR resident in HBM, results
+          left in HBM (CUDA events on the engine stream)
+  e2e     same metric through the same call with HOST buffers: pinned CSR
+          streamed H2D (overlapped with the relabel) + scan + roles/cluster
+          ids D2H inside the timed region
+  build_from_edges_ms  the edge-list -> CSR build (build_graph's job, timed
+          separately; not part of scan_in_memory)
   roofline  similarity pass (identify) algorithmic bytes W_sim
           / its measured time vs MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference hot loop (_eval_edge, scan.py:203-233, C port in
@@ -206,6 +211,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def eng_build_ms(eng) -> float:
+    """Device time of the engine's last load (gs_stats.phase_ms[BUILD] via a
+    stats-only call)."""
+    from paper_2311_12281_b200 import _lib
+
+    st = _lib.GsStats()
+    _lib.check(_lib.load().gs_engine_phase_stats(eng.handle, ctypes.byref(st)))
+    return float(st.phase_ms[_lib.GS_PH_BUILD])
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -267,8 +282,15 @@ def run_ours(args):
         else:
             shard.run(args.mu, eps2, role_ptr, clus_ptr, on_dev, stats)
 
+    # the reference Graph's CSR of the same graph (build_graph's output)
+    off_d = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    adj_d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+    _lib.check(lib.gs_build_csr_device(n, m, uv.data_ptr(), off_d.data_ptr(), adj_d.data_ptr(),
+                                       None))
+    torch.cuda.synchronize()
+
     def step_device():
-        _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv.data_ptr(), 1))
+        _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_d.data_ptr(), adj_d.data_ptr(), 1))
         scan_call(role_d.data_ptr(), clus_d.data_ptr(), 1, st)
 
     def barrier():
@@ -317,17 +339,27 @@ def run_ours(args):
         if td.get("config") == f"s{args.scale} eps={args.eps} mu={args.mu}":
             traffic = td.get("dram_bytes_per_step")
 
+    # ---- the edge-list -> CSR build, timed on its own (build_graph's job)
+    eb = []
+    for _ in range(3):
+        _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv.data_ptr(), 1))
+        eb.append(eng_build_ms(eng))
+    build_edges_ms = statistics.median(eb)
+
     # ---- e2e through the C-ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        uv_h = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
-        uv_h.copy_(uv)
+        off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        adj_h = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
+        off_h.copy_(off_d)
+        adj_h.copy_(adj_d)
         role_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
         clus_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
         st2 = _lib.GsStats()
 
         def step_host():
-            _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv_h.data_ptr(), 0))
+            _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_h.data_ptr(), adj_h.data_ptr(),
+                                              0))
             scan_call(role_h.data_ptr(), clus_h.data_ptr(), 0, st2)
 
         for _ in range(max(1, args.warmup)):
@@ -342,7 +374,7 @@ def run_ours(args):
         # parity of the two paths on the same input
         assert torch.equal(role_h, role_d.cpu()) and torch.equal(clus_h, clus_d.cpu())
         e2e = {"value": m / (ms_e2e / 1000.0), "unit": "edges/s",
-               "ms_per_step": ms_e2e, "h2d_bytes_per_step": 8 * m,
+               "ms_per_step": ms_e2e, "h2d_bytes_per_step": 8 * (n + 1) + 8 * m,
                "d2h_bytes_per_step": 5 * n}
 
     cpu = None
@@ -372,23 +404,29 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "int32",
             "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05, scrambled ids), "
-                    "generated + normalised on the device",
+                    "generated + normalised on the device; the reference-layout CSR built "
+                    "once on the device (gs_build_csr_device) before timing",
             "config": {
                 "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
                             f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
                 "n": n, "m": m, "seed": args.seed,
                 "parallelism": (f"edge-sharded x{world} (b % world), NCCL all-reduce/all-gather"
                                 if shard is not None else "single"),
-                "l2": "inputs larger than L2 (edge list 8m bytes), no flush",
-                "step": "device CSR build (degree-rank relabel) + identify + cluster + classify",
+                "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
+                "step": "scan_in_memory's C-ABI call on the reference CSR: degree-rank "
+                        "relabel + identify + cluster + classify",
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "dram_achieved": (traffic / t_sim / 1e9) if traffic and t_sim > 0 else None,
+                         "dram_frac": (traffic / t_sim / 1e9 / peak) if traffic and t_sim > 0
+                         else None,
                          "kernel": "similarity pass (identify phase: k_sim_hash*/k_sim_tiny)",
                          "alg_bytes_per_step": w_sim, "t_ms": t_sim * 1000, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "build_from_edges_ms": build_edges_ms,
             "clocks": clk.summary(),
             "phases_ms": {"h2d": phase[0], "build": phase[1], "identify": phase[2],
                           "cleanup": phase[3], "cluster": phase[4], "classify": phase[5],

@@ -197,6 +197,13 @@ int gs_engine_create(int device, uint64_t hbm_cap_bytes, gs_engine** out) {
     set_error(cuda_msg(err, "cudaStreamCreate", __FILE__, __LINE__));
     return GS_ECUDA;
   }
+  err = cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking);
+  if (err != cudaSuccess) {
+    cudaStreamDestroy(e->stream);
+    delete e;
+    set_error(cuda_msg(err, "cudaStreamCreate", __FILE__, __LINE__));
+    return GS_ECUDA;
+  }
   cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, dev);
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -215,6 +222,8 @@ void gs_engine_destroy(gs_engine* e) {
   for (auto& kv : e->sizes) cudaFreeAsync(kv.first, e->stream);
   for (auto& kv : e->cache) cudaFreeAsync(kv.second, e->stream);
   cudaStreamSynchronize(e->stream);
+  cudaStreamSynchronize(e->cstream);
+  cudaStreamDestroy(e->cstream);
   cudaStreamDestroy(e->stream);
   // hand the pool's reserved memory back (the release threshold keeps it
   // across calls of a live engine, not beyond its lifetime)
@@ -237,43 +246,32 @@ static int load_common(gs_engine* e, int64_t n, int64_t m) {
 int gs_engine_load_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* offsets,
                        const int32_t* adjacency, int on_device) {
   GS_TRY(load_common(e, n, m));
-  cudaEvent_t t0, t1, t2;
-  cudaEventCreate(&t0); cudaEventCreate(&t1); cudaEventCreate(&t2);
-  cudaEventRecord(t0, e->stream);
-  const int64_t* off = offsets;
-  const int32_t* adj = adjacency;
-  int64_t* d_off = nullptr;
-  int32_t* d_adj = nullptr;
-  if (!on_device) {
-    GS_TRY(e->alloc_n(&d_off, n + 1));
-    GS_TRY(e->alloc_n(&d_adj, 2 * m));
-    GS_CUDA(cudaMemcpyAsync(d_off, offsets, sizeof(int64_t) * (size_t)(n + 1),
-                            cudaMemcpyHostToDevice, e->stream));
-    if (m > 0)
-      GS_CUDA(cudaMemcpyAsync(d_adj, adjacency, sizeof(int32_t) * (size_t)(2 * m),
-                              cudaMemcpyHostToDevice, e->stream));
-    off = d_off;
-    adj = d_adj;
-  }
   int64_t h_ends[2] = {0, 0};
-  GS_CUDA(cudaMemcpyAsync(&h_ends[0], off, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
-  GS_CUDA(cudaMemcpyAsync(&h_ends[1], off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
-  cudaEventRecord(t1, e->stream);
-  GS_CUDA(cudaStreamSynchronize(e->stream));
+  if (on_device) {
+    GS_CUDA(cudaMemcpyAsync(&h_ends[0], offsets, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaMemcpyAsync(&h_ends[1], offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+  } else {
+    h_ends[0] = offsets[0];
+    h_ends[1] = offsets[n];
+  }
   if (h_ends[0] != 0 || h_ends[1] != 2 * m) {
-    e->release(d_off);
-    e->release(d_adj);
     set_error("invalid graph: vertex_offsets must start at 0 and end at 2m");
     return GS_EINVAL;
   }
-  int rc = build_from_csr(e, n, m, off, adj);
-  cudaEventRecord(t2, e->stream);
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0); cudaEventCreate(&t1);
+  cudaEventRecord(t0, e->stream);
+  // host input: the adjacency is streamed chunk by chunk and scattered into
+  // its rank-space runs as it lands (the copy overlaps the relabel)
+  int rc = on_device ? build_from_csr(e, n, m, offsets, adjacency)
+                     : build_from_csr_host(e, n, m, offsets, adjacency);
+  cudaEventRecord(t1, e->stream);
   cudaStreamSynchronize(e->stream);
-  e->release(d_off);
-  e->release(d_adj);
-  cudaEventElapsedTime(&e->last_h2d_ms, t0, t1);
-  cudaEventElapsedTime(&e->last_build_ms, t1, t2);
-  cudaEventDestroy(t0); cudaEventDestroy(t1); cudaEventDestroy(t2);
+  e->last_h2d_ms = 0;  // inside the build (overlapped)
+  cudaEventElapsedTime(&e->last_build_ms, t0, t1);
+  cudaEventDestroy(t0); cudaEventDestroy(t1);
   return rc;
 }
 

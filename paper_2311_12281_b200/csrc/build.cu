@@ -330,25 +330,27 @@ __global__ void k_scatter_edges(const int32_t* __restrict__ uv, int64_t m, int64
 // CSR input: slot i of caller vertex u lands at the same position of u's
 // rank-space run (no atomics); validates ids and the strictly increasing runs.
 __global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n,
-                              const int32_t* __restrict__ adj, int64_t slots,
-                              const int32_t* __restrict__ rank,
+                              const int32_t* __restrict__ chunk, int64_t i0, int64_t i1,
+                              int32_t prev, const int32_t* __restrict__ rank,
                               const int64_t* __restrict__ noff, int32_t* __restrict__ out,
                               int* __restrict__ bad) {
-  const int64_t base = blockIdx.x * (int64_t)blockDim.x;
+  // slots [i0, i1) of the caller's adjacency, values in chunk[i - i0];
+  // prev = the caller's adjacency[i0 - 1] (run-order check across chunks)
+  const int64_t base = i0 + blockIdx.x * (int64_t)blockDim.x;
   const int64_t i = base + threadIdx.x;
   __shared__ int64_t vlo, vhi;
   if (threadIdx.x == 0) {
     int64_t last = base + blockDim.x - 1;
-    if (last >= slots) last = slots - 1;
+    if (last >= i1) last = i1 - 1;
     vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
     vhi = upper_bound_i64(off, 0, n + 1, last);
   }
   __syncthreads();
-  if (i >= slots) return;
+  if (i >= i1) return;
   const int64_t u = upper_bound_i64(off, vlo, vhi, i) - 1;
-  int32_t v = adj[i];
+  int32_t v = chunk[i - i0];
   if (v < 0 || v >= n || v == u) { atomicExch(bad, 3); v = (int32_t)u; }
-  if (i > off[u] && adj[i - 1] >= v) atomicExch(bad, 4);  // runs strictly increasing
+  if (i > off[u] && (i > i0 ? chunk[i - 1 - i0] : prev) >= v) atomicExch(bad, 4);  // increasing
   const int32_t ru = rank[u];
   out[noff[ru] + (i - off[u])] = rank[v];
 }
@@ -674,10 +676,88 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   int32_t* arcs = nullptr;
   GS_TRY(e->alloc_n(&arcs, 2 * m));
   if (m > 0) {
-    k_scatter_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 2 * m, g.rank, g.off, arcs,
-                                                        d_bad);
+    k_scatter_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 0, 2 * m, 0, g.rank, g.off,
+                                                        arcs, d_bad);
     e->launches++;
   }
+  return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
+}
+
+// Host CSR (the reference Graph in pinned or pageable memory): the offsets
+// are copied first (degrees -> ranks -> rank-space offsets); the adjacency
+// follows in kSlots x kChunk-element chunks on the copy stream, and each chunk
+// is scattered into the rank-space runs as soon as it lands, so the PCIe
+// transfer overlaps the relabel and the scatter.  HBM holds the chunk ring,
+// not a second copy of the adjacency.
+int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_host,
+                        const int32_t* adj_host) {
+  constexpr int kSlots = 4;
+  constexpr int64_t kChunk = (int64_t)1 << 24;  // 64 MB of adjacency per chunk
+  cudaStream_t st = e->stream, cs = e->cstream;
+  DevGraph& g = e->g;
+  e->free_graph();
+  const int64_t slots = 2 * m;
+  const int64_t nchunks = (slots + kChunk - 1) / kChunk;
+  int* d_bad = nullptr;
+  int64_t* d_off = nullptr;
+  GS_TRY(e->alloc_n(&d_bad, 1));
+  GS_TRY(e->alloc_n(&d_off, n + 1));
+  int32_t* ring[kSlots] = {nullptr};
+  const int nring = (int)std::min<int64_t>(kSlots, nchunks);
+  for (int k = 0; k < nring; ++k) GS_TRY(e->alloc_n(&ring[k], kChunk));
+  cudaEvent_t copied[kSlots], freed[kSlots], ready;
+  for (int k = 0; k < kSlots; ++k) {
+    cudaEventCreateWithFlags(&copied[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&freed[k], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+  GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+  GS_CUDA(cudaMemcpyAsync(d_off, off_host, sizeof(int64_t) * (size_t)(n + 1),
+                          cudaMemcpyHostToDevice, st));
+  cudaEventRecord(ready, st);  // the ring is allocated and free from here on
+  GS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  auto issue = [&](int64_t c) -> int {
+    const int k = (int)(c % kSlots);
+    const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
+    if (c >= kSlots) GS_CUDA(cudaStreamWaitEvent(cs, freed[k], 0));
+    GS_CUDA(cudaMemcpyAsync(ring[k], adj_host + i0, sizeof(int32_t) * (size_t)len,
+                            cudaMemcpyHostToDevice, cs));
+    GS_CUDA(cudaEventRecord(copied[k], cs));
+    return GS_OK;
+  };
+  int64_t next = 0;
+  for (; next < nring; ++next) GS_TRY(issue(next));  // overlaps the relabel below
+  uint32_t* deg = nullptr;
+  GS_TRY(e->alloc_n(&deg, n));
+  if (n > 0) {
+    k_deg_from_off<<<grid_for(n, 256), 256, 0, st>>>(d_off, n, deg, d_bad);
+    e->launches++;
+  }
+  int64_t h_cls[DevGraph::kClasses + 1];
+  GS_TRY(rank_and_offsets(e, n, deg, h_cls));
+  e->release(deg);
+  int32_t* arcs = nullptr;
+  GS_TRY(e->alloc_n(&arcs, slots));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int k = (int)(c % kSlots);
+    const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
+    GS_CUDA(cudaStreamWaitEvent(st, copied[k], 0));
+    k_scatter_csr<<<grid_for(len, 256), 256, 0, st>>>(d_off, n, ring[k], i0, i0 + len,
+                                                      i0 > 0 ? adj_host[i0 - 1] : 0, g.rank,
+                                                      g.off, arcs, d_bad);
+    e->launches++;
+    GS_CUDA(cudaEventRecord(freed[k], st));
+    if (next < nchunks) GS_TRY(issue(next++));
+  }
+  GS_CUDA(cudaGetLastError());
+  GS_CUDA(cudaStreamSynchronize(cs));
+  for (int k = 0; k < nring; ++k) e->release(ring[k]);
+  e->release(d_off);
+  for (int k = 0; k < kSlots; ++k) {
+    cudaEventDestroy(copied[k]);
+    cudaEventDestroy(freed[k]);
+  }
+  cudaEventDestroy(ready);
   return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
 }
 

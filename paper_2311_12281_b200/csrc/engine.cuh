@@ -112,6 +112,7 @@ struct SimParams {
 struct gs_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cstream = nullptr;  // host->device copies overlapped with the build
   uint64_t cap = 0;
   size_t live = 0, peak = 0;  // bytes in use (peak = high-water mark)
   size_t reserved = 0;        // bytes held: in use + cached free blocks
@@ -147,6 +148,9 @@ namespace gs {
 int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_dev);
 int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
                    const int32_t* adj_dev);
+// host CSR: adjacency streamed in chunks on cstream, scattered as it lands
+int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_host,
+                        const int32_t* adj_host);
 // sim.cu
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
 int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split
