@@ -378,9 +378,9 @@ __device__ __forceinline__ int64_t rank_of_degree(const int64_t* off, int64_t n,
 
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t n,
                                int64_t* __restrict__ out) {
-  const int64_t th[5] = {2, 33, 257, 1025, 4096};
+  const int64_t th[7] = {2, 33, 257, 513, 1025, 2049, 4096};
   const int c = threadIdx.x;
-  if (c < 5) out[c] = rank_of_degree(off, n, th[c]);
+  if (c < 7) out[c] = rank_of_degree(off, n, th[c]);
 }
 
 __global__ void __launch_bounds__(256) k_sort_runs_reg(const int64_t* __restrict__ off,
@@ -457,12 +457,12 @@ __global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restric
 
 // one CTA per run of up to 256*ITEMS neighbours: block radix sort over the
 // rank bits (+ one bit that sends the padding to the end)
-template <int ITEMS>
-__global__ void __launch_bounds__(256) k_sort_runs_block(const int64_t* __restrict__ off,
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_sort_runs_block(const int64_t* __restrict__ off,
                                                          int64_t rlo, int64_t rhi, int endbit,
                                                          int32_t* __restrict__ arcs,
                                                          int* __restrict__ bad) {
-  using Sort = cub::BlockRadixSort<uint32_t, 256, ITEMS>;
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
   __shared__ typename Sort::TempStorage tmp;
   __shared__ int s_dup;
   const int t = threadIdx.x;
@@ -473,20 +473,20 @@ __global__ void __launch_bounds__(256) k_sort_runs_block(const int64_t* __restri
     uint32_t k[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {  // striped load; the sort ignores input order
-      const int idx = i * 256 + t;
+      const int idx = i * NT + t;
       k[i] = idx < d ? (uint32_t)arcs[o + idx] : 0xFFFFFFFFu;
     }
     Sort(tmp).SortBlockedToStriped(k, 0, endbit);
     bool dup = false;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * 256 + t;
+      const int idx = i * NT + t;
       if (idx < d) arcs[o + idx] = (int32_t)k[i];
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-      const int idx = i * 256 + t;
+      const int idx = i * NT + t;
       if (idx + 1 < d) dup |= arcs[o + idx] == arcs[o + idx + 1];
     }
     if (dup) s_dup = 1;
@@ -524,14 +524,14 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
   cudaStream_t st = e->stream;
   if (slots == 0 || n == 0) return GS_OK;
   int64_t* d_cls = nullptr;
-  GS_TRY(e->alloc_n(&d_cls, 5));
+  GS_TRY(e->alloc_n(&d_cls, 7));
   k_sort_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
-  int64_t r[5], hbig = 0;
+  int64_t r[7], hbig = 0;
   GS_CUDA(cudaMemcpyAsync(r, d_cls, sizeof(r), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_cls);
   e->launches++;
-  const int64_t r2 = r[0], r33 = r[1], r257 = r[2], r1025 = r[3], rbig = r[4];
+  const int64_t r2 = r[0], r33 = r[1], r257 = r[2], rbig = r[6];
   auto warps_grid = [&](int64_t runs) {
     const int64_t gr = (runs + 7) / 8;
     return (unsigned)(gr < (int64_t)e->sms * 64 ? gr : (int64_t)e->sms * 64);
@@ -549,14 +549,26 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
                                                                         d_bad);
     e->launches++;
   }
-  if (r1025 > r257) {
-    k_sort_runs_block<4><<<blocks_grid(r1025 - r257), 256, 0, st>>>(g.off, r257, r1025, endbit,
-                                                                   arcs, d_bad);
+  // CTA classes sized to the run: (256,512] 128x4, (512,1024] 128x8, (1024,2048] 256x8,
+  // (2048,4096) 256x16 slots
+  if (r[3] > r[2]) {
+    k_sort_runs_block<128, 4><<<blocks_grid(r[3] - r[2]), 128, 0, st>>>(g.off, r[2], r[3], endbit,
+                                                                        arcs, d_bad);
     e->launches++;
   }
-  if (rbig > r1025) {
-    k_sort_runs_block<16><<<blocks_grid(rbig - r1025), 256, 0, st>>>(g.off, r1025, rbig, endbit,
-                                                                    arcs, d_bad);
+  if (r[4] > r[3]) {
+    k_sort_runs_block<128, 8><<<blocks_grid(r[4] - r[3]), 128, 0, st>>>(g.off, r[3], r[4], endbit,
+                                                                        arcs, d_bad);
+    e->launches++;
+  }
+  if (r[5] > r[4]) {
+    k_sort_runs_block<256, 8><<<blocks_grid(r[5] - r[4]), 256, 0, st>>>(g.off, r[4], r[5], endbit,
+                                                                        arcs, d_bad);
+    e->launches++;
+  }
+  if (r[6] > r[5]) {
+    k_sort_runs_block<256, 16><<<blocks_grid(r[6] - r[5]), 256, 0, st>>>(g.off, r[5], r[6],
+                                                                         endbit, arcs, d_bad);
     e->launches++;
   }
   GS_CUDA(cudaGetLastError());
