@@ -329,30 +329,63 @@ __global__ void k_scatter_edges(const int32_t* __restrict__ uv, int64_t m, int64
 
 // CSR input: slot i of caller vertex u lands at the same position of u's
 // rank-space run (no atomics); validates ids and the strictly increasing runs.
-__global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n,
+static constexpr int64_t kHeavyScatter = 512;  // == deg_class(2): rclass[2] starts them
+
+__global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n, int64_t u0, int64_t u1,
                               const int32_t* __restrict__ chunk, int64_t i0, int64_t i1,
                               int32_t prev, const int32_t* __restrict__ rank,
                               const int64_t* __restrict__ noff, int32_t* __restrict__ out,
                               int* __restrict__ bad) {
-  // slots [i0, i1) of the caller's adjacency, values in chunk[i - i0];
-  // prev = the caller's adjacency[i0 - 1] (run-order check across chunks)
-  const int64_t base = i0 + blockIdx.x * (int64_t)blockDim.x;
-  const int64_t i = base + threadIdx.x;
-  __shared__ int64_t vlo, vhi;
-  if (threadIdx.x == 0) {
-    int64_t last = base + blockDim.x - 1;
-    if (last >= i1) last = i1 - 1;
-    vlo = upper_bound_i64(off, 0, n + 1, base) - 1;
-    vhi = upper_bound_i64(off, 0, n + 1, last);
+  // One warp per caller vertex u in [u0, u1): the slots of u's run inside
+  // [i0, i1) (values in chunk[i - i0]) go, relabelled, to the same positions
+  // of u's rank-space run -- coalesced reads and writes per run, three
+  // broadcast loads per vertex.  prev = the caller's adjacency[i0 - 1] (the
+  // run-order check across chunks).
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = u0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); u < u1;
+       u += nw) {
+    const int64_t ou = off[u], eu = off[u + 1];
+    if (eu - ou >= kHeavyScatter) continue;  // k_scatter_csr_heavy
+    const int64_t lo = max(ou, i0), hi = min(eu, i1);
+    if (lo >= hi) continue;
+    const int64_t base = noff[rank[u]] - ou;
+    bool b3 = false, b4 = false;
+    for (int64_t i = lo + lane; i < hi; i += 32) {
+      int32_t v = chunk[i - i0];
+      if (v < 0 || v >= n || v == u) { b3 = true; v = (int32_t)u; }
+      if (i > ou && (i > i0 ? chunk[i - 1 - i0] : prev) >= v) b4 = true;  // runs increasing
+      out[base + i] = rank[v];
+    }
+    if (b3) atomicExch(bad, 3);
+    if (b4) atomicExch(bad, 4);
   }
-  __syncthreads();
-  if (i >= i1) return;
-  const int64_t u = upper_bound_i64(off, vlo, vhi, i) - 1;
-  int32_t v = chunk[i - i0];
-  if (v < 0 || v >= n || v == u) { atomicExch(bad, 3); v = (int32_t)u; }
-  if (i > off[u] && (i > i0 ? chunk[i - 1 - i0] : prev) >= v) atomicExch(bad, 4);  // increasing
-  const int32_t ru = rank[u];
-  out[noff[ru] + (i - off[u])] = rank[v];
+}
+
+// Runs of kHeavyScatter+ neighbours (a contiguous rank range [rh, n)): one CTA
+// per run, so a hub's run does not serialise on one warp.
+__global__ void k_scatter_csr_heavy(const int64_t* __restrict__ off, int64_t n, int64_t rh,
+                                    const int32_t* __restrict__ orig,
+                                    const int32_t* __restrict__ chunk, int64_t i0, int64_t i1,
+                                    int32_t prev, const int32_t* __restrict__ rank,
+                                    const int64_t* __restrict__ noff, int32_t* __restrict__ out,
+                                    int* __restrict__ bad) {
+  for (int64_t r = rh + blockIdx.x; r < n; r += gridDim.x) {
+    const int64_t u = orig[r];
+    const int64_t ou = off[u];
+    const int64_t lo = max(ou, i0), hi = min(off[u + 1], i1);
+    if (lo >= hi) continue;
+    const int64_t base = noff[r] - ou;
+    bool b3 = false, b4 = false;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      int32_t v = chunk[i - i0];
+      if (v < 0 || v >= n || v == u) { b3 = true; v = (int32_t)u; }
+      if (i > ou && (i > i0 ? chunk[i - 1 - i0] : prev) >= v) b4 = true;
+      out[base + i] = rank[v];
+    }
+    if (b3) atomicExch(bad, 3);
+    if (b4) atomicExch(bad, 4);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -688,8 +721,13 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   int32_t* arcs = nullptr;
   GS_TRY(e->alloc_n(&arcs, 2 * m));
   if (m > 0) {
-    k_scatter_csr<<<grid_for(2 * m, 256), 256, 0, st>>>(off, n, adj, 0, 2 * m, 0, g.rank, g.off,
-                                                        arcs, d_bad);
+    k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
+                    0, st>>>(off, n, 0, n, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad);
+    const int64_t rh = h_cls[2];
+    if (n > rh)
+      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(n - rh, (int64_t)e->sms * 16), 256, 0,
+                            st>>>(off, n, rh, g.orig, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad);
+    e->launches++;
     e->launches++;
   }
   return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
@@ -754,9 +792,17 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
     GS_CUDA(cudaStreamWaitEvent(st, copied[k], 0));
-    k_scatter_csr<<<grid_for(len, 256), 256, 0, st>>>(d_off, n, ring[k], i0, i0 + len,
-                                                      i0 > 0 ? adj_host[i0 - 1] : 0, g.rank,
-                                                      g.off, arcs, d_bad);
+    // caller vertices whose runs meet [i0, i0 + len): host binary search
+    const int64_t ua = std::upper_bound(off_host, off_host + n + 1, i0) - off_host - 1;
+    const int64_t ub = std::upper_bound(off_host, off_host + n + 1, i0 + len - 1) - off_host;
+    k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for((ub - ua) * 32, 256), (int64_t)e->sms * 64),
+                    256, 0, st>>>(d_off, n, ua, ub, ring[k], i0, i0 + len,
+                                  i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad);
+    if (n > h_cls[2])
+      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(n - h_cls[2], (int64_t)e->sms * 16), 256, 0,
+                            st>>>(d_off, n, h_cls[2], g.orig, ring[k], i0, i0 + len,
+                                  i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad);
+    e->launches++;
     e->launches++;
     GS_CUDA(cudaEventRecord(freed[k], st));
     if (next < nchunks) GS_TRY(issue(next++));
