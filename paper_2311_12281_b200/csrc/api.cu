@@ -167,6 +167,7 @@ void gs_engine::free_state() {
   release(s.lmax);
   release(s.ctr);
   release(s.wq);
+  release(s.coreadj);
   release(s.thr);
   release(s.nlo);
   s = DevState();

@@ -172,11 +172,12 @@ __device__ __forceinline__ void hub_scan(const int32_t* __restrict__ adj, int64_
 __global__ void k_classify_thread(int64_t rlo, int64_t rhi, const int64_t* __restrict__ off,
                                   const int32_t* __restrict__ adj, const uint8_t* __restrict__ role,
                                   const int32_t* __restrict__ lmin, const int32_t* __restrict__ lmax,
-                                  uint8_t* __restrict__ fin) {
+                                  const uint8_t* __restrict__ near, uint8_t* __restrict__ fin) {
   for (int64_t v = rlo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < rhi;
        v += (int64_t)gridDim.x * blockDim.x) {
     if (role[v] == ROLE_CORE) { fin[v] = ROLE_CORE; continue; }
     if (lmax[v] >= 0) { fin[v] = ROLE_MEMBER; continue; }
+    if (near && !near[v]) { fin[v] = ROLE_OUTLIER; continue; }  // no clustered neighbour
     int cnt = 0;
     int32_t umin = 0x7fffffff, umax = -1;
     hub_scan(adj, off[v], off[v + 1], lmin, lmax, cnt, umin, umax);
@@ -187,13 +188,14 @@ __global__ void k_classify_thread(int64_t rlo, int64_t rhi, const int64_t* __res
 __global__ void k_classify_warp(int64_t rlo, int64_t rhi, const int64_t* __restrict__ off,
                                 const int32_t* __restrict__ adj, const uint8_t* __restrict__ role,
                                 const int32_t* __restrict__ lmin, const int32_t* __restrict__ lmax,
-                                uint8_t* __restrict__ fin) {
+                                const uint8_t* __restrict__ near, uint8_t* __restrict__ fin) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t v = rlo + wid; v < rhi; v += nw) {
     if (role[v] == ROLE_CORE) { if (lane == 0) fin[v] = ROLE_CORE; continue; }
     if (lmax[v] >= 0) { if (lane == 0) fin[v] = ROLE_MEMBER; continue; }
+    if (near && !near[v]) { if (lane == 0) fin[v] = ROLE_OUTLIER; continue; }
     int cnt = 0;
     int32_t umin = 0x7fffffff, umax = -1;
     const int64_t lo = off[v], hi = off[v + 1];
@@ -469,10 +471,63 @@ int phase_labels(gs_engine* e) {
 }
 
 // member attachment over this shard's similar core-noncore edges
+// flag[w] = 1 for every neighbour w of a vertex v with key[v] >= 0 (cores:
+// role; clustered vertices: lmax).  Ranks [0, rh) one warp per vertex, the
+// heavy ranks [rh, n) (degree >= 512) one CTA per vertex, so a hub's list does
+// not serialise on one warp.  The attach pass skips the b's whose owned edges
+// cannot join a core and a non-core; classify skips the hub scan of vertices
+// with no clustered neighbour.
+template <bool CORES>
+__global__ void k_flag_neighbours(int64_t rlo, int64_t rhi, bool per_cta,
+                                  const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ adj,
+                                  const uint8_t* __restrict__ role,
+                                  const int32_t* __restrict__ lmax, uint8_t* __restrict__ flag) {
+  const int lane = per_cta ? threadIdx.x : (threadIdx.x & 31);
+  const int step = per_cta ? blockDim.x : 32;
+  const int64_t g0 = per_cta ? blockIdx.x : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t ng = per_cta ? gridDim.x : ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = rlo + g0; v < rhi; v += ng) {
+    if (CORES ? role[v] != ROLE_CORE : lmax[v] < 0) continue;
+    for (int64_t i = off[v] + lane; i < off[v + 1]; i += step) flag[adj[i]] = 1;
+  }
+}
+
+__global__ void k_clustered_degree(int64_t n, const int64_t* __restrict__ off,
+                                   const int32_t* __restrict__ lmax,
+                                   unsigned long long* __restrict__ sum) {
+  unsigned long long acc = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    if (lmax[v] >= 0) acc += (unsigned long long)(off[v + 1] - off[v]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
+}
+
+template <bool CORES>
+static void flag_neighbours(gs_engine* e, uint8_t* flag) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  const int64_t n = g.n, rh = g.rclass[2];
+  if (rh > 0)
+    k_flag_neighbours<CORES><<<(unsigned)std::min<int64_t>(grid_for(rh * 32, 256),
+                                                            (int64_t)e->sms * 64),
+                               256, 0, e->stream>>>(0, rh, false, g.off, g.adj, s.role, s.lmax,
+                                                    flag);
+  if (n > rh)
+    k_flag_neighbours<CORES><<<(unsigned)std::min<int64_t>(n - rh, (int64_t)e->sms * 16), 256, 0,
+                               e->stream>>>(rh, n, true, g.off, g.adj, s.role, s.lmax, flag);
+  e->launches += 2;
+}
+
 int phase_attach(gs_engine* e) {
   if (e->ncores == 0) return GS_OK;
   DevGraph& g = e->g;
   DevState& s = e->s;
+  if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, g.n));
+  GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)(g.n > 0 ? g.n : 1), e->stream));
+  if (g.n > 0) flag_neighbours<true>(e, s.coreadj);
   GS_TRY(run_similarity(e, MODE_ATTACH, e->eps, e->mu));
   if (g.m > 0) {
     k_attach<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax,
@@ -517,16 +572,38 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     if (cluster_out) GS_TRY(e->alloc_n(&d_cluster_out, n));
   }
   const int64_t rsplit = e->ncores > 0 ? g.rclass[1] : 0;
+  // near[v]: v has a clustered neighbour (only those can be hubs).  Flagging
+  // costs the clustered vertices' degrees, the hub scan it saves the rest's:
+  // flag only when the clustered side is the smaller one.
+  bool use_near = false;
+  if (e->ncores > 0 && n > 0) {
+    unsigned long long* d_sum = nullptr;
+    GS_TRY(e->alloc_n(&d_sum, 1));
+    GS_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), str));
+    k_clustered_degree<<<gridv(e, n), 256, 0, str>>>(n, g.off, s.lmax, d_sum);
+    unsigned long long h_sum = 0;
+    GS_CUDA(cudaMemcpyAsync(&h_sum, d_sum, sizeof(h_sum), cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+    e->release(d_sum);
+    e->launches++;
+    use_near = (int64_t)h_sum < g.m;  // < half of the 2m arcs
+    if (use_near) {
+      if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, n));
+      GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)n, str));
+      flag_neighbours<false>(e, s.coreadj);
+    }
+  }
+  const uint8_t* near = use_near ? s.coreadj : nullptr;
   if (e->ncores == 0 && n > 0)  // nothing is clustered: every vertex is an outlier
     GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
   if (rsplit > 0) {
     k_classify_thread<<<gridv(e, rsplit), 256, 0, str>>>(0, rsplit, g.off, g.adj, s.role, s.lmin,
-                                                        s.lmax, fin);
+                                                        s.lmax, near, fin);
     e->launches++;
   }
   if (e->ncores > 0 && n > rsplit) {
     k_classify_warp<<<gridv(e, (n - rsplit) * 32), 256, 0, str>>>(rsplit, n, g.off, g.adj, s.role,
-                                                                 s.lmin, s.lmax, fin);
+                                                                 s.lmin, s.lmax, near, fin);
     e->launches++;
   }
   cudaEvent_t c0, c1;

@@ -56,6 +56,7 @@ struct DevState {
   int2* thr = nullptr;          // [dmax+1] per-degree O(1) thresholds for this epsilon
   int32_t* nlo = nullptr;       // [n] hub split of each adjacency run
   int32_t* wq = nullptr;        // work-queue heads for persistent kernels
+  uint8_t* coreadj = nullptr;   // [n] has a core neighbour (set before attach)
 };
 
 enum Ctr {
@@ -91,6 +92,7 @@ struct SimParams {
   uint8_t* sim;
   uint64_t* bounds;
   uint8_t* role;
+  const uint8_t* coreadj;  // [n] vertex has a core neighbour (attach pass only)
   int32_t* parent;
   unsigned long long* ctr;
   int32_t* wq;

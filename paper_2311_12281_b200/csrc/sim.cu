@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
        b += (int64_t)gridDim.x * blockDim.x * w) {
     const int64_t e0 = P.eoff[b], e1 = P.eoff[b + 1];
     if (e0 == e1) continue;
+    if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
     const int64_t ob = P.off[b], eb = P.off[b + 1], db = eb - ob;
     for (int64_t e = e0; e < e1; ++e) {
       const int32_t a = P.adj[ob + (e - e0)];
@@ -222,6 +223,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     __syncthreads();
     const int64_t b = shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
+    if (P.mode >= MODE_UNION && !b_needed(P, b)) {
+      __syncthreads();  // s_item read by all before the next claim
+      continue;
+    }
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
     const int32_t* __restrict__ nb = P.adj + ob;
@@ -351,6 +356,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
     item = __shfl_sync(0xffffffffu, item, 0);
     const int64_t b = shard_top(rlo, rhi, item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
+    if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
     const int32_t* __restrict__ nb = P.adj + ob;
@@ -531,6 +537,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.sim = s.sim;
   P.bounds = s.bounds;
   P.role = s.role;
+  P.coreadj = s.coreadj;
   P.parent = s.parent;
   P.ctr = s.ctr;
   P.wq = s.wq;

@@ -54,6 +54,14 @@ __device__ __forceinline__ void apply_bounds(uint64_t* bounds, uint8_t* role, in
   else if (upper < mu) role[x] = ROLE_NONCORE;
 }
 
+// Can any edge owned by b need a decision in this mode?  Union needs b core;
+// attach needs b core or b adjacent to a core (coreadj, set before attach).
+__device__ __forceinline__ bool b_needed(const SimParams& P, int64_t b) {
+  if (P.mode == MODE_UNION) return ld_role(P.role, b) == ROLE_CORE;
+  if (P.mode == MODE_ATTACH) return ld_role(P.role, b) == ROLE_CORE || P.coreadj[b];
+  return true;
+}
+
 // Does edge (a, b) need a decision in this mode?
 __device__ __forceinline__ bool edge_needed(const SimParams& P, int64_t e, int32_t a,
                                             int32_t b) {
