@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--input", choices=["csr", "edges"], default="csr",
+                    help="csr: scan_in_memory's call on the reference CSR (default); edges: "
+                         "build from the device edge list inside the step (large scales)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU phase path even with one process")
     return ap.parse_args()
@@ -283,14 +286,19 @@ def run_ours(args):
             shard.run(args.mu, eps2, role_ptr, clus_ptr, on_dev, stats)
 
     # the reference Graph's CSR of the same graph (build_graph's output)
-    off_d = torch.empty(n + 1, dtype=torch.int64, device="cuda")
-    adj_d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
-    _lib.check(lib.gs_build_csr_device(n, m, uv.data_ptr(), off_d.data_ptr(), adj_d.data_ptr(),
-                                       None))
-    torch.cuda.synchronize()
+    if args.input == "csr":
+        off_d = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        adj_d = torch.empty(2 * m, dtype=torch.int32, device="cuda")
+        _lib.check(lib.gs_build_csr_device(n, m, uv.data_ptr(), off_d.data_ptr(), adj_d.data_ptr(),
+                                           None))
+        torch.cuda.synchronize()
 
     def step_device():
-        _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_d.data_ptr(), adj_d.data_ptr(), 1))
+        if args.input == "csr":
+            _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_d.data_ptr(), adj_d.data_ptr(),
+                                              1))
+        else:
+            _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv.data_ptr(), 1))
         scan_call(role_d.data_ptr(), clus_d.data_ptr(), 1, st)
 
     def barrier():
@@ -348,7 +356,7 @@ def run_ours(args):
 
     # ---- e2e through the C-ABI with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.input == "csr":
         off_h = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
         adj_h = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
         off_h.copy_(off_d)
@@ -404,8 +412,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "int32",
             "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05, scrambled ids), "
-                    "generated + normalised on the device; the reference-layout CSR built "
-                    "once on the device (gs_build_csr_device) before timing",
+                    "generated + normalised on the device" + (
+                        "; the reference-layout CSR built once on the device "
+                        "(gs_build_csr_device) before timing" if args.input == "csr" else ""),
             "config": {
                 "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
                             f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
@@ -413,8 +422,9 @@ def run_ours(args):
                 "parallelism": (f"edge-sharded x{world} (b % world), NCCL all-reduce/all-gather"
                                 if shard is not None else "single"),
                 "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
-                "step": "scan_in_memory's C-ABI call on the reference CSR: degree-rank "
-                        "relabel + identify + cluster + classify",
+                "step": ("scan_in_memory's C-ABI call on the reference CSR: degree-rank "
+                         "relabel + identify + cluster + classify") if args.input == "csr" else
+                        "device edge list -> rank-space CSR build + identify + cluster + classify",
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
