@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.cuh"
@@ -742,7 +743,11 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
 int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_host,
                         const int32_t* adj_host) {
   constexpr int kSlots = 4;
-  constexpr int64_t kChunk = (int64_t)1 << 24;  // 64 MB of adjacency per chunk
+  int64_t kChunk = (int64_t)1 << 24;  // 64 MB of adjacency per chunk
+  if (const char* c = getenv("GS_H2D_CHUNK")) {  // test hook: many small chunks
+    const long long v = atoll(c);
+    if (v >= 64) kChunk = v;
+  }
   cudaStream_t st = e->stream, cs = e->cstream;
   DevGraph& g = e->g;
   e->free_graph();

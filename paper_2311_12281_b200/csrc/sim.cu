@@ -201,7 +201,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
                                                  uint32_t hub_lo, uint32_t bm_words) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm = smem;  // [bm_words] + zero guard words (kept 16-byte aligned)
-  uint32_t* tab_s = smem + bm_words + 4;
+  // bitmap + >= 4 zero guard words, padded so the 16-byte buckets stay aligned
+  uint32_t* tab_s = smem + ((bm_words + 4 + 3) & ~3u);
   // survivors of the O(1) filter: where N(a) starts, (a, deg a), (j, c_min)
   int64_t* surv_oa = reinterpret_cast<int64_t*>(tab_s + (GTAB ? 0 : 4 * (size_t)tcap));
   int2* surv_ad = reinterpret_cast<int2*>(surv_oa + chunk);
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   C.tab = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : tab_s;
   C.nstash = &s_nstash;
   C.stash = s_stash;
-  for (uint32_t i = tid; i < bm_words + 4; i += NT) bm[i] = 0u;
+  for (uint32_t i = tid; i < ((bm_words + 4 + 3) & ~3u); i += NT) bm[i] = 0u;
 
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&P.wq[qi], 1);
@@ -448,7 +449,7 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
                        uint32_t tcap, int qi, int chunk) {
   if (rhi <= rlo) return GS_OK;
   const size_t smem =
-      (size_t)(P.bm_words + 4) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
+      (size_t)((P.bm_words + 4 + 3) & ~3u) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
   auto kern = k_sim_hash<NT, GTAB>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
