@@ -122,3 +122,52 @@ def test_invalid_csr_detected_across_chunks(chunk_env, chunk):
     oor[70][-1] = n + 5  # id out of range
     with pytest.raises(ValueError):
         gs.scan_in_memory(_csr(n, oor), 2, "0.5")
+
+
+def _random_graph(rng, n, m):
+    u = rng.integers(0, n, size=m)
+    # skew: a third of the endpoints from a small hot set (hubs)
+    hot = rng.integers(0, max(1, n // 50), size=m)
+    v = np.where(rng.random(m) < 0.33, hot, rng.integers(0, n, size=m))
+    keep = u != v
+    a, b = np.minimum(u, v)[keep], np.maximum(u, v)[keep]
+    key = np.unique(a.astype(np.int64) * n + b)
+    return np.stack([key // n, key % n], 1).astype(np.int32)
+
+
+@pytest.mark.parametrize("n", [5, 97, 1000, 4097, 30000, 65537, 262143, 262145, 300001])
+def test_vertex_count_sweep_against_oracle(orc, n):
+    """Sizes around the hub-bitmap (2^18 ranks) and alignment boundaries."""
+    rng = np.random.default_rng(n)
+    e = _random_graph(rng, n, min(8 * n, 1_500_000))
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.2", 2), ("0.45", 4)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        r_roles, r_cl = _run(g, mu, eps)
+        np.testing.assert_array_equal(r_roles, roles, err_msg=f"n={n} {eps} {mu}")
+        np.testing.assert_array_equal(r_cl, cl, err_msg=f"n={n} {eps} {mu}")
+
+
+@pytest.mark.parametrize("n", [4097, 30000, 262145])
+def test_vertex_count_sweep_sharded_and_out_of_core(orc, n):
+    """The same sizes through the sharded phases (2 and 3 simulated ranks) and
+    the HBM-capped partitioned engine with several partitions."""
+    from test_gpu_shards import sharded
+
+    rng = np.random.default_rng(n + 1)
+    e = _random_graph(rng, n, min(8 * n, 1_500_000))
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    roles, cl = orc.serial_scan(c, 2, "0.2")
+    for world in (2, 3):
+        for r_roles, r_cl, _ in sharded(g, 2, "0.2", world):
+            np.testing.assert_array_equal(r_roles, roles, err_msg=f"n={n} w{world}")
+            np.testing.assert_array_equal(r_cl, cl, err_msg=f"n={n} w{world}")
+    dmax = int(np.diff(g.vertex_offsets).max())
+    budget = 13 * n + (2 << 20) + 8 * (dmax + 1) + max(2 * g.m // 4 * 4 * 4 // 3, 8 * 4 * dmax)
+    plan = gs.partition_graph(g, budget)
+    r, s = gs.scan_out_of_core(gs.GraphMeta.from_graph(g), plan, 2, "0.2")
+    assert s.extra["partitions"] >= 2
+    np.testing.assert_array_equal(r.role_codes, roles, err_msg=f"n={n} ooc")
+    np.testing.assert_array_equal(r.cluster_ids, cl, err_msg=f"n={n} ooc")
