@@ -294,7 +294,9 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def step_device():
-        if args.input == "csr":
+        if args.input == "csr" and shard is not None:  # partitioned build + row exchange
+            shard.load_csr(m, off_d.data_ptr(), adj_d.data_ptr(), 1)
+        elif args.input == "csr":
             _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_d.data_ptr(), adj_d.data_ptr(),
                                               1))
         else:
@@ -366,8 +368,11 @@ def run_ours(args):
         st2 = _lib.GsStats()
 
         def step_host():
-            _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_h.data_ptr(), adj_h.data_ptr(),
-                                              0))
+            if shard is not None:
+                shard.load_csr(m, off_h.data_ptr(), adj_h.data_ptr(), 0)
+            else:
+                _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off_h.data_ptr(),
+                                                  adj_h.data_ptr(), 0))
             scan_call(role_h.data_ptr(), clus_h.data_ptr(), 0, st2)
 
         for _ in range(max(1, args.warmup)):
@@ -419,7 +424,8 @@ def run_ours(args):
                 "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
                             f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
                 "n": n, "m": m, "seed": args.seed,
-                "parallelism": (f"edge-sharded x{world} (b % world), NCCL all-reduce/all-gather"
+                "parallelism": (f"edge-sharded x{world} (b % world), build partitioned by "
+                                f"rank-space rows; NCCL broadcast/all-reduce/all-gather"
                                 if shard is not None else "single"),
                 "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
                 "step": ("scan_in_memory's C-ABI call on the reference CSR: degree-rank "

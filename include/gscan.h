@@ -119,6 +119,18 @@ int gs_engine_load_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* offset
 int gs_engine_load_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_uv,
                          int on_device);
 
+/* Partitioned load for the sharded scan: every rank computes the
+ * degree-rank relabel, but relabels and sorts only the rank-space rows of its
+ * part (~2m/part_world arcs) into adj_out (caller-owned device buffer, 2m
+ * int32).  slot_bounds[part_world + 1] receives every part's slot range; the
+ * caller fills the other parts' slices of adj_out (e.g. NCCL broadcast from
+ * each owner, paper_2311_12281_b200/dist.py) and then calls
+ * gs_engine_load_finish.  part_world = 1 is gs_engine_load_csr. */
+int gs_engine_load_csr_part(gs_engine* e, int64_t n, int64_t m, const int64_t* offsets,
+                            const int32_t* adjacency, int on_device, int part_rank,
+                            int part_world, int32_t* adj_out, int64_t* slot_bounds);
+int gs_engine_load_finish(gs_engine* e);
+
 /* Run the three phases on the loaded graph.  Outputs are written to host
  * buffers (out_on_device = 0) or device buffers (1), indexed by the caller's
  * vertex ids.  role_out / cluster_out may be NULL to skip the copy. */

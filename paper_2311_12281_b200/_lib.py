@@ -76,6 +76,9 @@ SIGNATURES = [
     ("gs_engine_stream", _P, [_P]),
     ("gs_engine_load_csr", ctypes.c_int, [_P, _I64, _I64, _P, _P, ctypes.c_int]),
     ("gs_engine_load_edges", ctypes.c_int, [_P, _I64, _I64, _P, ctypes.c_int]),
+    ("gs_engine_load_csr_part", ctypes.c_int,
+     [_P, _I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]),
+    ("gs_engine_load_finish", ctypes.c_int, [_P]),
     ("gs_engine_scan", ctypes.c_int,
      [_P, _I32, ctypes.POINTER(GsEps2), _P, _P, ctypes.c_int, ctypes.POINTER(GsStats)]),
     ("gs_engine_set_shard", ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int]),

@@ -148,7 +148,9 @@ void gs_engine::trim(size_t need) {
 
 void gs_engine::free_graph() {
   release(g.off);
-  release(g.adj);
+  if (!g.adj_external) release(g.adj);
+  if (pend_bad) { release(pend_bad); pend_bad = nullptr; }
+  pend_finish = false;
   release(g.orig);
   release(g.rank);
   release(g.eoff);
@@ -272,6 +274,63 @@ int gs_engine_load_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* offset
   cudaStreamSynchronize(e->stream);
   e->last_h2d_ms = 0;  // inside the build (overlapped)
   cudaEventElapsedTime(&e->last_build_ms, t0, t1);
+  cudaEventDestroy(t0); cudaEventDestroy(t1);
+  return rc;
+}
+
+int gs_engine_load_csr_part(gs_engine* e, int64_t n, int64_t m, const int64_t* offsets,
+                            const int32_t* adjacency, int on_device, int part_rank,
+                            int part_world, int32_t* adj_out, int64_t* slot_bounds) {
+  GS_TRY(load_common(e, n, m));
+  if (part_world < 1 || part_rank < 0 || part_rank >= part_world) {
+    set_error("invalid part");
+    return GS_EINVAL;
+  }
+  if (part_world > 1 && !adj_out) {
+    set_error("a partitioned build needs the caller's adjacency buffer (2m int32)");
+    return GS_EINVAL;
+  }
+  int64_t h_ends[2] = {0, 0};
+  if (on_device) {
+    GS_CUDA(cudaMemcpyAsync(&h_ends[0], offsets, sizeof(int64_t), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaMemcpyAsync(&h_ends[1], offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+  } else {
+    h_ends[0] = offsets[0];
+    h_ends[1] = offsets[n];
+  }
+  if (h_ends[0] != 0 || h_ends[1] != 2 * m) {
+    set_error("invalid graph: vertex_offsets must start at 0 and end at 2m");
+    return GS_EINVAL;
+  }
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0); cudaEventCreate(&t1);
+  cudaEventRecord(t0, e->stream);
+  int rc = on_device ? build_from_csr(e, n, m, offsets, adjacency, part_rank, part_world, adj_out,
+                                      slot_bounds)
+                     : build_from_csr_host(e, n, m, offsets, adjacency, part_rank, part_world,
+                                           adj_out, slot_bounds);
+  cudaEventRecord(t1, e->stream);
+  cudaStreamSynchronize(e->stream);
+  e->last_h2d_ms = 0;
+  cudaEventElapsedTime(&e->last_build_ms, t0, t1);
+  cudaEventDestroy(t0); cudaEventDestroy(t1);
+  return rc;
+}
+
+int gs_engine_load_finish(gs_engine* e) {
+  if (!e) { set_error("engine is NULL"); return GS_EINVAL; }
+  GS_CUDA(cudaSetDevice(e->device));
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0); cudaEventCreate(&t1);
+  cudaEventRecord(t0, e->stream);
+  int rc = finish_build(e);
+  cudaEventRecord(t1, e->stream);
+  cudaStreamSynchronize(e->stream);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, t0, t1);
+  e->last_build_ms += ms;
   cudaEventDestroy(t0); cudaEventDestroy(t1);
   return rc;
 }

@@ -336,7 +336,7 @@ __global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n, int64_
                               const int32_t* __restrict__ chunk, int64_t i0, int64_t i1,
                               int32_t prev, const int32_t* __restrict__ rank,
                               const int64_t* __restrict__ noff, int32_t* __restrict__ out,
-                              int* __restrict__ bad) {
+                              int* __restrict__ bad, int64_t row_lo, int64_t row_hi) {
   // One warp per caller vertex u in [u0, u1): the slots of u's run inside
   // [i0, i1) (values in chunk[i - i0]) go, relabelled, to the same positions
   // of u's rank-space run -- coalesced reads and writes per run, three
@@ -350,7 +350,9 @@ __global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n, int64_
     if (eu - ou >= kHeavyScatter) continue;  // k_scatter_csr_heavy
     const int64_t lo = max(ou, i0), hi = min(eu, i1);
     if (lo >= hi) continue;
-    const int64_t base = noff[rank[u]] - ou;
+    const int64_t ru = rank[u];
+    if (ru < row_lo || ru >= row_hi) continue;  // another part's row
+    const int64_t base = noff[ru] - ou;
     bool b3 = false, b4 = false;
     for (int64_t i = lo + lane; i < hi; i += 32) {
       int32_t v = chunk[i - i0];
@@ -366,12 +368,12 @@ __global__ void k_scatter_csr(const int64_t* __restrict__ off, int64_t n, int64_
 // Runs of kHeavyScatter+ neighbours (a contiguous rank range [rh, n)): one CTA
 // per run, so a hub's run does not serialise on one warp.
 __global__ void k_scatter_csr_heavy(const int64_t* __restrict__ off, int64_t n, int64_t rh,
-                                    const int32_t* __restrict__ orig,
+                                    int64_t rhi, const int32_t* __restrict__ orig,
                                     const int32_t* __restrict__ chunk, int64_t i0, int64_t i1,
                                     int32_t prev, const int32_t* __restrict__ rank,
                                     const int64_t* __restrict__ noff, int32_t* __restrict__ out,
                                     int* __restrict__ bad) {
-  for (int64_t r = rh + blockIdx.x; r < n; r += gridDim.x) {
+  for (int64_t r = rh + blockIdx.x; r < rhi; r += gridDim.x) {
     const int64_t u = orig[r];
     const int64_t ou = off[u];
     const int64_t lo = max(ou, i0), hi = min(off[u + 1], i1);
@@ -553,7 +555,8 @@ __global__ void k_tail_extract(const uint64_t* __restrict__ keys, int64_t cnt, i
 }
 
 // Sort every run of `arcs` (offsets g.off) in place.
-static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad) {
+static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad,
+                     int64_t row_lo, int64_t row_hi) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
   if (slots == 0 || n == 0) return GS_OK;
@@ -565,7 +568,8 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
   GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_cls);
   e->launches++;
-  const int64_t r2 = r[0], r33 = r[1], r257 = r[2], rbig = r[6];
+  for (int k = 0; k < 7; ++k) r[k] = std::min(std::max(r[k], row_lo), row_hi);  // this part
+  const int64_t r2 = std::max(r[0], row_lo), r33 = r[1], r257 = r[2], rbig = r[6];
   auto warps_grid = [&](int64_t runs) {
     const int64_t gr = (runs + 7) / 8;
     return (unsigned)(gr < (int64_t)e->sms * 64 ? gr : (int64_t)e->sms * 64);
@@ -606,19 +610,22 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
     e->launches++;
   }
   GS_CUDA(cudaGetLastError());
-  // long runs
+  // long runs of this part: ranks [rbig, row_hi)
+  int64_t hend = 0;
   GS_CUDA(cudaMemcpyAsync(&hbig, g.off + rbig, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaMemcpyAsync(&hend, g.off + row_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaStreamSynchronize(st));
-  const int64_t cnt = slots - hbig;
+  const int64_t cnt = hend - hbig;
+  (void)slots;
   if (cnt > 0) {
     const int B = bits_for(n - 1);
-    const int R = bits_for(n - 1 - rbig);
+    const int R = bits_for(row_hi - 1 - rbig);
     uint64_t *k1 = nullptr, *k2 = nullptr;
     GS_TRY(e->alloc_n(&k1, cnt));
     GS_TRY(e->alloc_n(&k2, cnt));
-    const int64_t nv = n - rbig;
-    k_tail_keys<<<(unsigned)(nv < 65535 * 4 ? nv : 65535 * 4), 256, 0, st>>>(g.off, rbig, n, arcs,
-                                                                            B, k1);
+    const int64_t nv = row_hi - rbig;
+    k_tail_keys<<<(unsigned)(nv < 65535 * 4 ? nv : 65535 * 4), 256, 0, st>>>(g.off, rbig, row_hi,
+                                                                            arcs, B, k1);
     cub::DoubleBuffer<uint64_t> db(k1, k2);
     GS_TRY(cub_call(e, [&](void* t, size_t& b) {
       return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, B + R, st);
@@ -634,7 +641,8 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
 // shared tail: arcs scattered into their runs (`arcs`, 2m) -> sorted CSR
 static int finish_scatter_build(gs_engine* e, int64_t n, int64_t m, int32_t* arcs,
                                 const int64_t* h_cls, int* d_bad) {
-  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad));
+  e->g.adj_external = false;
+  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, 0, n));
   e->g.adj = arcs;
   return finish_rest(e, n, m, h_cls, d_bad);
 }
@@ -702,8 +710,89 @@ int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
   return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
 }
 
-int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
-                   const int32_t* adj) {
+// rank-space row bounds of every part: first row whose offset reaches
+// k * slots / world (k = 0..world); parts get ~equal numbers of arcs
+__global__ void k_row_split(const int64_t* __restrict__ off, int64_t n, int64_t slots, int world,
+                            int64_t* __restrict__ rows) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > world) return;
+  if (k == world) { rows[k] = n; return; }
+  const int64_t target = (int64_t)((__int128)slots * k / world);
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] < target) lo = mid + 1; else hi = mid;
+  }
+  rows[k] = lo;
+}
+
+// rows (and slot bounds) of every part; [row_lo, row_hi) of part_rank
+static int part_rows(gs_engine* e, int64_t n, int64_t slots, int part_rank, int part_world,
+                     int64_t* row_lo, int64_t* row_hi, int64_t* slot_bounds) {
+  if (part_world <= 1) {
+    *row_lo = 0;
+    *row_hi = n;
+    if (slot_bounds) { slot_bounds[0] = 0; slot_bounds[1] = slots; }
+    return GS_OK;
+  }
+  DevGraph& g = e->g;
+  int64_t* d_rows = nullptr;
+  GS_TRY(e->alloc_n(&d_rows, part_world + 1));
+  k_row_split<<<grid_for(part_world + 1, 64), 64, 0, e->stream>>>(g.off, n, slots, part_world,
+                                                                 d_rows);
+  e->launches++;
+  std::vector<int64_t> rows(part_world + 1), sb(part_world + 1);
+  GS_CUDA(cudaMemcpyAsync(rows.data(), d_rows, sizeof(int64_t) * (part_world + 1),
+                          cudaMemcpyDeviceToHost, e->stream));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  e->release(d_rows);
+  for (int k = 0; k <= part_world; ++k)
+    GS_CUDA(cudaMemcpyAsync(&sb[k], g.off + rows[k], sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            e->stream));
+  GS_CUDA(cudaStreamSynchronize(e->stream));
+  *row_lo = rows[part_rank];
+  *row_hi = rows[part_rank + 1];
+  if (slot_bounds)
+    for (int k = 0; k <= part_world; ++k) slot_bounds[k] = sb[k];
+  return GS_OK;
+}
+
+// the arcs buffer: the caller's (partitioned builds) or a fresh one
+static int arcs_buffer(gs_engine* e, int64_t slots, int32_t* adj_out, int32_t** arcs) {
+  if (adj_out) {
+    *arcs = adj_out;
+    e->g.adj_external = true;
+    return GS_OK;
+  }
+  e->g.adj_external = false;
+  return e->alloc_n(arcs, slots);
+}
+
+// after the scatter: sort this part's runs, then finish now or on finish_build
+static int finish_part(gs_engine* e, int64_t n, int64_t m, int32_t* arcs, const int64_t* h_cls,
+                       int* d_bad, int64_t row_lo, int64_t row_hi, bool defer) {
+  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, row_lo, row_hi));
+  e->g.adj = arcs;
+  if (!defer) return finish_rest(e, n, m, h_cls, d_bad);
+  GS_CUDA(cudaStreamSynchronize(e->stream));  // the part is complete for the exchange
+  e->pend_finish = true;
+  e->pend_n = n;
+  e->pend_m = m;
+  for (int c = 0; c <= DevGraph::kClasses; ++c) e->pend_cls[c] = h_cls[c];
+  e->pend_bad = d_bad;
+  return GS_OK;
+}
+
+int finish_build(gs_engine* e) {
+  if (!e->pend_finish) { set_error("no partitioned build waiting to be finished"); return GS_EINVAL; }
+  e->pend_finish = false;
+  int* d_bad = e->pend_bad;
+  e->pend_bad = nullptr;
+  return finish_rest(e, e->pend_n, e->pend_m, e->pend_cls, d_bad);
+}
+
+int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const int32_t* adj,
+                   int part_rank, int part_world, int32_t* adj_out, int64_t* slot_bounds) {
   cudaStream_t st = e->stream;
   DevGraph& g = e->g;
   e->free_graph();
@@ -719,19 +808,22 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   int64_t h_cls[DevGraph::kClasses + 1];
   GS_TRY(rank_and_offsets(e, n, deg, h_cls));
   e->release(deg);
+  int64_t row_lo = 0, row_hi = n;
+  GS_TRY(part_rows(e, n, 2 * m, part_rank, part_world, &row_lo, &row_hi, slot_bounds));
   int32_t* arcs = nullptr;
-  GS_TRY(e->alloc_n(&arcs, 2 * m));
+  GS_TRY(arcs_buffer(e, 2 * m, adj_out, &arcs));
   if (m > 0) {
     k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
-                    0, st>>>(off, n, 0, n, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad);
-    const int64_t rh = h_cls[2];
-    if (n > rh)
-      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(n - rh, (int64_t)e->sms * 16), 256, 0,
-                            st>>>(off, n, rh, g.orig, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad);
-    e->launches++;
-    e->launches++;
+                    0, st>>>(off, n, 0, n, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad, row_lo,
+                             row_hi);
+    const int64_t rh = std::max<int64_t>(h_cls[2], row_lo);
+    if (row_hi > rh)
+      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(row_hi - rh, (int64_t)e->sms * 16), 256,
+                            0, st>>>(off, n, rh, row_hi, g.orig, adj, 0, 2 * m, 0, g.rank, g.off,
+                                     arcs, d_bad);
+    e->launches += 2;
   }
-  return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
+  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1);
 }
 
 // Host CSR (the reference Graph in pinned or pageable memory): the offsets
@@ -741,7 +833,8 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
 // transfer overlaps the relabel and the scatter.  HBM holds the chunk ring,
 // not a second copy of the adjacency.
 int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_host,
-                        const int32_t* adj_host) {
+                        const int32_t* adj_host, int part_rank, int part_world,
+                        int32_t* adj_out, int64_t* slot_bounds) {
   constexpr int kSlots = 4;
   int64_t kChunk = (int64_t)1 << 24;  // 64 MB of adjacency per chunk
   if (const char* c = getenv("GS_H2D_CHUNK")) {  // test hook: many small chunks
@@ -791,8 +884,11 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
   int64_t h_cls[DevGraph::kClasses + 1];
   GS_TRY(rank_and_offsets(e, n, deg, h_cls));
   e->release(deg);
+  int64_t row_lo = 0, row_hi = n;
+  GS_TRY(part_rows(e, n, slots, part_rank, part_world, &row_lo, &row_hi, slot_bounds));
   int32_t* arcs = nullptr;
-  GS_TRY(e->alloc_n(&arcs, slots));
+  GS_TRY(arcs_buffer(e, slots, adj_out, &arcs));
+  const int64_t rh = std::max<int64_t>(h_cls[2], row_lo);
   for (int64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
@@ -802,13 +898,13 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     const int64_t ub = std::upper_bound(off_host, off_host + n + 1, i0 + len - 1) - off_host;
     k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for((ub - ua) * 32, 256), (int64_t)e->sms * 64),
                     256, 0, st>>>(d_off, n, ua, ub, ring[k], i0, i0 + len,
-                                  i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad);
-    if (n > h_cls[2])
-      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(n - h_cls[2], (int64_t)e->sms * 16), 256, 0,
-                            st>>>(d_off, n, h_cls[2], g.orig, ring[k], i0, i0 + len,
-                                  i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad);
-    e->launches++;
-    e->launches++;
+                                  i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad,
+                                  row_lo, row_hi);
+    if (row_hi > rh)
+      k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(row_hi - rh, (int64_t)e->sms * 16), 256,
+                            0, st>>>(d_off, n, rh, row_hi, g.orig, ring[k], i0, i0 + len,
+                                     i0 > 0 ? adj_host[i0 - 1] : 0, g.rank, g.off, arcs, d_bad);
+    e->launches += 2;
     GS_CUDA(cudaEventRecord(freed[k], st));
     if (next < nchunks) GS_TRY(issue(next++));
   }
@@ -820,8 +916,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     cudaEventDestroy(copied[k]);
     cudaEventDestroy(freed[k]);
   }
-  cudaEventDestroy(ready);
-  return finish_scatter_build(e, n, m, arcs, h_cls, d_bad);
+  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1);
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ d, int64_t n, int64_t* __restrict__ o) {

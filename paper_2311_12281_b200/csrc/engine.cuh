@@ -34,6 +34,7 @@ struct DevGraph {
   // rank boundaries of degree classes: first rank with degree >= kDegClass[i]
   static constexpr int kClasses = 6;
   int64_t rclass[kClasses] = {0};
+  bool adj_external = false;  // adj is a caller buffer (partitioned build), not ours
 };
 
 // degree-class thresholds used to route edges to kernels (by HIGH endpoint):
@@ -131,6 +132,11 @@ struct gs_engine {
   gs::Eps2 eps{};
   unsigned long long ncores = 0;
   float phase_ms[GS_PH_COUNT] = {0};    // timings of the sharded phase calls
+  // partitioned build (gs_engine_load_csr_part) waiting for gs_engine_load_finish
+  bool pend_finish = false;
+  int64_t pend_n = 0, pend_m = 0;
+  int64_t pend_cls[gs::DevGraph::kClasses + 1] = {0};
+  int* pend_bad = nullptr;
   // host-side pinned staging for counters
   unsigned long long* h_ctr = nullptr;
   std::vector<cudaEvent_t> ev;
@@ -148,11 +154,18 @@ struct gs_engine {
 namespace gs {
 // build.cu
 int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* edges_dev);
+// Partitioned builds: with part_world > 1 only the rank-space rows of part
+// part_rank (~2m/part_world arcs each) are built, into adj_out (caller-owned,
+// 2m) when given; slot_bounds[part_world + 1] receives every part's slot range;
+// the engine then waits for finish_build once the caller filled the other parts.
 int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off_dev,
-                   const int32_t* adj_dev);
+                   const int32_t* adj_dev, int part_rank = 0, int part_world = 1,
+                   int32_t* adj_out = nullptr, int64_t* slot_bounds = nullptr);
 // host CSR: adjacency streamed in chunks on cstream, scattered as it lands
 int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_host,
-                        const int32_t* adj_host);
+                        const int32_t* adj_host, int part_rank = 0, int part_world = 1,
+                        int32_t* adj_out = nullptr, int64_t* slot_bounds = nullptr);
+int finish_build(gs_engine* e);
 // sim.cu
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
 int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split

@@ -48,6 +48,24 @@ def all_gather_varlen(t: torch.Tensor, n_valid: int, group=None) -> torch.Tensor
     return torch.cat([o[:s] for o, s in zip(out, sizes)])
 
 
+def exchange_row_slices(buf: torch.Tensor, bounds, group=None) -> None:
+    """Part k's slice buf[bounds[k]:bounds[k+1]] is broadcast from rank k, so
+    every rank ends with the whole buffer (the partitioned build's exchange)."""
+    world = dist.get_world_size(group)
+    for k in range(world):
+        lo, hi = int(bounds[k]), int(bounds[k + 1])
+        if hi > lo:
+            src = dist.get_global_rank(group, k) if group is not None else k
+            dist.broadcast(buf[lo:hi], src=src, group=group)
+
+
+def all_ok(rc: int, device, group=None) -> bool:
+    """True iff every rank's return code is GS_OK (so all ranks fail together)."""
+    ok = torch.tensor([1 if rc == _lib.GS_OK else 0], dtype=torch.int32, device=device)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    return int(ok.item()) == 1
+
+
 def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
     """Sum the per-rank counters, max the timings (whole-job view)."""
     ints = ["sim_evals", "adj_probes", "union_retries", "probe_bound_violations",
@@ -65,7 +83,12 @@ def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
 
 
 class ShardedScan:
-    """Run the phases of one engine as this rank's shard of a scan."""
+    """Run the phases of one engine as this rank's shard of a scan.
+
+    ``load_csr`` is the partitioned build: each rank relabels and sorts 1/world
+    of the rank-space rows, the row slices are broadcast from their owners
+    (NCCL), and every rank finishes the same full CSR -- the build's work
+    divides by world instead of being replicated."""
 
     def __init__(self, engine: _lib.Engine, n: int, group=None):
         self.eng = engine
@@ -79,6 +102,25 @@ class ShardedScan:
         self.counts = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
         self.pairs = torch.empty((max(self.n, 1), 2), dtype=torch.int32, device=dev)
         self.labels = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
+
+    def load_csr(self, m: int, offsets: int, adjacency: int, on_device: int) -> None:
+        """Partitioned gs_engine_load_csr (the reference CSR at the given
+        pointers, host or device) with the row slices exchanged by broadcast."""
+        lib, h, n, g = self.lib, self.eng.handle, self.n, self.group
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if getattr(self, "adj", None) is None or self.adj.numel() != max(2 * m, 1):
+            self.adj = torch.empty(max(2 * m, 1), dtype=torch.int32, device=dev)
+        bounds = (ctypes.c_int64 * (self.world + 1))()
+        rc = lib.gs_engine_load_csr_part(h, n, m, offsets, adjacency, on_device, self.rank,
+                                         self.world, self.adj.data_ptr(), bounds)
+        everyone_ok = all_ok(rc, dev, g)  # every rank fails together
+        if rc != _lib.GS_OK:
+            _lib.check(rc)
+        if not everyone_ok:
+            raise ValueError("invalid graph (detected by another rank's part)")
+        exchange_row_slices(self.adj, list(bounds), g)                     # exchange 0
+        if self.world > 1:
+            _lib.check(lib.gs_engine_load_finish(h))
 
     def run(self, mu: int, eps2: _lib.GsEps2, role_out: int, cluster_out: int,
             out_on_device: int, stats: Optional[_lib.GsStats] = None) -> _lib.GsStats:

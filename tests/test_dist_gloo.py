@@ -25,7 +25,8 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2311_12281_b200 import _lib
-        from paper_2311_12281_b200.dist import all_gather_varlen, reduce_stats
+        from paper_2311_12281_b200.dist import (all_gather_varlen, all_ok, exchange_row_slices,
+                                                reduce_stats)
 
         # variable-length all-gather of (core, root) pairs, rank order kept
         k = 3 if rank == 0 else 5
@@ -43,7 +44,15 @@ def _worker(rank, world, port, q):
         st.sim_evals = 10 + rank
         st.phase_ms[2] = 1.0 + rank
         reduce_stats(st)
-        q.put((rank, out.tolist(), c.tolist(), lab.tolist(), st.sim_evals, st.phase_ms[2]))
+        # partitioned build: part k of the adjacency lives on rank k only
+        bounds = [0, 7, 12]
+        buf = torch.full((12,), -1, dtype=torch.int32)
+        buf[bounds[rank]:bounds[rank + 1]] = torch.arange(bounds[rank], bounds[rank + 1],
+                                                          dtype=torch.int32)
+        exchange_row_slices(buf, bounds)
+        oks = (all_ok(0, "cpu"), all_ok(_lib.GS_EINVAL if rank == 1 else 0, "cpu"))
+        q.put((rank, out.tolist(), c.tolist(), lab.tolist(), st.sim_evals, st.phase_ms[2],
+               buf.tolist(), oks))
     finally:
         dist.destroy_process_group()
 
@@ -59,8 +68,10 @@ def test_collectives_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, out, c, lab, evals, ph in res:
+    for rank, out, c, lab, evals, ph, buf, oks in res:
         assert out == [[0, 0], [1, 0], [2, 0], [100, 1], [101, 1], [102, 1], [103, 1], [104, 1]]
         assert c == [3, 10]
         assert lab == [4, 1]
         assert evals == 21 and ph == 2.0
+        assert buf == list(range(12))
+        assert oks == (True, False)

@@ -21,14 +21,48 @@ import paper_2311_12281_b200 as gs  # noqa: E402
 from paper_2311_12281_b200 import _lib  # noqa: E402
 
 
-def sharded(g, mu, eps, world):
+def partitioned_load(engs, g, on_device=False):
+    """gs_engine_load_csr_part on every simulated rank, then the row slices
+    copied owner -> everyone (what dist.ShardedScan.load_csr broadcasts)."""
+    lib = _lib.load()
+    n, m, world = g.n, g.m, len(engs)
+    bufs = [torch.empty(max(2 * m, 1), dtype=torch.int32, device="cuda") for _ in engs]
+    if on_device:
+        off_d = torch.from_numpy(np.asarray(g.vertex_offsets)).cuda()
+        adj_d = torch.from_numpy(np.asarray(g.adjacency)).cuda()
+        off_p, adj_p = off_d.data_ptr(), adj_d.data_ptr()
+    else:
+        off_p, adj_p = g.vertex_offsets.ctypes.data, g.adjacency.ctypes.data
+    bounds = []
+    for r, e in enumerate(engs):
+        b = (ctypes.c_int64 * (world + 1))()
+        _lib.check(lib.gs_engine_load_csr_part(e.handle, n, m, off_p, adj_p, int(on_device), r,
+                                               world, bufs[r].data_ptr(), b))
+        bounds.append([int(x) for x in b])
+    assert all(b == bounds[0] for b in bounds)
+    torch.cuda.synchronize()
+    for k in range(world):
+        lo, hi = bounds[0][k], bounds[0][k + 1]
+        for r in range(world):
+            if r != k and hi > lo:
+                bufs[r][lo:hi].copy_(bufs[k][lo:hi])
+    torch.cuda.synchronize()
+    if world > 1:
+        for e in engs:
+            _lib.check(lib.gs_engine_load_finish(e.handle))
+    return bufs
+
+
+def sharded(g, mu, eps, world, partitioned=False, on_device=False):
     lib = _lib.load()
     n, m = g.n, g.m
     eps2 = _lib.eps2_struct(gs.epsilon_fraction(eps))
     engs = [_lib.Engine() for _ in range(world)]
+    keep = partitioned_load(engs, g, on_device) if partitioned else None
     for r, e in enumerate(engs):
-        _lib.check(lib.gs_engine_load_csr(e.handle, n, m, g.vertex_offsets.ctypes.data,
-                                          g.adjacency.ctypes.data, 0))
+        if not partitioned:
+            _lib.check(lib.gs_engine_load_csr(e.handle, n, m, g.vertex_offsets.ctypes.data,
+                                              g.adjacency.ctypes.data, 0))
         _lib.check(lib.gs_engine_set_shard(e.handle, r, world))
         _lib.check(lib.gs_engine_phase_begin(e.handle, mu, ctypes.byref(eps2)))
     cnt = [torch.empty(2 * n, dtype=torch.int32, device="cuda") for _ in range(world)]
@@ -72,6 +106,7 @@ def sharded(g, mu, eps, world):
         outs.append((roles, cl, stats.sim_evals))
     for e in engs:
         e.close()
+    del keep
     return outs
 
 
@@ -112,3 +147,29 @@ def test_sharded_golden_corpus(golden):
                 np.testing.assert_array_equal(cl, golden.get(k, f"c{jj}_cluster"))
             n_cfg += 1
     assert n_cfg > 100
+
+
+@pytest.mark.parametrize("world,on_device", [(2, False), (3, True), (4, False), (8, True)])
+def test_partitioned_build_matches_single_gpu_and_oracle(orc, world, on_device):
+    """Each rank builds 1/world of the rank-space rows; after the exchange all
+    ranks hold the same CSR and produce the single-GPU canonical result."""
+    n, e = orc.rmat(15, seed=6)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.2", 3), ("0.5", 5)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        for r_roles, r_cl, _ in sharded(g, mu, eps, world, partitioned=True, on_device=on_device):
+            np.testing.assert_array_equal(r_roles, roles, err_msg=f"w{world} {eps} {mu}")
+            np.testing.assert_array_equal(r_cl, cl, err_msg=f"w{world} {eps} {mu}")
+
+
+def test_partitioned_build_rejects_invalid_part():
+    lib = _lib.load()
+    g = make_graph(14, sorted(TWO_COMMUNITIES))
+    eng = _lib.Engine()
+    b = (ctypes.c_int64 * 3)()
+    with pytest.raises(ValueError):  # a partitioned build needs the caller's buffer
+        _lib.check(lib.gs_engine_load_csr_part(eng.handle, g.n, g.m, g.vertex_offsets.ctypes.data,
+                                               g.adjacency.ctypes.data, 0, 0, 2, None, b))
+    with pytest.raises(ValueError):
+        _lib.check(lib.gs_engine_load_finish(eng.handle))
