@@ -727,7 +727,7 @@ __global__ void k_row_split(const int64_t* __restrict__ off, int64_t n, int64_t 
 }
 
 // rows (and slot bounds) of every part; [row_lo, row_hi) of part_rank
-static int part_rows(gs_engine* e, int64_t n, int64_t slots, int part_rank, int part_world,
+int part_rows(gs_engine* e, int64_t n, int64_t slots, int part_rank, int part_world,
                      int64_t* row_lo, int64_t* row_hi, int64_t* slot_bounds) {
   if (part_world <= 1) {
     *row_lo = 0;

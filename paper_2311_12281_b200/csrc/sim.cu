@@ -120,7 +120,8 @@ __device__ __forceinline__ void prepass_finish(int64_t v, uint32_t dv, uint32_t 
   role[v] = (int64_t)lower >= mu ? ROLE_CORE : (int64_t)upper < mu ? ROLE_NONCORE : ROLE_UNKNOWN;
 }
 
-__global__ void k_prepass_thread(int64_t rlo, int64_t rhi, const int64_t* __restrict__ off,
+__global__ void k_prepass_thread(int64_t rlo, int64_t rhi, int64_t own_lo, int64_t own_hi,
+                                 const int64_t* __restrict__ off,
                                  const int32_t* __restrict__ adj, const uint32_t* __restrict__ deg,
                                  const int2* __restrict__ thr, int32_t mu, int rank, int world,
                                  uint64_t* __restrict__ bounds, uint8_t* __restrict__ role,
@@ -130,6 +131,10 @@ __global__ void k_prepass_thread(int64_t rlo, int64_t rhi, const int64_t* __rest
        v += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t dv = deg[v];
     uint32_t sim = 0, dis = 0, mine = 0;
+    if (v < own_lo || v >= own_hi) {  // another rank's row: initial bounds only
+      prepass_finish(v, dv, 0, 0, mu, bounds, role);
+      continue;
+    }
     for (int64_t i = off[v]; i < off[v + 1]; ++i) {
       const int32_t w = adj[i];
       prepass_edge(dv, v, deg[w], w, thr, rank, world, sim, dis, mine);
@@ -145,7 +150,8 @@ __global__ void k_prepass_thread(int64_t rlo, int64_t rhi, const int64_t* __rest
   }
 }
 
-__global__ void k_prepass_warp(int64_t rlo, int64_t rhi, const int64_t* __restrict__ off,
+__global__ void k_prepass_warp(int64_t rlo, int64_t rhi, int64_t own_lo, int64_t own_hi,
+                                 const int64_t* __restrict__ off,
                                const int32_t* __restrict__ adj, const uint32_t* __restrict__ deg,
                                const int2* __restrict__ thr, int32_t mu, int rank, int world,
                                uint64_t* __restrict__ bounds, uint8_t* __restrict__ role,
@@ -157,6 +163,10 @@ __global__ void k_prepass_warp(int64_t rlo, int64_t rhi, const int64_t* __restri
   for (int64_t v = rlo + wid; v < rhi; v += nw) {
     const uint32_t dv = deg[v];
     uint32_t sim = 0, dis = 0, mine = 0;
+    if (v < own_lo || v >= own_hi) {  // another rank's row: initial bounds only
+      if (lane == 0) prepass_finish(v, dv, 0, 0, mu, bounds, role);
+      continue;
+    }
     for (int64_t i = off[v] + lane; i < off[v + 1]; i += 32) {
       const int32_t w = adj[i];
       prepass_edge(dv, v, deg[w], w, thr, rank, world, sim, dis, mine);
@@ -486,23 +496,29 @@ static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
 // hub bitmap range: the top 2^18 ranks (32 KB of shared memory per CTA)
 static constexpr int64_t kHubBits = 1 << 18;
 
+// Sharded runs split the pre-pass by rank-space rows: each rank folds ALL the
+// O(1)-decided edges of its own rows into their bounds (each vertex counted by
+// one rank, so the exchanged counts sum exactly), instead of every rank
+// reading every arc for the edges it owns.
 int run_prepass(gs_engine* e, int32_t mu) {
   DevGraph& g = e->g;
   DevState& s = e->s;
   const int64_t n = g.n, rsplit = g.rclass[1];
   if (n == 0) return GS_OK;
+  int64_t own_lo = 0, own_hi = n;
+  if (e->shard_world > 1)
+    GS_TRY(part_rows(e, n, 2 * g.m, e->shard_rank, e->shard_world, &own_lo, &own_hi, nullptr));
   uint32_t* deg = nullptr;
   GS_TRY(e->alloc_n(&deg, n));
   k_degrees<<<grid_for(n, 256), 256, 0, e->stream>>>(g.off, n, deg);
   if (rsplit > 0)
     k_prepass_thread<<<(unsigned)std::min<int64_t>(grid_for(rsplit, 256), (int64_t)e->sms * 32), 256,
-                       0, e->stream>>>(0, rsplit, g.off, g.adj, deg, s.thr, mu, e->shard_rank,
-                                       e->shard_world, s.bounds, s.role, s.ctr);
+                       0, e->stream>>>(0, rsplit, own_lo, own_hi, g.off, g.adj, deg, s.thr, mu, 0,
+                                       1, s.bounds, s.role, s.ctr);
   if (n > rsplit)
     k_prepass_warp<<<(unsigned)std::min<int64_t>(grid_for((n - rsplit) * 32, 256),
                                                  (int64_t)e->sms * 32), 256, 0, e->stream>>>(
-        rsplit, n, g.off, g.adj, deg, s.thr, mu, e->shard_rank, e->shard_world, s.bounds, s.role,
-        s.ctr);
+        rsplit, n, own_lo, own_hi, g.off, g.adj, deg, s.thr, mu, 0, 1, s.bounds, s.role, s.ctr);
   e->launches += 3;
   GS_CUDA(cudaGetLastError());
   e->release(deg);
