@@ -1,7 +1,7 @@
 """Where does a bench step's time go?  Host wall time per C-ABI call (with a
 stream sync on each side) against the engine's own phase events.
 
-    python tools/diag_step.py [scale] [steps]
+    python tools/diag_step.py [scale] [steps] [eps] [mu]
 """
 
 import ctypes
@@ -20,6 +20,8 @@ from fractions import Fraction  # noqa: E402
 def main():
     scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+    eps = sys.argv[3] if len(sys.argv) > 3 else "0.5"
+    mu = int(sys.argv[4]) if len(sys.argv) > 4 else 5
     lib = _lib.load()
     n = 1 << scale
     cnt = 16 << scale
@@ -39,7 +41,7 @@ def main():
     torch.cuda.synchronize()
     csr = os.environ.get("GS_DIAG_EDGES") is None  # default: the bench's CSR call
     eng = _lib.Engine()
-    eps2 = _lib.eps2_struct(Fraction("0.5"))
+    eps2 = _lib.eps2_struct(Fraction(eps))
     role = torch.empty(n, dtype=torch.uint8, device="cuda")
     clus = torch.empty(n, dtype=torch.int32, device="cuda")
     st = _lib.GsStats()
@@ -51,7 +53,7 @@ def main():
         else:
             _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv.data_ptr(), 1))
         t1 = time.perf_counter()
-        _lib.check(lib.gs_engine_scan(eng.handle, 5, ctypes.byref(eps2), role.data_ptr(),
+        _lib.check(lib.gs_engine_scan(eng.handle, mu, ctypes.byref(eps2), role.data_ptr(),
                                       clus.data_ptr(), 1, ctypes.byref(st)))
         t2 = time.perf_counter()
         ph = [round(st.phase_ms[k], 2) for k in range(9)]
