@@ -171,6 +171,8 @@ void gs_engine::free_state() {
   release(s.wq);
   release(s.coreadj);
   release(s.thr);
+  release(s.rdeg);
+  release(s.dxs);
   release(s.nlo);
   s = DevState();
 }

@@ -20,6 +20,28 @@
 
 namespace gs {
 
+__device__ __forceinline__ int64_t lower_bound_run(const int32_t* __restrict__ a, int64_t lo,
+                                                   int64_t hi, int64_t key) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t rdeg_at(const int32_t* rdeg, int64_t dmax, int64_t d) {
+  return rdeg[d < 0 ? 0 : (d > dmax + 2 ? dmax + 2 : d)];
+}
+
+// first index of b's owned prefix that can survive the O(1) bounds: the
+// survivors are the suffix with deg(a) >= max(xmin - 1, simmax + 1)
+__device__ __forceinline__ int64_t survivor_start(const SimParams& P, const int32_t* nb,
+                                                  int64_t nlow, int2 th, int64_t dmax) {
+  if (P.mode > MODE_CLEANUP) return 0;  // union / attach re-decide O(1) edges too
+  const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
+  return lower_bound_run(nb, 0, nlow, rdeg_at(P.rdeg, dmax, dstart));
+}
+
 // ---------------------------------------------------------------------------
 // tiny b: one thread per high endpoint b (deg < 64), its owned edges in
 // order, merging two short runs.  Walking b's edges sequentially lets each
@@ -36,7 +58,8 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
     if (e0 == e1) continue;
     if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
     const int64_t ob = P.off[b], eb = P.off[b + 1], db = eb - ob;
-    for (int64_t e = e0; e < e1; ++e) {
+    const int64_t j0 = survivor_start(P, P.adj + ob, e1 - e0, P.thr[db], P.dmax);
+    for (int64_t e = e0 + j0; e < e1; ++e) {
       const int32_t a = P.adj[ob + (e - e0)];
       const int64_t ia0 = P.off[a], ea = P.off[a + 1];
       const int64_t da = ea - ia0;
@@ -118,6 +141,76 @@ __device__ __forceinline__ void prepass_finish(int64_t v, uint32_t dv, uint32_t 
   const uint64_t lower = 1 + (uint64_t)sim, upper = (uint64_t)dv + 1 - dis;
   bounds[v] = lower | (upper << 32);
   role[v] = (int64_t)lower >= mu ? ROLE_CORE : (int64_t)upper < mu ? ROLE_NONCORE : ROLE_UNKNOWN;
+}
+
+// Degree tables for rank-space O(1) decisions.  Degrees ascend with the rank,
+// so "deg(w) < d" is "w < rdeg[d]", and every O(1)-decided set of a vertex's
+// neighbours is a prefix or suffix of its sorted run:
+//   rdeg[d]  first rank with degree >= d (d in [0, dmax+2])
+//   dx[d]    smallest high degree dh with d + 1 < xmin[dh] (low degree d is
+//            dissimilar-by-bound against every dh >= dx[d]); dmax+1: none
+//   ds[d]    largest high degree dh with d <= simmax[dh]; -1: none
+__global__ void k_degree_tables(const int64_t* __restrict__ off, int64_t n, int64_t dmax,
+                                const int2* __restrict__ thr, int32_t* __restrict__ rdeg,
+                                int2* __restrict__ dxs) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d <= dmax + 2;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid + 1] - off[mid] < d) lo = mid + 1; else hi = mid;
+    }
+    rdeg[d] = (int32_t)lo;
+    if (d > dmax) continue;
+    int64_t a = 0, b = dmax + 1;  // xmin non-decreasing in dh: first dh with d + 1 < xmin
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (d + 1 < thr[mid].x) b = mid; else a = mid + 1;
+    }
+    int64_t c = 0, z = dmax + 1;  // simmax non-increasing in dh: first dh with simmax < d
+    while (c < z) {
+      const int64_t mid = (c + z) >> 1;
+      if (thr[mid].y < d) z = mid; else c = mid + 1;
+    }
+    dxs[d] = make_int2((int32_t)a, (int32_t)(c - 1));
+  }
+}
+
+// Lemma-1 pre-pass by binary search: four searches over v's sorted run give
+// its O(1)-decided similar / dissimilar counts without touching each arc.
+__global__ void k_prepass_bs(int64_t n, int64_t own_lo, int64_t own_hi, int64_t dmax,
+                             const int64_t* __restrict__ off, const int64_t* __restrict__ eoff,
+                             const int32_t* __restrict__ adj, const int2* __restrict__ thr,
+                             const int32_t* __restrict__ rdeg, const int2* __restrict__ dxs,
+                             int32_t mu, uint64_t* __restrict__ bounds,
+                             uint8_t* __restrict__ role, unsigned long long* __restrict__ ctr) {
+  unsigned long long decided = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = off[v], dv = off[v + 1] - o;
+    uint32_t sim = 0, dis = 0;
+    if (v >= own_lo && v < own_hi && dv > 0) {
+      const int64_t p0 = eoff[v + 1] - eoff[v];  // neighbours below v (v is their high end)
+      const int2 th = thr[dv];
+      const int64_t dl = lower_bound_run(adj, o, o + p0, rdeg_at(rdeg, dmax, (int64_t)th.x - 1)) - o;
+      const int64_t sl = lower_bound_run(adj, o, o + p0, rdeg_at(rdeg, dmax, (int64_t)th.y + 1)) - o;
+      const int2 xs = dxs[dv];
+      const int64_t dh = dv - (lower_bound_run(adj, o + p0, o + dv, rdeg_at(rdeg, dmax, xs.x)) - o);
+      const int64_t sh = lower_bound_run(adj, o + p0, o + dv,
+                                         rdeg_at(rdeg, dmax, min(xs.y + 1, xs.x))) - o - p0;
+      const int64_t slo = sl > dl ? sl - dl : 0;
+      dis = (uint32_t)(dl + dh);
+      sim = (uint32_t)(slo + (sh > 0 ? sh : 0));
+      decided += (unsigned long long)(dl + slo);
+    }
+    prepass_finish(v, (uint32_t)dv, sim, dis, mu, bounds, role);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) decided += __shfl_xor_sync(0xffffffffu, decided, o);
+  if ((threadIdx.x & 31) == 0 && decided) {
+    atomicAdd(&ctr[CTR_SIM_EVALS], decided);
+    atomicAdd(&ctr[CTR_BOUND_DECIDED], decided);
+  }
 }
 
 __global__ void k_prepass_thread(int64_t rlo, int64_t rhi, int64_t own_lo, int64_t own_hi,
@@ -244,7 +337,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
     bool built = false;
-    for (int64_t base = 0; base < nlow; base += chunk) {
+    const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
+    for (int64_t base = j0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
       __syncthreads();
       const int64_t lim = base + chunk < nlow ? base + chunk : nlow;
@@ -374,7 +468,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
     const int2 th = P.thr[db];
     bool built = false;
     uint32_t bsim = 0, bdis = 0;
-    for (int64_t base = 0; base < nlow; base += 32) {
+    const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
+    for (int64_t base = j0; base < nlow; base += 32) {
       const int64_t j = base + lane;
       int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
       int32_t a = 0, da = 0, cmin = 0;
@@ -508,20 +603,11 @@ int run_prepass(gs_engine* e, int32_t mu) {
   int64_t own_lo = 0, own_hi = n;
   if (e->shard_world > 1)
     GS_TRY(part_rows(e, n, 2 * g.m, e->shard_rank, e->shard_world, &own_lo, &own_hi, nullptr));
-  uint32_t* deg = nullptr;
-  GS_TRY(e->alloc_n(&deg, n));
-  k_degrees<<<grid_for(n, 256), 256, 0, e->stream>>>(g.off, n, deg);
-  if (rsplit > 0)
-    k_prepass_thread<<<(unsigned)std::min<int64_t>(grid_for(rsplit, 256), (int64_t)e->sms * 32), 256,
-                       0, e->stream>>>(0, rsplit, own_lo, own_hi, g.off, g.adj, deg, s.thr, mu, 0,
-                                       1, s.bounds, s.role, s.ctr);
-  if (n > rsplit)
-    k_prepass_warp<<<(unsigned)std::min<int64_t>(grid_for((n - rsplit) * 32, 256),
-                                                 (int64_t)e->sms * 32), 256, 0, e->stream>>>(
-        rsplit, n, own_lo, own_hi, g.off, g.adj, deg, s.thr, mu, 0, 1, s.bounds, s.role, s.ctr);
-  e->launches += 3;
+  k_prepass_bs<<<(unsigned)std::min<int64_t>(grid_for(n, 256), (int64_t)e->sms * 32), 256, 0,
+                 e->stream>>>(n, own_lo, own_hi, g.dmax, g.off, g.eoff, g.adj, s.thr, s.rdeg,
+                              s.dxs, mu, s.bounds, s.role, s.ctr);
+  e->launches++;
   GS_CUDA(cudaGetLastError());
-  e->release(deg);
   return GS_OK;
 }
 
@@ -531,6 +617,11 @@ int prepare_similarity(gs_engine* e, const Eps2& eps) {
   GS_TRY(e->alloc_n(&s.thr, g.dmax + 1));
   GS_TRY(e->alloc_n(&s.nlo, g.n));
   k_thresholds<<<grid_for(g.dmax + 1, 256), 256, 0, e->stream>>>(g.dmax, eps, s.thr);
+  GS_TRY(e->alloc_n(&s.rdeg, g.dmax + 3));
+  GS_TRY(e->alloc_n(&s.dxs, g.dmax + 1));
+  k_degree_tables<<<grid_for(g.dmax + 3, 256), 256, 0, e->stream>>>(g.off, g.n, g.dmax, s.thr,
+                                                                    s.rdeg, s.dxs);
+  e->launches++;
   const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
   const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
   if (g.n > 0) {
@@ -564,6 +655,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.gtab = nullptr;
   P.gtab_stride = 0;
   P.thr = s.thr;
+  P.rdeg = s.rdeg;
+  P.dmax = g.dmax;
   P.nlo = s.nlo;
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
