@@ -269,6 +269,19 @@ static int finish_rest(gs_engine* e, int64_t n, int64_t m, const int64_t* h_cls,
     set_error("invalid graph: adjacency is not symmetric");
     return GS_EINVAL;
   }
+  GS_CUDA(cudaGetLastError());
+  g.n = n;
+  g.m = m;
+  return GS_OK;  // the endpoint arrays are built on first use (ensure_endpoints)
+}
+
+// elo/ehi (endpoints of every oriented edge) for the edge-parallel cluster
+// kernels and the state export; a scan without cores never needs them
+int ensure_endpoints(gs_engine* e) {
+  DevGraph& g = e->g;
+  if (g.elo || g.m == 0) return GS_OK;
+  cudaStream_t st = e->stream;
+  const int64_t n = g.n, m = g.m;
   GS_TRY(e->alloc_n(&g.elo, m));
   GS_TRY(e->alloc_n(&g.ehi, m));
   const int64_t rsplit = g.rclass[1];  // degree >= 64 -> block per vertex
@@ -284,8 +297,6 @@ static int finish_rest(gs_engine* e, int64_t n, int64_t m, const int64_t* h_cls,
     e->launches++;
   }
   GS_CUDA(cudaGetLastError());
-  g.n = n;
-  g.m = m;
   return GS_OK;
 }
 

@@ -417,6 +417,7 @@ int phase_union(gs_engine* e) {
   DevGraph& g = e->g;
   DevState& s = e->s;
   if (g.m > 0) {
+    GS_TRY(ensure_endpoints(e));
     k_union_known<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.parent,
                                                        s.ctr, e->shard_rank, e->shard_world);
     e->launches++;
@@ -530,6 +531,7 @@ int phase_attach(gs_engine* e) {
   if (g.n > 0) flag_neighbours<true>(e, s.coreadj);
   GS_TRY(run_similarity(e, MODE_ATTACH, e->eps, e->mu));
   if (g.m > 0) {
+    GS_TRY(ensure_endpoints(e));
     k_attach<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax,
                                                   e->shard_rank, e->shard_world);
     e->launches++;
@@ -791,6 +793,7 @@ int export_state(gs_engine* e, int stage, int32_t* lower, int32_t* upper, uint8_
     int32_t* dpairs = nullptr;
     if (sim) GS_TRY(e->alloc_n(&ds, m));
     if (pairs) GS_TRY(e->alloc_n(&dpairs, 2 * m));
+    GS_TRY(ensure_endpoints(e));
     k_export_edges<<<gridv(e, m), 256, 0, str>>>(m, g.elo, g.ehi, g.orig, g.off, s.thr, s.sim, ds,
                                                  dpairs);
     e->launches++;

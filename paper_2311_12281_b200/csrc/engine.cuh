@@ -170,6 +170,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
                         const int32_t* adj_host, int part_rank = 0, int part_world = 1,
                         int32_t* adj_out = nullptr, int64_t* slot_bounds = nullptr);
 int finish_build(gs_engine* e);
+int ensure_endpoints(gs_engine* e);  // elo / ehi on first use
 // rank-space rows [row_lo, row_hi) of part part_rank (~slots/part_world arcs each)
 int part_rows(gs_engine* e, int64_t n, int64_t slots, int part_rank, int part_world,
               int64_t* row_lo, int64_t* row_hi, int64_t* slot_bounds);
