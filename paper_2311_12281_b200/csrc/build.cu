@@ -82,28 +82,6 @@ __global__ void k_deg_from_off(const int64_t* __restrict__ off, int64_t n,
   }
 }
 
-__global__ void k_rank_keys(const uint32_t* __restrict__ deg, int64_t n,
-                            uint64_t* __restrict__ keys) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    keys[v] = ((uint64_t)deg[v] << 32) | (uint64_t)v;
-}
-
-// sorted (deg, id) keys -> orig[rank], rank[orig], ndeg[rank]
-__global__ void k_rank_scatter(const uint64_t* __restrict__ keys, int64_t n,
-                               int32_t* __restrict__ orig, int32_t* __restrict__ rank,
-                               int64_t* __restrict__ ndeg) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[r];
-    int32_t v = (int32_t)(uint32_t)k;
-    orig[r] = v;
-    rank[v] = (int32_t)r;
-    ndeg[r] = (int64_t)(k >> 32);
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ndeg[n] = 0;
-}
-
 __global__ void k_arc_keys_edges(const int32_t* __restrict__ uv, int64_t m,
                                  const int32_t* __restrict__ rank, int B,
                                  uint64_t* __restrict__ keys) {
@@ -659,32 +637,69 @@ static int finish_scatter_build(gs_engine* e, int64_t n, int64_t m, int32_t* arc
 }
 
 // degrees -> (degree, id) order: orig[rank], rank[orig], rank-space offsets
+__global__ void k_iota(int64_t n, uint32_t* __restrict__ x) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    x[v] = (uint32_t)v;
+}
+
+// sorted (degree key, id value) -> orig[rank], rank[orig], ndeg[rank]
+__global__ void k_rank_scatter_pairs(const uint32_t* __restrict__ dk,
+                                     const uint32_t* __restrict__ ids, int64_t n,
+                                     int32_t* __restrict__ orig, int32_t* __restrict__ rank,
+                                     int64_t* __restrict__ ndeg) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = (int32_t)ids[r];
+    orig[r] = v;
+    rank[v] = (int32_t)r;
+    ndeg[r] = (int64_t)dk[r];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ndeg[n] = 0;
+}
+
+// degrees -> (degree, id) order: orig[rank], rank[orig], rank-space offsets.
+// A stable radix sort of the degrees with the ids as values (ids enter in
+// ascending order, so equal degrees keep id order) over only the bits the
+// largest degree needs: 3 passes at s24 instead of 8 over (degree, id) keys.
 static int rank_and_offsets(gs_engine* e, int64_t n, uint32_t* deg, int64_t* h_cls) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
-  uint64_t *vk = nullptr, *vk2 = nullptr;
-  GS_TRY(e->alloc_n(&vk, n));
-  GS_TRY(e->alloc_n(&vk2, n));
+  uint32_t *dk2 = nullptr, *ids = nullptr, *ids2 = nullptr, *dmx = nullptr;
+  GS_TRY(e->alloc_n(&dk2, n));
+  GS_TRY(e->alloc_n(&ids, n));
+  GS_TRY(e->alloc_n(&ids2, n));
+  GS_TRY(e->alloc_n(&dmx, 1));
+  uint32_t hmax = 0;
   if (n > 0) {
-    k_rank_keys<<<grid_for(n, 256), 256, 0, st>>>(deg, n, vk);
+    k_iota<<<grid_for(n, 256), 256, 0, st>>>(n, ids);
     e->launches++;
+    GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+      return cub::DeviceReduce::Max(t, b, deg, dmx, n, st);
+    }));
+    GS_CUDA(cudaMemcpyAsync(&hmax, dmx, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
   }
-  cub::DoubleBuffer<uint64_t> dbk(vk, vk2);
+  e->release(dmx);
+  cub::DoubleBuffer<uint32_t> dbk(deg, dk2), dbv(ids, ids2);
+  const int endbit = bits_for((int64_t)hmax);
   GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-    return cub::DeviceRadixSort::SortKeys(t, b, dbk, n, 0, 64, st);
+    return cub::DeviceRadixSort::SortPairs(t, b, dbk, dbv, n, 0, endbit, st);
   }));
   int64_t* ndeg = nullptr;
   GS_TRY(e->alloc_n(&g.orig, n));
   GS_TRY(e->alloc_n(&g.rank, n));
   GS_TRY(e->alloc_n(&ndeg, n + 1));
   if (n > 0) {
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), n, g.orig, g.rank, ndeg);
+    k_rank_scatter_pairs<<<grid_for(n, 256), 256, 0, st>>>(dbk.Current(), dbv.Current(), n,
+                                                           g.orig, g.rank, ndeg);
     e->launches++;
   } else {
     GS_CUDA(cudaMemsetAsync(ndeg, 0, sizeof(int64_t), st));
   }
-  e->release(vk);
-  e->release(vk2);
+  e->release(dk2);
+  e->release(ids);
+  e->release(ids2);
   GS_TRY(finish_offsets(e, n, ndeg, h_cls));
   e->release(ndeg);
   return GS_OK;

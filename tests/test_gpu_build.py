@@ -73,9 +73,9 @@ def test_every_sort_class_against_oracle(orc):
         np.testing.assert_array_equal(r.cluster_ids, cl)
 
 
-@pytest.mark.parametrize("chunk", [64, 1000, 4093, 1 << 16])
-def test_host_csr_many_chunks(orc, chunk_env, chunk):
-    n, e = orc.rmat(15, seed=4)
+@pytest.mark.parametrize("chunk,scale", [(64, 11), (1000, 14), (4093, 15), (1 << 16, 15)])
+def test_host_csr_many_chunks(orc, chunk_env, chunk, scale):
+    n, e = orc.rmat(scale, seed=4)
     g = make_graph(n, e)
     ref = _run(g, 3, "0.3")
     os.environ["GS_H2D_CHUNK"] = str(chunk)
