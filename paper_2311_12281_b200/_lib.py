@@ -160,17 +160,20 @@ def check(rc: int) -> None:
 _MASK64 = (1 << 64) - 1
 
 
-def eps2_struct(eps: Fraction, dmax: int | None = None) -> GsEps2:
+def eps2_struct(eps: Fraction, dmax=None) -> GsEps2:
     """epsilon (exact Fraction in (0,1]) -> exact epsilon^2 = p/q halves.
 
     p and q must fit in 128 bits for the device predicate.  When they do not
     (only for absurdly fine rationals) and the threshold is below what any
     edge of the graph can reach, the equivalent "everything similar" ratio is
-    used; otherwise ValueError.
+    used; otherwise ValueError.  ``dmax`` may be a callable (it is needed
+    only on that path).
     """
     f2 = eps * eps
     p, q = f2.numerator, f2.denominator
     if p >= 1 << 128 or q >= 1 << 128:
+        if callable(dmax):  # computed only on this (rare) path
+            dmax = dmax()
         if dmax is not None and p * (dmax + 1) ** 2 <= 4 * q:
             p, q = 1, 1 << 127  # every (c+2)^2/D >= 4/(dmax+1)^2 >= eps^2
         else:

@@ -228,6 +228,7 @@ void gs_engine_destroy(gs_engine* e) {
   for (auto& kv : e->cache) cudaFreeAsync(kv.second, e->stream);
   cudaStreamSynchronize(e->stream);
   cudaStreamSynchronize(e->cstream);
+  if (e->hstage) cudaFreeHost(e->hstage);
   cudaStreamDestroy(e->cstream);
   cudaStreamDestroy(e->stream);
   // hand the pool's reserved memory back (the release threshold keeps it

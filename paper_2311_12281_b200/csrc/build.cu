@@ -886,15 +886,58 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
   }
   cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
   GS_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
-  GS_CUDA(cudaMemcpyAsync(d_off, off_host, sizeof(int64_t) * (size_t)(n + 1),
-                          cudaMemcpyHostToDevice, st));
+  // Pageable caller arrays (numpy, array.array) go through a pinned staging
+  // ring filled by a multi-threaded host copy, so the DMA stays asynchronous
+  // and the link saturated; pinned arrays are streamed directly.
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, adj_host) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  int32_t* hring[kSlots] = {nullptr};
+  // small inputs copy directly (a pinned allocation would cost more than it saves)
+  const bool stage = !pinned && slots * (int64_t)sizeof(int32_t) >= ((int64_t)32 << 20);
+  if (stage) {
+    const size_t need = (size_t)std::min<int64_t>(kSlots, nchunks) * (size_t)kChunk * sizeof(int32_t);
+    if (e->hstage_bytes < need) {
+      if (e->hstage) cudaFreeHost(e->hstage);
+      e->hstage = nullptr;
+      e->hstage_bytes = 0;
+      GS_CUDA(cudaHostAlloc(&e->hstage, need, cudaHostAllocDefault));
+      e->hstage_bytes = need;
+    }
+    for (int k = 0; k < (int)std::min<int64_t>(kSlots, nchunks); ++k)
+      hring[k] = static_cast<int32_t*>(e->hstage) + (size_t)k * (size_t)kChunk;
+  }
+  if (stage) {  // the offsets through the staging slots too, slot by slot
+    const size_t ob = sizeof(int64_t) * (size_t)(n + 1);
+    const size_t sb = (size_t)kChunk * sizeof(int32_t);
+    const int nslots = (int)std::min<int64_t>(kSlots, nchunks);
+    for (size_t at = 0, i = 0; at < ob; at += sb, ++i) {
+      const int k = (int)(i % nslots);
+      const size_t len = std::min(sb, ob - at);
+      if (i >= (size_t)nslots) GS_CUDA(cudaEventSynchronize(copied[k]));
+      gs_parallel_copy(hring[k], reinterpret_cast<const char*>(off_host) + at, len);
+      GS_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(d_off) + at, hring[k], len,
+                              cudaMemcpyHostToDevice, st));
+      GS_CUDA(cudaEventRecord(copied[k], st));
+    }
+  } else {
+    GS_CUDA(cudaMemcpyAsync(d_off, off_host, sizeof(int64_t) * (size_t)(n + 1),
+                            cudaMemcpyHostToDevice, st));
+  }
   cudaEventRecord(ready, st);  // the ring is allocated and free from here on
   GS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
   auto issue = [&](int64_t c) -> int {
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
     if (c >= kSlots) GS_CUDA(cudaStreamWaitEvent(cs, freed[k], 0));
-    GS_CUDA(cudaMemcpyAsync(ring[k], adj_host + i0, sizeof(int32_t) * (size_t)len,
+    const int32_t* src = adj_host + i0;
+    if (stage) {  // the staging slot's previous DMA must be done before refilling it
+      GS_CUDA(cudaEventSynchronize(copied[k]));  // (the offsets' or chunk c - kSlots's)
+      gs_parallel_copy(hring[k], adj_host + i0, sizeof(int32_t) * (size_t)len);
+      src = hring[k];
+    }
+    GS_CUDA(cudaMemcpyAsync(ring[k], src, sizeof(int32_t) * (size_t)len,
                             cudaMemcpyHostToDevice, cs));
     GS_CUDA(cudaEventRecord(copied[k], cs));
     return GS_OK;

@@ -120,6 +120,9 @@ struct gs_engine {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cstream = nullptr;  // host->device copies overlapped with the build
+  // pinned staging for pageable host inputs (allocated on first use, kept)
+  void* hstage = nullptr;
+  size_t hstage_bytes = 0;
   uint64_t cap = 0;
   size_t live = 0, peak = 0;  // bytes in use (peak = high-water mark)
   size_t reserved = 0;        // bytes held: in use + cached free blocks
@@ -154,6 +157,9 @@ struct gs_engine {
   void free_graph();
   void free_state();
 };
+
+// ingest.cpp: multi-threaded host memcpy (pageable -> pinned staging)
+void gs_parallel_copy(void* dst, const void* src, size_t bytes);
 
 namespace gs {
 // build.cu

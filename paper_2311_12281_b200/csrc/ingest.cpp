@@ -234,3 +234,24 @@ extern "C" int gs_format_result(int64_t n, const uint8_t* role, const int32_t* c
   for (auto& t : ts) t.join();
   return GS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Parallel host copy (pageable caller arrays -> pinned staging) for the host
+// CSR load: the DMA engines only stream asynchronously from pinned memory, and
+// one thread's memcpy (~10 GB/s) would starve the ~55 GB/s link.
+#include <omp.h>
+
+void gs_parallel_copy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = 1 << 20;
+  if (bytes < 4 * kMin) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  const int nt = std::max(1, std::min(omp_get_max_threads(), (int)(bytes / kMin)));
+#pragma omp parallel num_threads(nt)
+  {
+    const int t = omp_get_thread_num();
+    const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
+    memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  }
+}

@@ -269,7 +269,7 @@ def scan_in_memory(g, mu: int, epsilon: EpsilonLike, *, workers: int = 1):
     f = _validate(mu, workers, epsilon)
     n, m, off, adj = graph_arrays(g)
     orig = as_array(g.orig_ids, np.uint32) if n else np.empty(0, np.uint32)
-    eps2 = _lib.eps2_struct(f, _dmax(off))
+    eps2 = _lib.eps2_struct(f, lambda: _dmax(off))
     roles = np.empty(n, dtype=np.uint8)
     cids = np.empty(n, dtype=np.int32)
     st = _lib.GsStats()
@@ -453,7 +453,7 @@ def identify_core(g, mu: int, epsilon: EpsilonLike, st: ClusterState, *, workers
         st._engine = _lib.Engine()
     h = st._engine.handle
     _lib.check(lib.gs_engine_load_csr(h, n, m, off.ctypes.data, adj.ctypes.data, 0))
-    eps2 = _lib.eps2_struct(f, _dmax(off))
+    eps2 = _lib.eps2_struct(f, lambda: _dmax(off))
     _lib.check(lib.gs_engine_phase_begin(h, int(mu), ctypes.byref(eps2)))
     _lib.check(lib.gs_engine_phase_identify(h, None))
     if on_edge is not None:
