@@ -90,8 +90,6 @@ struct SimParams {
   const int64_t* off;
   const int32_t* adj;
   const int64_t* eoff;
-  const int32_t* elo;
-  const int32_t* ehi;
   uint8_t* sim;
   uint64_t* bounds;
   uint8_t* role;

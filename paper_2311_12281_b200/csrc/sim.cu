@@ -640,8 +640,6 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.off = g.off;
   P.adj = g.adj;
   P.eoff = g.eoff;
-  P.elo = g.elo;
-  P.ehi = g.ehi;
   P.sim = s.sim;
   P.bounds = s.bounds;
   P.role = s.role;
