@@ -232,12 +232,21 @@ def run_ours(args):
     from paper_2311_12281_b200 import _lib
 
     rank, world, local = dist_env()
+    # GS_DIST_BACKEND=gloo runs N ranks on fewer GPUs (ranks share devices):
+    # a functional check of the multi-process path on a one-GPU box, not a
+    # scaling measurement (NCCL refuses two ranks on one device).
+    backend = os.environ.get("GS_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     lib = _lib.load()
     f = gs.epsilon_fraction(args.eps)
     eps2 = _lib.eps2_struct(f)
@@ -425,7 +434,10 @@ def run_ours(args):
                             f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
                 "n": n, "m": m, "seed": args.seed,
                 "parallelism": (f"edge-sharded x{world} (b % world), build partitioned by "
-                                f"rank-space rows; NCCL broadcast/all-reduce/all-gather"
+                                f"rank-space rows; {backend.upper()} broadcast/all-reduce/all-gather"
+                                + ("" if backend == "nccl" else
+                                   f" (ranks sharing {torch.cuda.device_count()} GPU(s): "
+                                   "functional check, not a scaling number)")
                                 if shard is not None else "single"),
                 "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
                 "step": ("scan_in_memory's C-ABI call on the reference CSR: degree-rank "

@@ -99,9 +99,23 @@ class ShardedScan:
         self.lib = _lib.load()
         _lib.check(self.lib.gs_engine_set_shard(engine.handle, self.rank, self.world))
         dev = torch.device("cuda", torch.cuda.current_device())
+        # the engine works on its own non-blocking stream; collectives run on
+        # (or are waited for by) torch's current stream
+        self.estream = torch.cuda.ExternalStream(engine.stream(), device=dev)
         self.counts = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
         self.pairs = torch.empty((max(self.n, 1), 2), dtype=torch.int32, device=dev)
         self.labels = torch.empty(2 * max(self.n, 1), dtype=torch.int32, device=dev)
+
+    def _after_collective(self) -> None:
+        """Order the engine stream after the exchange just issued: every
+        gs_engine_phase_* call that reads an exchanged buffer runs on the
+        engine's own non-blocking stream, which is not implicitly ordered
+        after torch's current stream (where NCCL's / gloo's work is waited
+        for).  Device-side wait, no host synchronisation.  (The engine side
+        synchronises its stream before returning a buffer to exchange.)"""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        self.estream.wait_event(ev)
 
     def load_csr(self, m: int, offsets: int, adjacency: int, on_device: int) -> None:
         """Partitioned gs_engine_load_csr (the reference CSR at the given
@@ -120,6 +134,7 @@ class ShardedScan:
             raise ValueError("invalid graph (detected by another rank's part)")
         exchange_row_slices(self.adj, list(bounds), g)                     # exchange 0
         if self.world > 1:
+            self._after_collective()
             _lib.check(lib.gs_engine_load_finish(h))
 
     def run(self, mu: int, eps2: _lib.GsEps2, role_out: int, cluster_out: int,
@@ -129,6 +144,7 @@ class ShardedScan:
         _lib.check(lib.gs_engine_phase_begin(h, int(mu), ctypes.byref(eps2)))
         _lib.check(lib.gs_engine_phase_identify(h, self.counts.data_ptr()))
         dist.all_reduce(self.counts[: 2 * n], op=dist.ReduceOp.SUM, group=g)    # exchange 1
+        self._after_collective()
         nc = ctypes.c_int64(0)
         _lib.check(lib.gs_engine_phase_resolve(h, self.counts.data_ptr(), ctypes.byref(nc)))
         labels_ptr = None
@@ -136,11 +152,13 @@ class ShardedScan:
             npairs = ctypes.c_int64(0)
             _lib.check(lib.gs_engine_phase_union(h, self.pairs.data_ptr(), ctypes.byref(npairs)))
             allp = all_gather_varlen(self.pairs, npairs.value, g).contiguous()  # exchange 2
+            self._after_collective()
             _lib.check(lib.gs_engine_phase_merge(h, allp.data_ptr() if len(allp) else None,
                                                  len(allp)))
             _lib.check(lib.gs_engine_phase_attach(h, self.labels.data_ptr()))
             dist.all_reduce(self.labels[:n], op=dist.ReduceOp.MIN, group=g)      # exchange 3
             dist.all_reduce(self.labels[n: 2 * n], op=dist.ReduceOp.MAX, group=g)
+            self._after_collective()
             labels_ptr = self.labels.data_ptr()
         else:
             _lib.check(lib.gs_engine_phase_merge(h, None, 0))

@@ -69,6 +69,7 @@ def sharded(g, mu, eps, world, partitioned=False, on_device=False):
     for e, c in zip(engs, cnt):
         _lib.check(lib.gs_engine_phase_identify(e.handle, c.data_ptr()))
     tot = torch.stack(cnt).sum(0).to(torch.int32).contiguous()          # all-reduce SUM
+    torch.cuda.synchronize()  # the engines read it on their own streams
     ncs = []
     for e in engs:
         nc = ctypes.c_int64(0)
@@ -84,6 +85,7 @@ def sharded(g, mu, eps, world, partitioned=False, on_device=False):
             _lib.check(lib.gs_engine_phase_union(e.handle, p.data_ptr(), ctypes.byref(npr)))
             nps.append(npr.value)
         allp = torch.cat([p[:k] for p, k in zip(pairs, nps)]).contiguous()   # all-gather
+        torch.cuda.synchronize()
         for e in engs:
             _lib.check(lib.gs_engine_phase_merge(e.handle, allp.data_ptr() if len(allp) else None,
                                                  len(allp)))
@@ -92,6 +94,7 @@ def sharded(g, mu, eps, world, partitioned=False, on_device=False):
             _lib.check(lib.gs_engine_phase_attach(e.handle, l.data_ptr()))
         st = torch.stack(lab)
         labels = torch.cat([st[:, :n].min(0).values, st[:, n:].max(0).values]).contiguous()
+        torch.cuda.synchronize()
     else:
         for e in engs:
             _lib.check(lib.gs_engine_phase_merge(e.handle, None, 0))
