@@ -95,6 +95,7 @@ typedef struct gs_stats {
   int64_t partitions;             /* out-of-core / sharded passes */
   int64_t kernel_launches;        /* kernels launched (gs_engine_scan: load + scan) */
   int64_t peak_device_bytes;      /* high-water mark of engine allocations */
+  int64_t sim_decided_by_sketch;  /* decided dissimilar by the sketch bound (no scan) */
   double phase_ms[GS_PH_COUNT];
 } gs_stats;
 

@@ -57,6 +57,7 @@ class GsStats(ctypes.Structure):
         ("partitions", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64),
         ("peak_device_bytes", ctypes.c_int64),
+        ("sim_decided_by_sketch", ctypes.c_int64),
         ("phase_ms", ctypes.c_double * GS_PH_COUNT),
     ]
 

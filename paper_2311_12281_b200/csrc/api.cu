@@ -156,6 +156,8 @@ void gs_engine::free_graph() {
   release(g.eoff);
   release(g.elo);
   release(g.ehi);
+  release(g.sk);
+  release(g.skbase);
   g = DevGraph();
 }
 
@@ -210,6 +212,7 @@ int gs_engine_create(int device, uint64_t hbm_cap_bytes, gs_engine** out) {
     return GS_ECUDA;
   }
   cudaDeviceGetAttribute(&e->sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&e->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;  // keep freed blocks for the next call

@@ -662,6 +662,7 @@ void fill_counters(gs_stats* st, int64_t n, int64_t m, const unsigned long long*
     st->n_hub = (int64_t)h[CTR_N_HUB];
     st->n_outlier = (int64_t)h[CTR_N_OUTLIER];
     st->n_clusters = (int64_t)h[CTR_N_CLUSTERS];
+    st->sim_decided_by_sketch = (int64_t)h[CTR_SKETCH_DECIDED];
 }
 
 int read_counters(gs_engine* e, gs_stats* st) {

@@ -35,7 +35,26 @@ struct DevGraph {
   static constexpr int kClasses = 6;
   int64_t rclass[kClasses] = {0};
   bool adj_external = false;  // adj is a caller buffer (partitioned build), not ours
+  // Neighbourhood sketches (sketch.cu): vertex v of degree d >= sk_dmin owns
+  // sk_words(d) words at sk + skbase[d] + (v - rdeg[d]) * sk_words(d), a
+  // bitmap of hash(w) mod M over its neighbours w, M = pow2 >= 2^sk_lk * d.
+  uint32_t* sk = nullptr;
+  int64_t* skbase = nullptr;  // [dmax+2] first word of each degree's block
+  int sk_lk = -1;             // log2 of bits per neighbour; -1: not built
+  int64_t sk_dmin = 0;
 };
+
+// words of a degree-d sketch: M = the smallest power of two >= 2^lk * d
+// (at least four words)
+__host__ __device__ __forceinline__ int64_t sk_words(int64_t d, int lk) {
+  const int64_t x = d << lk;
+  if (x <= 128) return 4;  // >= 4 words: every sketch row is 16-byte aligned
+#ifdef __CUDA_ARCH__
+  return (1ll << (64 - __clzll(x - 1))) >> 5;
+#else
+  return (1ll << (64 - __builtin_clzll((unsigned long long)(x - 1)))) >> 5;
+#endif
+}
 
 // degree-class thresholds used to route edges to kernels (by HIGH endpoint):
 // [1,64) tiny (thread per edge), [64,512) small, [512,4096) medium,
@@ -76,6 +95,7 @@ enum Ctr {
   CTR_N_OUTLIER,
   CTR_N_CLUSTERS,
   CTR_CORES_PRE,
+  CTR_SKETCH_DECIDED,
   CTR_COUNT
 };
 
@@ -105,6 +125,12 @@ struct SimParams {
   const int32_t* nlo;   // per vertex: neighbours below hub_lo (the non-hub prefix)
   uint32_t hub_lo;      // first rank of the hub bitmap range
   uint32_t bm_words;    // hub bitmap words (range [hub_lo, n))
+  const uint32_t* sk;   // neighbourhood sketches (nullptr: none), see DevGraph
+  const int64_t* skbase;
+  int sk_lk;
+  int32_t sk_dmin;
+  float sk_gate;        // try the sketch bound iff expected false hits < gate * c_min
+  int32_t sk_minscan;   //   and the scan would need at least this many misses
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;
@@ -130,6 +156,7 @@ struct gs_engine {
   gs::DevGraph g;
   gs::DevState s;
   int sms = 148;
+  int smem_optin = 227 * 1024;  // max dynamic shared memory per block
   int64_t launches = 0;
   float last_h2d_ms = 0, last_build_ms = 0;
   int shard_rank = 0, shard_world = 1;  // multi-GPU edge ownership (b % world == rank)
@@ -182,6 +209,9 @@ int part_rows(gs_engine* e, int64_t n, int64_t slots, int part_rank, int part_wo
 int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu);
 int prepare_similarity(gs_engine* e, const Eps2& eps);  // thresholds + hub split
 int run_prepass(gs_engine* e, int32_t mu);  // O(1)-decided edges -> initial bounds
+// sketch.cu: neighbourhood sketches for the exact dissimilarity bound (needs
+// the per-scan rdeg table); lk < 0 releases them
+int build_sketch(gs_engine* e, int lk, int64_t dmin);
 // cluster.cu: the scan as phases (single GPU: all of them in a row; sharded:
 // the host layer runs the collectives between them, see dist.py)
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,

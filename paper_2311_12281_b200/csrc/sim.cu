@@ -14,6 +14,9 @@
 // stops as soon as c >= c_min or c + remaining < c_min (exact, c_min is
 // computed with the integer predicate).  Progressive pruning (Lemma 1): in
 // MODE_IDENTIFY an edge whose endpoints both have a decided role is skipped.
+#include <math.h>
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "simcore.cuh"
@@ -301,7 +304,8 @@ __global__ void k_hubsplit(const int64_t* __restrict__ off, const int32_t* __res
 template <int NT, bool GTAB>
 __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_hash(SimParams P, int64_t rlo, int64_t rhi,
                                                  uint32_t tcap, int qi, int chunk,
-                                                 uint32_t hub_lo, uint32_t bm_words) {
+                                                 uint32_t hub_lo, uint32_t bm_words,
+                                                 int64_t skw) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm = smem;  // [bm_words] + zero guard words (kept 16-byte aligned)
   // bitmap + >= 4 zero guard words, padded so the 16-byte buckets stay aligned
@@ -310,6 +314,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   int64_t* surv_oa = reinterpret_cast<int64_t*>(tab_s + (GTAB ? 0 : 4 * (size_t)tcap));
   int2* surv_ad = reinterpret_cast<int2*>(surv_oa + chunk);
   int2* surv_jc = surv_ad + chunk;
+  // sketch levels of b: S_b, then folded to 1/2, 1/4, ... (2 wb words, 16-byte aligned)
+  uint32_t* sk_lev = reinterpret_cast<uint32_t*>(surv_jc + chunk);
   __shared__ int s_item, s_nsurv, s_next, s_nstash;
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ int64_t s_nlo;
@@ -390,12 +396,18 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           __syncthreads();
           built = true;
           if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
+          if (P.sk != nullptr && db >= P.sk_dmin && 2 * sk_words(db, P.sk_lk) <= skw) {
+            const int64_t wb = sk_words(db, P.sk_lk);  // b's sketch and its folds
+            sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
+          }
         }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
         const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
         // one warp per surviving a, dynamic (scan_survivor), software-pipelined:
         // survivor s+1 is claimed and its first load issued before s is scanned
+        const int64_t wb = P.sk != nullptr ? sk_words(db, P.sk_lk) : 0;
+        const bool lev = 2 * wb <= skw && wb > 0;
         int s = 0;
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(0xffffffffu, s, 0);
@@ -408,12 +420,25 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
               s2 < ns ? first_element(P.adj + surv_oa[s2], surv_ad[s2].y, lane) : kPast;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
-          int32_t scanned;
-          const bool res = scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo, rmax,
-                                               C, nstash, nb, nlo, lane, scanned, first);
+          int32_t scanned = 0;
+          bool skd = false;
+          if (sk_try(P, ad.y, db, jc.y)) {
+            const int64_t wa = sk_words(ad.y, P.sk_lk);
+            const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
+            if (GTAB)  // huge b: long rows, folded from global with wide loads
+              skd = sk_rejects_fold4(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
+            else if (lev)
+              skd = sk_rejects_lev(A, sk_lev + 2 * (wb - wa), wa, ad.y, jc.y, lane);
+            else
+              skd = sk_rejects_fold(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
+          }
+          const bool res = !skd && scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo,
+                                                       rmax, C, nstash, nb, nlo, lane, scanned,
+                                                       first);
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
-            lc.inters++;
+            lc.inters += !skd;
+            lc.sketch += skd;
             lc.bytes += 4ull * (unsigned long long)ad.y;
             record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
@@ -444,8 +469,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
 static constexpr int kWarpBuckets = 256;  // 4 KB: deg < 512 -> <= 0.5 keys per slot
 static constexpr int kWarpWords = 4 * kWarpBuckets + kStash + 4;
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int64_t rlo,
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
                                                                int64_t rhi, int qi) {
   extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -468,6 +493,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
     const int2 th = P.thr[db];
     bool built = false;
     uint32_t bsim = 0, bdis = 0;
+    int64_t wb = 0;
     const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
     for (int64_t base = j0; base < nlow; base += 32) {
       const int64_t j = base + lane;
@@ -502,6 +528,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
         if (lane == 0) *C.nstash = 0;
         __syncwarp();
         for (int64_t i = lane; i < db; i += 32) cuckoo_insert(C, (uint32_t)nb[i]);
+        if (P.sk != nullptr && db >= P.sk_dmin) wb = sk_words(db, P.sk_lk);
         __syncwarp();
         built = true;
         if (lane == 0) lc.bytes += 4ull * (unsigned long long)db;
@@ -525,13 +552,21 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_sim_warp(SimParams P, int
         const int32_t da2 = __shfl_sync(0xffffffffu, da, src2);
         const int64_t oa2 = __shfl_sync(0xffffffffu, oa, src2);
         const uint32_t first2 = smask ? first_element(P.adj + oa2, da2, lane) : kPast;
-        int32_t scanned;
-        const bool res = scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu, 0, C,
-                                              nstash, nb, db, lane, scanned, first);
+        int32_t scanned = 0;
+        bool skd = false;
+        if (sk_try(P, sda, db, scm)) {
+          const int64_t wa = sk_words(sda, P.sk_lk);
+          // S_b (<= 128 words at k <= 8) folded from global: L1-resident
+          skd = sk_rejects_fold(sk_row(P, sa, sda, wa), sk_row(P, b, db, wb), wa, wb, sda, scm,
+                                lane);
+        }
+        const bool res = !skd && scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu,
+                                                      0, C, nstash, nb, db, lane, scanned, first);
         if (res) ++bsim; else ++bdis;
         if (lane == 0) {
           lc.probes += (unsigned long long)scanned;
-          lc.inters++;
+          lc.inters += !skd;
+          lc.sketch += skd;
           lc.bytes += 4ull * (unsigned long long)sda;
           record_edge(P, e0 + base + src, sa, (int32_t)b, res, false, lc);
         }
@@ -553,8 +588,22 @@ template <int NT, bool GTAB>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
                        uint32_t tcap, int qi, int chunk) {
   if (rhi <= rlo) return GS_OK;
-  const size_t smem =
+  size_t smem =
       (size_t)((P.bm_words + 4 + 3) & ~3u) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
+  // b's sketch levels in shared memory when they fit (else folded from global)
+  int64_t skw = 0;
+  if (P.sk != nullptr && !GTAB) {
+    int64_t dhi = 0;
+    GS_CUDA(cudaMemcpyAsync(&dhi, e->g.off + rhi, 8, cudaMemcpyDeviceToHost, e->stream));
+    int64_t dlo = 0;
+    GS_CUDA(cudaMemcpyAsync(&dlo, e->g.off + rhi - 1, 8, cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    const int64_t want = 2 * sk_words(dhi - dlo, P.sk_lk);  // the class's largest degree
+    if (smem + (size_t)want * 4 <= (size_t)e->smem_optin) {
+      skw = want;
+      smem += (size_t)want * 4;
+    }
+  }
   auto kern = k_sim_hash<NT, GTAB>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
@@ -564,7 +613,7 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   if (grid > rhi - rlo) grid = rhi - rlo;
   if (GTAB && grid > e->sms * 2) grid = e->sms * 2;
   kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk, P.hub_lo,
-                                                P.bm_words);
+                                                P.bm_words, skw);
   e->launches++;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
@@ -574,7 +623,8 @@ static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   if (rhi <= rlo) return GS_OK;
   constexpr int NT = 256;
   const size_t smem = (size_t)(NT / 32) * kWarpWords * 4;
-  auto kern = k_sim_warp<NT>;
+  static const int minb = getenv("GS_WARP_MINB") ? atoi(getenv("GS_WARP_MINB")) : 4;
+  auto kern = minb == 3 ? k_sim_warp<NT, 3> : k_sim_warp<NT, 4>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -611,6 +661,15 @@ int run_prepass(gs_engine* e, int32_t mu) {
   return GS_OK;
 }
 
+// Sketch resolution by epsilon (k bits per neighbour): the bound proves
+// dissimilarity when c_min = eps sqrt(d_a d_b) clears the false hits
+// ~ d_a d_b / M; lower eps needs finer sketches (sketch.cu).
+static constexpr int64_t kSketchDmin = 48;  // below: one scan step decides
+static int sketch_lk(const Eps2& eps) {
+  const double e = sqrt(eps.ratio);
+  return e >= 0.45 ? 2 : 3;
+}
+
 int prepare_similarity(gs_engine* e, const Eps2& eps) {
   DevGraph& g = e->g;
   DevState& s = e->s;
@@ -622,6 +681,16 @@ int prepare_similarity(gs_engine* e, const Eps2& eps) {
   k_degree_tables<<<grid_for(g.dmax + 3, 256), 256, 0, e->stream>>>(g.off, g.n, g.dmax, s.thr,
                                                                     s.rdeg, s.dxs);
   e->launches++;
+  {
+    int lk = sketch_lk(eps);
+    int64_t dmin = kSketchDmin;
+    if (const char* v = getenv("GS_SKETCH")) {  // bits per neighbour (0: off), experiments
+      const int k = atoi(v);
+      lk = k <= 0 ? -1 : 31 - __builtin_clz((unsigned)k);
+    }
+    if (const char* v = getenv("GS_SKETCH_DMIN")) dmin = std::max(1, atoi(v));
+    GS_TRY(build_sketch(e, lk, dmin));
+  }
   const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
   const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
   if (g.n > 0) {
@@ -656,6 +725,14 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.rdeg = s.rdeg;
   P.dmax = g.dmax;
   P.nlo = s.nlo;
+  P.sk = g.sk;
+  P.skbase = g.skbase;
+  P.sk_lk = g.sk_lk;
+  P.sk_dmin = (int32_t)g.sk_dmin;
+  P.sk_gate = 1.0f;
+  P.sk_minscan = 128;
+  if (const char* v = getenv("GS_SKETCH_GATE")) P.sk_gate = (float)atof(v);
+  if (const char* v = getenv("GS_SKETCH_MINSCAN")) P.sk_minscan = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
   {

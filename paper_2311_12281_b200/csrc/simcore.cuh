@@ -81,7 +81,8 @@ __device__ __forceinline__ bool edge_needed(const SimParams& P, int64_t e, int32
 }
 
 struct LocalCtr {
-  unsigned long long evals = 0, probes = 0, bound = 0, inters = 0, bytes = 0, retries = 0;
+  unsigned long long evals = 0, probes = 0, bound = 0, inters = 0, bytes = 0, retries = 0,
+                     sketch = 0;
 };
 
 // Record one decided edge.  b's bound update is returned to the caller
@@ -103,9 +104,10 @@ __device__ __forceinline__ void record_edge(const SimParams& P, int64_t e, int32
 
 __device__ __forceinline__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
   // warp reduce then one atomic per warp
-  unsigned long long v[6] = {lc.evals, lc.probes, lc.bound, lc.inters, lc.bytes, lc.retries};
+  unsigned long long v[7] = {lc.evals, lc.probes, lc.bound, lc.inters, lc.bytes, lc.retries,
+                             lc.sketch};
 #pragma unroll
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 7; ++i) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
   }
@@ -116,6 +118,7 @@ __device__ __forceinline__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
     if (v[3]) atomicAdd(&P.ctr[CTR_INTERSECTIONS], v[3]);
     if (v[4]) atomicAdd(&P.ctr[CTR_ALG_BYTES], v[4]);
     if (v[5]) atomicAdd(&P.ctr[CTR_UNION_RETRIES], v[5]);
+    if (v[6]) atomicAdd(&P.ctr[CTR_SKETCH_DECIDED], v[6]);
   }
 }
 
@@ -317,6 +320,98 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
       for (int u = 0; u < 4; ++u)
         cur[u] = (u < cu && 32 * u < rem) ? (uint32_t)__ldg(q - 32 * u) : kPast;
     }
+  }
+}
+
+// 32-bit mixer of the neighbourhood sketches (sketch.cu)
+__device__ __forceinline__ uint32_t sk_hash(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x85EBCA6Bu;
+  x ^= x >> 13;
+  x *= 0xC2B2AE35u;
+  x ^= x >> 16;
+  return x;
+}
+
+// Sketch bound (sketch.cu): U = |S_a & fold(S_b)| + d_a - |S_a| < c_min
+// proves (a, b) dissimilar.  sk_try decides (warp-uniformly) whether to
+// attempt it: the scan must have work to save (more than sk_minscan misses
+// needed to reject) and the expected false hits, d_a (1 - e^(-d_b/M_a)) +
+// d_a^2 / (2 M_a), must leave room below c_min -- otherwise U cannot decide
+// and the read is wasted.
+__device__ __forceinline__ bool sk_try(const SimParams& P, int64_t da, int64_t db, int32_t cmin) {
+  if (P.sk == nullptr || da < P.sk_dmin || da - cmin + 1 < P.sk_minscan) return false;
+  const float ma = 32.f * (float)sk_words(da, P.sk_lk), fa = (float)da;
+  const float ef = fa * (1.f - __expf(-(float)db / ma)) + fa * fa / (2.f * ma);
+  return ef < P.sk_gate * (float)cmin;
+}
+
+__device__ __forceinline__ const uint32_t* sk_row(const SimParams& P, int64_t v, int64_t d,
+                                                  int64_t w) {
+  return P.sk + P.skbase[d] + (v - P.rdeg[d]) * w;
+}
+
+// B is S_b already folded to a's wa words (a shared-memory level, sim.cu)
+__device__ __forceinline__ bool sk_rejects_lev(const uint32_t* __restrict__ A,
+                                               const uint32_t* B, int64_t wa, int64_t da,
+                                               int32_t cmin, int lane) {
+  int acc = 0;
+  for (int64_t j = lane; j < wa; j += 32) {
+    const uint32_t x = __ldg(A + j);
+    acc += __popc(x & B[j]) - __popc(x);
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  return da + acc < cmin;
+}
+
+// B is S_b in global memory (wb >= wa words), folded on the fly
+__device__ __forceinline__ bool sk_rejects_fold(const uint32_t* __restrict__ A,
+                                                const uint32_t* __restrict__ B, int64_t wa,
+                                                int64_t wb, int64_t da, int32_t cmin, int lane) {
+  int acc = 0;
+  for (int64_t j = lane; j < wa; j += 32) {
+    const uint32_t x = __ldg(A + j);
+    uint32_t y = 0;
+    for (int64_t t = j; t < wb; t += wa) y |= __ldg(B + t);
+    acc += __popc(x & y) - __popc(x);
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  return da + acc < cmin;
+}
+
+// Wide variant of sk_rejects_fold for long rows (huge b): 16-byte loads
+// (rows are 16-byte aligned, wa and wb multiples of 4 words).
+__device__ __forceinline__ bool sk_rejects_fold4(const uint32_t* __restrict__ A,
+                                                 const uint32_t* __restrict__ B, int64_t wa,
+                                                 int64_t wb, int64_t da, int32_t cmin, int lane) {
+  int acc = 0;
+  for (int64_t j = 4 * lane; j < wa; j += 128) {
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + j));
+    uint4 y = __ldg(reinterpret_cast<const uint4*>(B + j));
+    for (int64_t t = j + wa; t < wb; t += wa) {
+      const uint4 z = __ldg(reinterpret_cast<const uint4*>(B + t));
+      y.x |= z.x; y.y |= z.y; y.z |= z.z; y.w |= z.w;
+    }
+    acc += __popc(x.x & y.x) + __popc(x.y & y.y) + __popc(x.z & y.z) + __popc(x.w & y.w) -
+           __popc(x.x) - __popc(x.y) - __popc(x.z) - __popc(x.w);
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  return da + acc < cmin;
+}
+
+// Stage S_b (wb words) and its folds into `lev`: level L (wb >> L words)
+// starts at word 2 (wb - (wb >> L)), so a's level (wa words) is at
+// lev + 2 (wb - wa).  Threads [t0, t0 + nt) cooperate; sync() orders the
+// levels (__syncthreads for a CTA, __syncwarp for a warp).
+template <class Sync>
+__device__ __forceinline__ void sk_stage_levels(const uint32_t* __restrict__ Bg, int64_t wb,
+                                                uint32_t* lev, int t, int nt, Sync sync) {
+  for (int64_t i = t; i < wb; i += nt) lev[i] = __ldg(Bg + i);
+  sync();
+  for (int64_t lo = 0, w = wb; w > 4; lo += w, w >>= 1) {
+    const int64_t h = w >> 1;
+    for (int64_t i = t; i < h; i += nt) lev[lo + w + i] = lev[lo + i] | lev[lo + h + i];
+    sync();
   }
 }
 

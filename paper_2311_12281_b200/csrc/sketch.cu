@@ -1,0 +1,177 @@
+// sketch.cu -- neighbourhood sketches: an exact upper bound on |N(a) ∩ N(b)|
+// that decides most surviving edges "dissimilar" without walking N(a).
+//
+// Vertex v of degree d keeps a bitmap S_v of M(d) bits, M(d) = the smallest
+// power of two >= k*d (k = 2^lk bits per neighbour), bit h(w) mod M(d) set
+// for every neighbour w (h = a 32-bit mixer).  For an edge (a, b), d_a <= d_b
+// so M(d_a) <= M(d_b), and S_b folded to M(d_a) bits (OR of the M(d_b)/M(d_a)
+// slices; h mod M(d_a) = (h mod M(d_b)) mod M(d_a)) is the bitmap of N(b) at
+// a's resolution.  Every common neighbour sets a bit in both maps, and the
+// neighbours of a that share a bit of S_a with another neighbour of a number
+// d_a - |S_a|, so
+//
+//     c = |N(a) ∩ N(b)|  <=  |S_a & fold(S_b)| + (d_a - |S_a|)  =: U.
+//
+// U < c_min proves sigma(a, b) < eps with the same exact integer c_min the
+// scan uses (sim.cu), so the decision is exact; U >= c_min decides nothing
+// and the edge is scanned as before.  The bound pays off when the edge is
+// far from the threshold -- on R-MAT graphs almost every surviving edge has
+// few common neighbours (the s24 eps 0.5 sweep ends with no core)
+// -- and it reads k*d_a/8 bytes of a's sketch in one coalesced burst instead
+// of a dependent chain of adjacency steps.  The similar side is never decided
+// by the sketch (no lower bound), so results are unchanged bit for bit.
+#include <algorithm>
+
+#include <cub/cub.cuh>
+
+#include "simcore.cuh"
+
+namespace gs {
+
+// per degree: words of all sketches of that degree (0 below dmin)
+__global__ void k_sk_sizes(int64_t dmax, int64_t dmin, int lk, const int32_t* __restrict__ rdeg,
+                           int64_t* __restrict__ sizes) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d <= dmax + 1;
+       d += (int64_t)gridDim.x * blockDim.x)
+    sizes[d] = (d >= dmin && d <= dmax) ? (int64_t)(rdeg[d + 1] - rdeg[d]) * sk_words(d, lk) : 0;
+}
+
+// warp per vertex, sketch of <= WMAX words built in shared memory
+template <int NT, int WMAX>
+__global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
+                                                const int32_t* __restrict__ adj, int64_t r0,
+                                                int64_t r1, const int32_t* __restrict__ rdeg,
+                                                const int64_t* __restrict__ skbase, int lk,
+                                                uint32_t* __restrict__ sk) {
+  __shared__ uint32_t sm[NT / 32][WMAX];
+  const int lane = threadIdx.x & 31;
+  uint32_t* s = sm[threadIdx.x >> 5];
+  const int64_t nw = ((int64_t)gridDim.x * NT) >> 5;
+  for (int64_t v = r0 + ((blockIdx.x * (int64_t)NT + threadIdx.x) >> 5); v < r1; v += nw) {
+    const int64_t o = off[v], d = off[v + 1] - o;
+    const int64_t W = sk_words(d, lk);
+    const uint32_t mask = (uint32_t)(W * 32 - 1);
+    for (int64_t j = lane; j < W; j += 32) s[j] = 0u;
+    __syncwarp();
+    for (int64_t i = lane; i < d; i += 32) {
+      const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+      atomicOr(&s[h >> 5], 1u << (h & 31));
+    }
+    __syncwarp();
+    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
+    for (int64_t j = lane; j < W; j += 32) out[j] = s[j];
+    __syncwarp();
+  }
+}
+
+// CTA per vertex: shared memory up to smem_words, global atomics beyond
+__global__ void __launch_bounds__(512) k_sk_cta(const int64_t* __restrict__ off,
+                                                const int32_t* __restrict__ adj, int64_t r0,
+                                                int64_t r1, const int32_t* __restrict__ rdeg,
+                                                const int64_t* __restrict__ skbase, int lk,
+                                                uint32_t* __restrict__ sk, int64_t smem_words) {
+  extern __shared__ uint32_t s[];
+  for (int64_t v = r0 + blockIdx.x; v < r1; v += gridDim.x) {
+    const int64_t o = off[v], d = off[v + 1] - o;
+    const int64_t W = sk_words(d, lk);
+    const uint32_t mask = (uint32_t)(W * 32 - 1);
+    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
+    const bool in_smem = W <= smem_words;
+    uint32_t* t = in_smem ? s : out;
+    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) t[j] = 0u;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+      const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+      atomicOr(&t[h >> 5], 1u << (h & 31));
+    }
+    __syncthreads();
+    if (in_smem)
+      for (int64_t j = threadIdx.x; j < W; j += blockDim.x) out[j] = s[j];
+    __syncthreads();
+  }
+}
+
+int build_sketch(gs_engine* e, int lk, int64_t dmin) {
+  DevGraph& g = e->g;
+  DevState& s = e->s;
+  cudaStream_t st = e->stream;
+  if (lk < 0 || g.n == 0 || g.dmax < dmin) {
+    e->release(g.sk);
+    e->release(g.skbase);
+    g.sk = nullptr;
+    g.skbase = nullptr;
+    g.sk_lk = -1;
+    return GS_OK;
+  }
+  if (g.sk && g.sk_lk == lk && g.sk_dmin == dmin) return GS_OK;  // cached with the graph
+  e->release(g.sk);
+  e->release(g.skbase);
+  g.sk = nullptr;
+  g.skbase = nullptr;
+  g.sk_lk = -1;
+  int64_t* sizes = nullptr;
+  GS_TRY(e->alloc_n(&sizes, g.dmax + 2));
+  GS_TRY(e->alloc_n(&g.skbase, g.dmax + 2));
+  k_sk_sizes<<<grid_for(g.dmax + 2, 256), 256, 0, st>>>(g.dmax, dmin, lk, s.rdeg, sizes);
+  e->launches++;
+  size_t tb = 0;
+  GS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, sizes, g.skbase, g.dmax + 2, st));
+  void* tmp = nullptr;
+  GS_TRY(e->alloc(&tmp, tb > 0 ? tb : 1));
+  GS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, sizes, g.skbase, g.dmax + 2, st));
+  e->launches++;
+  e->release(tmp);
+  e->release(sizes);
+  int64_t total = 0;
+  int32_t r[3] = {0, 0, 0};
+  // rank ranges by sketch size: <= 128 words (warp per vertex), <= 2048
+  // words (8 KB CTA), larger (one big CTA per vertex)
+  const int64_t dsplit = 128 * 32 >> lk, dsplit2 = 2048 * 32 >> lk;
+  GS_CUDA(cudaMemcpyAsync(&total, g.skbase + g.dmax + 1, sizeof(total), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaMemcpyAsync(&r[0], s.rdeg + dmin, 4, cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaMemcpyAsync(&r[1], s.rdeg + std::min<int64_t>(dsplit + 1, g.dmax + 2), 4,
+                          cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaMemcpyAsync(&r[2], s.rdeg + std::min<int64_t>(dsplit2 + 1, g.dmax + 2), 4,
+                          cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  if (e->alloc_n(&g.sk, total) != GS_OK) {  // no room (HBM cap): scan without sketches
+    e->release(g.skbase);
+    g.skbase = nullptr;
+    g.sk = nullptr;
+    return GS_OK;
+  }
+  const int64_t r0 = r[0], r1 = std::max<int64_t>(r[0], r[1]), n = g.n;
+  const int64_t r2 = std::max<int64_t>(r1, r[2]);
+  if (r1 > r0) {
+    constexpr int NT = 256;
+    int64_t grid = (r1 - r0 + NT / 32 - 1) / (NT / 32);
+    grid = std::min<int64_t>(grid, (int64_t)e->sms * 8);
+    k_sk_warp<NT, 128><<<(unsigned)grid, NT, 0, st>>>(g.off, g.adj, r0, r1, s.rdeg, g.skbase, lk,
+                                                      g.sk);
+    e->launches++;
+  }
+  if (r2 > r1) {
+    const int64_t smem_words = 2048;  // 8 KB: many CTAs per SM
+    const int64_t grid = std::min<int64_t>(r2 - r1, (int64_t)e->sms * 8);
+    k_sk_cta<<<(unsigned)grid, 256, smem_words * 4, st>>>(g.off, g.adj, r1, r2, s.rdeg, g.skbase,
+                                                          lk, g.sk, smem_words);
+    e->launches++;
+  }
+  if (n > r2) {
+    const int64_t smem_words =
+        std::min<int64_t>(32768, sk_words(g.dmax, lk));  // <= 128 KB, global atomics beyond
+    auto kern = k_sk_cta;
+    GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(smem_words * 4)));
+    const int64_t grid = std::min<int64_t>(n - r2, (int64_t)e->sms * 2);
+    kern<<<(unsigned)grid, 512, smem_words * 4, st>>>(g.off, g.adj, r2, n, s.rdeg, g.skbase, lk,
+                                                      g.sk, smem_words);
+    e->launches++;
+  }
+  GS_CUDA(cudaGetLastError());
+  g.sk_lk = lk;
+  g.sk_dmin = dmin;
+  return GS_OK;
+}
+
+}  // namespace gs

@@ -69,7 +69,8 @@ def all_ok(rc: int, device, group=None) -> bool:
 def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
     """Sum the per-rank counters, max the timings (whole-job view)."""
     ints = ["sim_evals", "adj_probes", "union_retries", "probe_bound_violations",
-            "sim_decided_by_bound", "sim_intersections", "alg_bytes_sim", "kernel_launches"]
+            "sim_decided_by_bound", "sim_intersections", "alg_bytes_sim", "kernel_launches",
+            "sim_decided_by_sketch"]
     dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
     t = torch.tensor([getattr(st, k) for k in ints], dtype=torch.int64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)

@@ -240,6 +240,7 @@ def stats_from_native(st: _lib.GsStats, n: int, m: int, workers: int) -> StatsRe
         "clusters": int(st.n_clusters),
         "kernel_launches": int(st.kernel_launches),
         "peak_device_bytes": int(st.peak_device_bytes),
+        "sim_decided_by_sketch": int(st.sim_decided_by_sketch),
     }
     if st.partitions:
         rep.extra["partitions"] = int(st.partitions)

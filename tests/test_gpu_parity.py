@@ -394,3 +394,38 @@ def test_chunglu_against_oracle(orc, logn, wmax, seed):
         assert ss.extra["partitions"] >= 2
         np.testing.assert_array_equal(rr.role_codes, roles, err_msg=f"ooc {eps} {mu}")
         np.testing.assert_array_equal(rr.cluster_ids, cl, err_msg=f"ooc {eps} {mu}")
+
+
+@pytest.mark.parametrize("k", ["4", "8", "16"])
+def test_sketch_bound_forced_everywhere(orc, monkeypatch, k):
+    """The neighbourhood-sketch bound (sketch.cu) tried on EVERY survivor,
+    sketches for every degree, at each resolution: it may only ever prove
+    dissimilarity, so roles and ids stay bit-exact with the oracle (R-MAT
+    with hubs -> huge/large/medium/warp classes, and the skewed Chung-Lu)."""
+    monkeypatch.setenv("GS_SKETCH", k)
+    monkeypatch.setenv("GS_SKETCH_DMIN", "1")
+    monkeypatch.setenv("GS_SKETCH_MINSCAN", "-1000000")
+    monkeypatch.setenv("GS_SKETCH_GATE", "1e30")
+    graphs = [orc.rmat(16, seed=3), _chunglu(15, 2.1, 20000, 12 << 15, 4)]
+    for n, e in graphs:
+        c = orc.CSR(n, e)
+        g = make_graph(n, e)
+        decided = 0
+        for eps, mu in (("0.1", 3), ("0.2", 3), ("0.3", 5), ("0.5", 2), ("0.8", 2)):
+            roles, cl = orc.serial_scan(c, mu, eps)
+            r_roles, r_cl, _, s = run(g, mu, eps)
+            np.testing.assert_array_equal(r_roles, roles, err_msg=f"k{k} {eps} {mu}")
+            np.testing.assert_array_equal(r_cl, cl, err_msg=f"k{k} {eps} {mu}")
+            decided += s.extra["sim_decided_by_sketch"]
+        assert decided > 0
+
+
+def test_sketch_default_is_on_and_exact(orc):
+    n, e = orc.rmat(17, seed=5)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    roles, cl = orc.serial_scan(c, 5, "0.5")
+    r_roles, r_cl, _, s = run(g, 5, "0.5")
+    np.testing.assert_array_equal(r_roles, roles)
+    np.testing.assert_array_equal(r_cl, cl)
+    assert s.extra["sim_decided_by_sketch"] > 0
