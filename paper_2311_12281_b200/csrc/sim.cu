@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   int2* surv_jc = surv_ad + chunk;
   // sketch levels of b: S_b, then folded to 1/2, 1/4, ... (2 wb words, 16-byte aligned)
   uint32_t* sk_lev = reinterpret_cast<uint32_t*>(surv_jc + chunk);
-  __shared__ int s_item, s_nsurv, s_next, s_nstash;
+  __shared__ int s_item, s_nsurv, s_next, s_nstash, s_nkeep;
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ int64_t s_nlo;
   __shared__ uint32_t s_stash[kStash];
@@ -401,6 +401,49 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
           }
         }
+        int ns_scan = ns;
+        const bool tpass = !GTAB && P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
+                           2 * sk_words(db, P.sk_lk) <= skw;
+        if (tpass) {
+          // thread-per-survivor sketch pass; the survivors it cannot decide
+          // are compacted to the front for the warp scans
+          const int64_t wbx = sk_words(db, P.sk_lk);
+          int2 kad[2], kjc[2];
+          int64_t koa[2];
+          bool keep[2] = {false, false};
+          if (tid == 0) s_nkeep = 0;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int i = tid + r * NT;
+            if (i >= ns) continue;
+            kad[r] = surv_ad[i];
+            kjc[r] = surv_jc[i];
+            koa[r] = surv_oa[i];
+            keep[r] = true;
+            if (sk_try(P, kad[r].y, db, kjc[r].y)) {
+              const int64_t wa = sk_words(kad[r].y, P.sk_lk);
+              if (sk_thread_rejects(sk_row(P, kad[r].x, kad[r].y, wa), sk_lev + 2 * (wbx - wa),
+                                    wa, wa, kad[r].y, kjc[r].y)) {
+                keep[r] = false;
+                record_edge(P, e0 + kjc[r].x, kad[r].x, (int32_t)b, false, false, lc);
+                lc.sketch++;
+                lc.bytes += 4ull * (unsigned long long)kad[r].y;
+                atomicAdd(&s_bdis, 1u);
+              }
+            }
+          }
+          __syncthreads();
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            if (!keep[r]) continue;
+            const int k = atomicAdd(&s_nkeep, 1);
+            surv_ad[k] = kad[r];
+            surv_jc[k] = kjc[r];
+            surv_oa[k] = koa[r];
+          }
+          __syncthreads();
+          ns_scan = s_nkeep;
+        }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
         const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
@@ -411,18 +454,18 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
         int s = 0;
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(0xffffffffu, s, 0);
-        uint32_t first = s < ns ? first_element(P.adj + surv_oa[s], surv_ad[s].y, lane) : kPast;
-        while (s < ns) {
+        uint32_t first = s < ns_scan ? first_element(P.adj + surv_oa[s], surv_ad[s].y, lane) : kPast;
+        while (s < ns_scan) {
           int s2 = 0;
           if (lane == 0) s2 = atomicAdd(&s_next, 1);
           s2 = __shfl_sync(0xffffffffu, s2, 0);
           const uint32_t first2 =
-              s2 < ns ? first_element(P.adj + surv_oa[s2], surv_ad[s2].y, lane) : kPast;
+              s2 < ns_scan ? first_element(P.adj + surv_oa[s2], surv_ad[s2].y, lane) : kPast;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
           int32_t scanned = 0;
           bool skd = false;
-          if (sk_try(P, ad.y, db, jc.y)) {
+          if (!tpass && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
             if (GTAB)  // huge b: long rows, folded from global with wide loads
@@ -511,12 +554,23 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
           else {
             st = 3;
             cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
+            // thread-per-candidate sketch bound (S_b folded from global, L1-resident)
+            if (P.sk_thread && P.sk != nullptr && db >= P.sk_dmin && sk_try(P, da, db, cmin)) {
+              const int64_t wa = sk_words(da, P.sk_lk), wbb = sk_words(db, P.sk_lk);
+              if (sk_thread_rejects(sk_row(P, a, da, wa), sk_row(P, b, db, wbb), wa, wbb, da,
+                                    cmin)) {
+                st = 4;
+                record_edge(P, e0 + j, a, (int32_t)b, false, false, lc);
+                lc.sketch++;
+                lc.bytes += 4ull * (unsigned long long)da;
+              }
+            }
           }
           if (st == 1 || st == 2)  // only union / attach get here (identify: pre-pass)
             record_edge(P, e0 + j, a, (int32_t)b, st == 2, false, lc, false);
         }
       }
-      bdis += __popc(__ballot_sync(0xffffffffu, st == 1));
+      bdis += __popc(__ballot_sync(0xffffffffu, st == 1 || st == 4));
       bsim += __popc(__ballot_sync(0xffffffffu, st == 2));
       uint32_t smask = __ballot_sync(0xffffffffu, st == 3);
       if (smask && !built) {  // stage N(b) once per b, warp-private
@@ -554,7 +608,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
         const uint32_t first2 = smask ? first_element(P.adj + oa2, da2, lane) : kPast;
         int32_t scanned = 0;
         bool skd = false;
-        if (sk_try(P, sda, db, scm)) {
+        if (!P.sk_thread && sk_try(P, sda, db, scm)) {
           const int64_t wa = sk_words(sda, P.sk_lk);
           // S_b (<= 128 words at k <= 8) folded from global: L1-resident
           skd = sk_rejects_fold(sk_row(P, sa, sda, wa), sk_row(P, b, db, wb), wa, wb, sda, scm,
@@ -730,9 +784,11 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.sk_lk = g.sk_lk;
   P.sk_dmin = (int32_t)g.sk_dmin;
   P.sk_gate = 1.0f;
-  P.sk_minscan = 128;
+  P.sk_minscan = 0;
   if (const char* v = getenv("GS_SKETCH_GATE")) P.sk_gate = (float)atof(v);
   if (const char* v = getenv("GS_SKETCH_MINSCAN")) P.sk_minscan = atoi(v);
+  P.sk_thread = 1;
+  if (const char* v = getenv("GS_SKETCH_THREAD")) P.sk_thread = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
   {

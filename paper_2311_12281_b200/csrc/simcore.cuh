@@ -399,6 +399,39 @@ __device__ __forceinline__ bool sk_rejects_fold4(const uint32_t* __restrict__ A,
   return da + acc < cmin;
 }
 
+// Thread-per-survivor form of the sketch bound: one thread walks S_a in
+// 16-byte steps against b's level (B: wa words, shared or global) or S_b
+// folded on the fly (wb > wa), stopping as soon as U = d_a - sum popc(x & ~y)
+// drops below c_min (U only decreases).  Used where many survivors are
+// checked at once, so hundreds of rows are in flight per SM instead of one
+// per warp.
+__device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A,
+                                                  const uint32_t* B, int64_t wa, int64_t wb,
+                                                  int64_t da, int32_t cmin) {
+  const uint4* __restrict__ a4 = reinterpret_cast<const uint4*>(A);
+  const uint4* b4 = reinterpret_cast<const uint4*>(B);
+  const int64_t q = wa >> 2, qb = wb >> 2;
+  int64_t u = da;
+  for (int64_t j = 0; j < q; j += 2) {
+    uint4 x[2], y[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      x[t] = j + t < q ? __ldg(a4 + j + t) : make_uint4(0u, 0u, 0u, 0u);
+      y[t] = j + t < q ? b4[j + t] : make_uint4(0u, 0u, 0u, 0u);
+      for (int64_t f = j + t + q; f < qb; f += q) {  // fold (global S_b only)
+        const uint4 z = __ldg(b4 + f);
+        y[t].x |= z.x; y[t].y |= z.y; y[t].z |= z.z; y[t].w |= z.w;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      u -= __popc(x[t].x & ~y[t].x) + __popc(x[t].y & ~y[t].y) + __popc(x[t].z & ~y[t].z) +
+           __popc(x[t].w & ~y[t].w);
+    if (u < cmin) return true;
+  }
+  return false;
+}
+
 // Stage S_b (wb words) and its folds into `lev`: level L (wb >> L words)
 // starts at word 2 (wb - (wb >> L)), so a's level (wa words) is at
 // lev + 2 (wb - wa).  Threads [t0, t0 + nt) cooperate; sync() orders the
