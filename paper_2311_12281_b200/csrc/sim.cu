@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int32_t* __restrict__ nb = P.adj + ob;
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
-    bool built = false;
+    bool built = false, sk_staged = false;
     const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
     for (int64_t base = j0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
@@ -371,39 +371,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       __syncthreads();
       const int ns = s_nsurv;
       if (ns > 0) {
-        if (!built) {  // stage N(b) once per b: hub suffix -> bitmap, rest -> cuckoo
-          if (tid == 0) {
-            s_nlo = P.nlo[b];
-            s_nstash = 0;
-          }
-          __syncthreads();
-          const int64_t nlo = s_nlo;
-          uint32_t T = (uint32_t)((nlo * 5) / 12 + 1);  // <= 0.6 keys per slot
-          if (T > tcap) T = tcap;
-          C.T = T;
-          for (uint32_t i = tid; i < T; i += NT)
-              reinterpret_cast<uint4*>(C.tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-          __syncthreads();
-          for (int64_t i = tid; i < db; i += NT) {
-            const uint32_t w = (uint32_t)nb[i];
-            if (i >= nlo) {
-              const uint32_t r = w - hub_lo;
-              atomicOr(&bm[r >> 5], 1u << (r & 31));
-            } else {
-              cuckoo_insert(C, w);
-            }
-          }
-          __syncthreads();
-          built = true;
-          if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
-          if (P.sk != nullptr && db >= P.sk_dmin && 2 * sk_words(db, P.sk_lk) <= skw) {
-            const int64_t wb = sk_words(db, P.sk_lk);  // b's sketch and its folds
-            sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
-          }
-        }
         int ns_scan = ns;
         const bool tpass = !GTAB && P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
                            2 * sk_words(db, P.sk_lk) <= skw;
+        if (!GTAB && !sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
+            2 * sk_words(db, P.sk_lk) <= skw) {  // b's sketch and its folds, once per b
+          const int64_t wb = sk_words(db, P.sk_lk);
+          sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
+          sk_staged = true;
+        }
         if (tpass) {
           // thread-per-survivor sketch pass; the survivors it cannot decide
           // are compacted to the front for the warp scans
@@ -444,13 +420,39 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           __syncthreads();
           ns_scan = s_nkeep;
         }
+        if (ns_scan > 0 && !built) {  // stage N(b) once per b: hub suffix -> bitmap, rest -> cuckoo
+          if (tid == 0) {
+            s_nlo = P.nlo[b];
+            s_nstash = 0;
+          }
+          __syncthreads();
+          const int64_t nlo = s_nlo;
+          uint32_t T = (uint32_t)((nlo * 5) / 12 + 1);  // <= 0.6 keys per slot
+          if (T > tcap) T = tcap;
+          C.T = T;
+          for (uint32_t i = tid; i < T; i += NT)
+              reinterpret_cast<uint4*>(C.tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+          __syncthreads();
+          for (int64_t i = tid; i < db; i += NT) {
+            const uint32_t w = (uint32_t)nb[i];
+            if (i >= nlo) {
+              const uint32_t r = w - hub_lo;
+              atomicOr(&bm[r >> 5], 1u << (r & 31));
+            } else {
+              cuckoo_insert(C, w);
+            }
+          }
+          __syncthreads();
+          built = true;
+          if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
+        }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
         const uint32_t rmax = bm_words * 32u;  // first bit of the zero guard word
         // one warp per surviving a, dynamic (scan_survivor), software-pipelined:
         // survivor s+1 is claimed and its first load issued before s is scanned
         const int64_t wb = P.sk != nullptr ? sk_words(db, P.sk_lk) : 0;
-        const bool lev = 2 * wb <= skw && wb > 0;
+        const bool lev = 2 * wb <= skw && wb > 0 && sk_staged;
         int s = 0;
         if (lane == 0) s = atomicAdd(&s_next, 1);
         s = __shfl_sync(0xffffffffu, s, 0);
