@@ -45,6 +45,49 @@ __device__ __forceinline__ int64_t survivor_start(const SimParams& P, const int3
   return lower_bound_run(nb, 0, nlow, rdeg_at(P.rdeg, dmax, dstart));
 }
 
+// The same search done by a whole CTA (NT threads, nlow <= NT^2 per round
+// pair): NT sampled positions per round, __syncthreads_count brackets the
+// answer, so two rounds of parallel loads replace ~log2(nlow) dependent ones.
+template <int NT>
+__device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const int32_t* nb,
+                                                      int64_t nlow, int2 th, int64_t dmax) {
+  if (P.mode > MODE_CLEANUP || nlow == 0) return 0;
+  const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
+  const int64_t key = rdeg_at(P.rdeg, dmax, dstart);
+  int64_t lo = 0, hi = nlow;  // answer in [lo, hi]: first index with nb[idx] >= key
+  while (hi > lo) {
+    const int64_t step = (hi - lo + NT - 1) / NT;
+    const int64_t idx = lo + (int64_t)threadIdx.x * step;  // probes lo, lo+step, ...
+    const int cnt = __syncthreads_count(idx < hi && (int64_t)nb[idx] < key);
+    // nb[lo + (cnt-1) step] < key <= nb[lo + cnt step] (if in range)
+    const int64_t nlo = cnt == 0 ? lo : lo + (int64_t)(cnt - 1) * step + 1;
+    const int64_t nhi = min(hi, lo + (int64_t)cnt * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
+// ... and by one warp
+__device__ __forceinline__ int64_t survivor_start_warp(const SimParams& P, const int32_t* nb,
+                                                       int64_t nlow, int2 th, int64_t dmax,
+                                                       int lane) {
+  if (P.mode > MODE_CLEANUP || nlow == 0) return 0;
+  const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
+  const int64_t key = rdeg_at(P.rdeg, dmax, dstart);
+  int64_t lo = 0, hi = nlow;
+  while (hi > lo) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t idx = lo + (int64_t)lane * step;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, idx < hi && (int64_t)nb[idx] < key));
+    const int64_t nlo = cnt == 0 ? lo : lo + (int64_t)(cnt - 1) * step + 1;
+    const int64_t nhi = min(hi, lo + (int64_t)cnt * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
 // ---------------------------------------------------------------------------
 // tiny b: one thread per high endpoint b (deg < 64), its owned edges in
 // order, merging two short runs.  Walking b's edges sequentially lets each
@@ -343,7 +386,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
     bool built = false, sk_staged = false;
-    const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
+    const int64_t j0 = survivor_start_cta<NT>(P, nb, nlow, th, P.dmax);
     for (int64_t base = j0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
       __syncthreads();
@@ -396,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             kjc[r] = surv_jc[i];
             koa[r] = surv_oa[i];
             keep[r] = true;
-            if (sk_try(P, kad[r].y, db, kjc[r].y)) {
+            if (sk_words(kad[r].y, P.sk_lk) <= P.sk_tmax && sk_try(P, kad[r].y, db, kjc[r].y)) {
               const int64_t wa = sk_words(kad[r].y, P.sk_lk);
               if (sk_thread_rejects(sk_row(P, kad[r].x, kad[r].y, wa), sk_lev + 2 * (wbx - wa),
                                     wa, wa, kad[r].y, kjc[r].y)) {
@@ -467,7 +510,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           const int2 ad = surv_ad[s];
           int32_t scanned = 0;
           bool skd = false;
-          if (!tpass && sk_try(P, ad.y, db, jc.y)) {
+          // long rows are left to the warp (thread-pass imbalance)
+          if ((!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
             if (GTAB)  // huge b: long rows, folded from global with wide loads
@@ -539,7 +583,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     bool built = false;
     uint32_t bsim = 0, bdis = 0;
     int64_t wb = 0;
-    const int64_t j0 = survivor_start(P, nb, nlow, th, P.dmax);
+    const int64_t j0 = survivor_start_warp(P, nb, nlow, th, P.dmax, lane);
     for (int64_t base = j0; base < nlow; base += 32) {
       const int64_t j = base + lane;
       int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
@@ -791,6 +835,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   if (const char* v = getenv("GS_SKETCH_MINSCAN")) P.sk_minscan = atoi(v);
   P.sk_thread = 1;
   if (const char* v = getenv("GS_SKETCH_THREAD")) P.sk_thread = atoi(v);
+  P.sk_tmax = 1 << 30;
+  if (const char* v = getenv("GS_SKETCH_TMAX")) P.sk_tmax = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
   {
