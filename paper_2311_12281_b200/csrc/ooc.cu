@@ -18,6 +18,9 @@
 //     device footprint is independent of m.
 //   * Every device allocation is counted against the HBM cap (engine
 //     allocator); GS_EBUDGET if the resident state alone cannot fit.
+#include <math.h>
+#include <stdlib.h>
+
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -107,10 +110,18 @@ struct OocParams {
   int32_t* wq;
   uint32_t* gtab;
   int64_t gtab_stride;
+  // neighbourhood sketches (sketch.cu) of every vertex, in mapped pinned host
+  // memory: vertex v's row starts at 16-byte unit hsk_off[v] (nullptr: none)
+  const uint32_t* hsk;
+  const uint32_t* hsk_off;
+  int sk_lk;
+  int32_t sk_dmin;
+  float sk_gate;
 };
 
 static constexpr int64_t kOocWarpMax = 512;      // deg(b) <= this: warp per b
-static constexpr int64_t kOocSmemBuckets = 12288;  // 192 KB cuckoo, deg(b) <= 29491
+static constexpr int kOocWarpSk = 256;           // words of b's sketch levels per warp
+static constexpr int64_t kOocSmemBuckets = 10240;  // 160 KB cuckoo, deg(b) <= 24576
 
 __device__ __forceinline__ bool ooc_owns(uint32_t da, int32_t a, uint32_t db, int32_t b) {
   return da < db || (da == db && a < b);  // graph.py:226
@@ -125,6 +136,40 @@ __device__ __forceinline__ bool ooc_needed(const OocParams& P, int32_t a, int32_
     return uf_find(P.parent, a) != uf_find(P.parent, b);
   }
   return (ra == ROLE_CORE) != (rb == ROLE_CORE);  // attach
+}
+
+// Should (a, b) try the sketch bound (as sk_try, sim.cu)?
+__device__ __forceinline__ bool ooc_sk_try(const OocParams& P, int64_t da, int64_t db,
+                                           int32_t cmin) {
+  if (P.hsk == nullptr || da < P.sk_dmin) return false;
+  const float ma = 32.f * (float)sk_words(da, P.sk_lk), fa = (float)da;
+  const float ef = fa * (1.f - __expf(-(float)db / ma)) + fa * fa / (2.f * ma);
+  return ef < P.sk_gate * (float)cmin;
+}
+
+__device__ __forceinline__ const uint32_t* ooc_sk_row(const OocParams& P, int64_t v) {
+  return P.hsk + 4 * (int64_t)P.hsk_off[v];  // zero-copy
+}
+
+// S_b and its folds (the layout of sk_stage_levels) hashed straight from the
+// streamed slice N(b) -- the same bits as b's stored sketch, no host read
+template <class Sync>
+__device__ __forceinline__ void ooc_sk_levels(const int32_t* __restrict__ nb, int64_t db, int lk,
+                                              uint32_t* lev, int t, int nt, Sync sync) {
+  const int64_t wb = sk_words(db, lk);
+  const uint32_t mask = (uint32_t)(wb * 32 - 1);
+  for (int64_t i = t; i < wb; i += nt) lev[i] = 0u;
+  sync();
+  for (int64_t i = t; i < db; i += nt) {
+    const uint32_t h = sk_hash((uint32_t)nb[i]) & mask;
+    atomicOr(&lev[h >> 5], 1u << (h & 31));
+  }
+  sync();
+  for (int64_t lo = 0, w = wb; w > 4; lo += w, w >>= 1) {
+    const int64_t h = w >> 1;
+    for (int64_t i = t; i < h; i += nt) lev[lo + w + i] = lev[lo + i] | lev[lo + h + i];
+    sync();
+  }
 }
 
 // record one decided edge; b's identify bounds are aggregated by the caller
@@ -155,9 +200,10 @@ template <int NT>
 __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   constexpr int kWB = 256;
-  constexpr int kWW = 4 * kWB + kStash + 4;
+  constexpr int kWW = 4 * kWB + kStash + 4 + kOocWarpSk;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* tab = smem + (size_t)wid * kWW;
+  uint32_t* lev = tab + 4 * kWB + kStash + 4;  // b's sketch levels (16-byte aligned)
   Cuckoo C;
   C.tab = tab;
   C.stash = tab + 4 * kWB;
@@ -173,13 +219,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
     if (db == 0 || db > kOocWarpMax) continue;
     const int32_t* __restrict__ nb = P.padj + (P.poff[b - P.lo] - P.base);
     const int2 th = P.thr[db];
-    bool built = false;
+    bool built = false, skb = false;
     uint32_t bsim = 0, bdis = 0;
+    const bool bsk = P.hsk != nullptr && 2 * sk_words(db, P.sk_lk) <= kOocWarpSk;
     for (uint32_t base = 0; base < db; base += 32) {
       const uint32_t j = base + lane;
-      int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
+      int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor, 4 sketch
       int32_t a = 0, cmin = 0;
       uint32_t da = 0;
+      bool want = false;
       if (j < db) {
         a = nb[j];
         da = P.deg[a];
@@ -189,12 +237,19 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
           else {
             st = 3;
             cmin = (int32_t)c_min_exact(da, db, (int64_t)da - 1, P.eps);
+            want = bsk && ooc_sk_try(P, da, db, cmin);
           }
           if (st == 1 || st == 2) {
             lc.bound++;
             ooc_record(P, a, (int32_t)b, st == 2, lc);
           }
         }
+      }
+      uint32_t sku = 0;  // the candidate's sketch row (16-byte units), read here in parallel
+      if (want) sku = P.hsk_off[a];
+      if (__any_sync(0xffffffffu, want) && !skb) {
+        ooc_sk_levels(nb, db, P.sk_lk, lev, lane, 32, [] { __syncwarp(); });
+        skb = true;
       }
       bdis += __popc(__ballot_sync(0xffffffffu, st == 1));
       bsim += __popc(__ballot_sync(0xffffffffu, st == 2));
@@ -218,6 +273,18 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
         const int32_t sa = __shfl_sync(0xffffffffu, a, src);
         const int32_t sda = (int32_t)__shfl_sync(0xffffffffu, da, src);
         const int32_t scm = __shfl_sync(0xffffffffu, cmin, src);
+        if (__shfl_sync(0xffffffffu, want, src)) {  // sketch bound: the warp reads a's row
+          const uint32_t u = __shfl_sync(0xffffffffu, sku, src);
+          const int64_t wa = sk_words(sda, P.sk_lk), wb = sk_words(db, P.sk_lk);
+          if (sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, sda, scm, lane)) {
+            if (P.mode == OOC_IDENTIFY) ++bdis;
+            if (lane == 0) {
+              lc.sketch++;
+              ooc_record(P, sa, (int32_t)b, false, lc);
+            }
+            continue;
+          }
+        }
         int64_t oa = 0;
         if (lane == 0) oa = P.hoff[sa];  // zero-copy: where N(a) starts in host memory
         oa = __shfl_sync(0xffffffffu, oa, 0);
@@ -243,12 +310,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
 // big b: one CTA per b (listed in P.big), cuckoo of N(b) in shared memory or,
 // for the largest lists, in an HBM slab per CTA
 template <int NT, bool GTAB>
-__global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, int chunk) {
+__global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, int chunk,
+                                                  int64_t skw) {
   extern __shared__ __align__(16) uint32_t smem[];
   int64_t* surv_oa = reinterpret_cast<int64_t*>(smem + (GTAB ? 0 : 4 * (size_t)tcap));
   int2* surv_ad = reinterpret_cast<int2*>(surv_oa + chunk);
   int2* surv_jc = surv_ad + chunk;
-  __shared__ int s_item, s_nsurv, s_next, s_nstash;
+  uint32_t* surv_sk = reinterpret_cast<uint32_t*>(surv_jc + chunk);  // sketch row or ~0
+  uint32_t* lev = surv_sk + chunk;  // b's sketch levels [skw] (16-byte aligned: chunk % 4 == 0)
+  __shared__ int s_item, s_nsurv, s_next, s_nstash, s_nkeep;
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ uint32_t s_stash[kStash];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -270,7 +340,8 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
     uint32_t T = (uint32_t)(((int64_t)db * 5) / 12 + 1);
     if (T > tcap) T = tcap;
     C.T = T;
-    bool built = false;
+    bool built = false, skb = false;
+    const bool bsk = P.hsk != nullptr && 2 * sk_words(db, P.sk_lk) <= skw;
     for (uint32_t base = 0; base < db; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
       __syncthreads();
@@ -289,14 +360,21 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
           atomicAdd(&s_bsim, 1u);
         } else {
           const int slot = atomicAdd(&s_nsurv, 1);
+          const int32_t cm = (int32_t)c_min_exact(da, db, (int64_t)da - 1, P.eps);
           surv_oa[slot] = P.hoff[a];  // zero-copy
           surv_ad[slot] = make_int2(a, (int32_t)da);
-          surv_jc[slot] = make_int2((int32_t)j, (int32_t)c_min_exact(da, db, (int64_t)da - 1, P.eps));
+          surv_jc[slot] = make_int2((int32_t)j, cm);
+          surv_sk[slot] = bsk && ooc_sk_try(P, da, db, cm) ? P.hsk_off[a] : 0xFFFFFFFFu;
         }
       }
       __syncthreads();
       const int ns = s_nsurv;
-      if (ns > 0) {
+      int ns_scan = ns;
+      if (ns > 0 && bsk && !skb) {  // b's sketch levels, hashed from the slice
+        ooc_sk_levels(nb, db, P.sk_lk, lev, tid, NT, [] { __syncthreads(); });
+        skb = true;
+      }
+      if (ns_scan > 0) {
         if (!built) {
           for (uint32_t i = tid; i < T; i += NT)
             reinterpret_cast<uint4*>(C.tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
@@ -311,9 +389,22 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
           int s = 0;
           if (lane == 0) s = atomicAdd(&s_next, 1);
           s = __shfl_sync(0xffffffffu, s, 0);
-          if (s >= ns) break;
+          if (s >= ns_scan) break;
           const int2 jc = surv_jc[s];
           const int2 ad = surv_ad[s];
+          const uint32_t u = surv_sk[s];
+          if (u != 0xFFFFFFFFu) {  // sketch bound: the warp reads a's row
+            const int64_t wa = sk_words(ad.y, P.sk_lk), wb = sk_words(db, P.sk_lk);
+            if (sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, ad.y, jc.y,
+                                lane)) {
+              if (lane == 0) {
+                lc.sketch++;
+                ooc_record(P, ad.x, b, false, lc);
+                atomicAdd(&s_bdis, 1u);
+              }
+              continue;
+            }
+          }
           int32_t scanned;
           const bool res = scan_survivor<GTAB>(P.hadj + surv_oa[s], ad.y, jc.y, nullptr,
                                                0xffffffffu, 0, C, nstash, nb, db, lane, scanned,
@@ -333,6 +424,37 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
     }
   }
   ooc_flush(P, lc);
+}
+
+// Sketches of the partition's vertices (sketch.cu layout per vertex) into
+// skbuf (16-byte unit u0 = hsk_off[lo]); the host copies them out.
+__global__ void __launch_bounds__(256) k_ooc_sk_build(OocParams P, uint32_t* __restrict__ skbuf,
+                                                      uint32_t u0) {
+  __shared__ uint32_t sm[8][128];
+  const int lane = threadIdx.x & 31;
+  uint32_t* s = sm[threadIdx.x >> 5];
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = P.lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); v < P.hi;
+       v += nw) {
+    const int64_t d = P.deg[v];
+    if (d < P.sk_dmin) continue;
+    const int64_t W = sk_words(d, P.sk_lk);
+    const uint32_t mask = (uint32_t)(W * 32 - 1);
+    const int32_t* __restrict__ nb = P.padj + (P.poff[v - P.lo] - P.base);
+    uint32_t* out = skbuf + 4 * (int64_t)(P.hsk_off[v] - u0);
+    uint32_t* t = W <= 128 ? s : out;  // long rows: global atomics (zeroed by the host)
+    if (W <= 128)
+      for (int64_t j = lane; j < W; j += 32) s[j] = 0u;
+    __syncwarp();
+    for (int64_t i = lane; i < d; i += 32) {
+      const uint32_t h = sk_hash((uint32_t)nb[i]) & mask;
+      atomicOr(&t[h >> 5], 1u << (h & 31));
+    }
+    __syncwarp();
+    if (W <= 128)
+      for (int64_t j = lane; j < W; j += 32) out[j] = s[j];
+    __syncwarp();
+  }
 }
 
 // list the partition's b with deg > kOocWarpMax, split at the smem capacity
@@ -559,6 +681,15 @@ static void unmap_host(Mapped& m) {
   m = Mapped();
 }
 
+static void* mapped_ptr(void* host) {
+  void* dev = nullptr;
+  if (cudaHostGetDevicePointer(&dev, host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return host;  // UVA: the host pointer is valid on the device
+  }
+  return dev;
+}
+
 struct Partition {
   int64_t lo, hi, a0, a1;  // b range and adjacency slice [a0, a1)
 };
@@ -607,6 +738,9 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   cudaEventCreate(&t3); cudaEventCreate(&t4);
   int result = GS_OK;
   int64_t launches = 0;
+  uint32_t* hsk = nullptr;      // pinned host sketch rows
+  uint32_t* hsk_off = nullptr;  // pinned host row offsets (16-byte units)
+  uint32_t* skbuf = nullptr;    // device scratch: one partition's rows
   do {
     uint32_t* deg = nullptr;
     uint8_t* role = nullptr;
@@ -635,8 +769,17 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     const int64_t tcap_g = (int64_t)dmax > smem_max ? ((int64_t)dmax * 5) / 12 + 1 : 0;
     size_t fixed = e->live + (size_t)nslab * 16 * (size_t)tcap_g + (2u << 20);
     size_t avail = e->cap ? (e->cap > fixed ? e->cap - fixed : 0) : ((size_t)1 << 30);
+    // sketch resolution as in sim.cu (k = 2^sk_lk bits per neighbour; -1: off)
+    int sk_lk = sqrt(eps.ratio) >= 0.45 ? 2 : 3;
+    int64_t sk_dmin = 48;
+    if (const char* v = getenv("GS_SKETCH")) {
+      const int k = atoi(v);
+      sk_lk = k <= 0 ? -1 : 31 - __builtin_clz((unsigned)k);
+    }
+    if (const char* v = getenv("GS_SKETCH_DMIN")) sk_dmin = std::max(1, atoi(v));
     // two buffers of adjacency (4 B/elem) + offsets (8 B/vertex) + big lists
-    int64_t buf_elems = (int64_t)(avail / 2 / 4 * 3 / 4);
+    // (+ with sketches, one partition's rows: <= k/4 bytes per element)
+    int64_t buf_elems = (int64_t)(avail / 2 / 4 * (sk_lk >= 0 ? 1 : 3) / (sk_lk >= 0 ? 2 : 4));
     buf_elems = std::min<int64_t>(buf_elems, (int64_t)1 << 28);
     if (buf_elems < (int64_t)dmax || buf_elems < 1024) {
       char buf[200];
@@ -663,6 +806,37 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     }
     int64_t vmax = 0;
     for (auto& p : parts) vmax = std::max(vmax, p.hi - p.lo);
+    // ---- neighbourhood sketches (sketch.cu) in mapped pinned host memory:
+    // per-vertex row offsets (16-byte units) are laid out here, the rows are
+    // hashed on the device from the streamed slices in a pre-pass below
+    int64_t skbuf_units = 0;
+    if (sk_lk >= 0) {
+      if (cudaHostAlloc(&hsk_off, 4 * (size_t)(n + 1), cudaHostAllocMapped) != cudaSuccess) {
+        cudaGetLastError();
+        hsk_off = nullptr;
+      }
+      uint64_t acc = 0;
+      for (int64_t v = 0; hsk_off && v < n; ++v) {
+        hsk_off[v] = (uint32_t)acc;
+        const int64_t d = off[v + 1] - off[v];
+        if (d >= sk_dmin) acc += (uint64_t)sk_words(d, sk_lk) / 4;
+        if (acc >= 0xFFFFFFFFull) break;
+      }
+      if (hsk_off && acc < 0xFFFFFFFFull) {
+        hsk_off[n] = (uint32_t)acc;
+        for (auto& p : parts)
+          skbuf_units = std::max<int64_t>(skbuf_units, (int64_t)hsk_off[p.hi] - hsk_off[p.lo]);
+        if (cudaHostAlloc(&hsk, 16 * (size_t)std::max<uint64_t>(acc, 1), cudaHostAllocMapped) !=
+            cudaSuccess) {
+          cudaGetLastError();
+          hsk = nullptr;
+        }
+      }
+      if (!hsk) {  // no room on the host: scan without sketches
+        if (hsk_off) cudaFreeHost(hsk_off);
+        hsk_off = nullptr;
+      }
+    }
     int32_t* pbuf[2] = {nullptr, nullptr};
     int64_t* obuf[2] = {nullptr, nullptr};
     int32_t *bigmid = nullptr, *bighuge = nullptr;
@@ -677,6 +851,13 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     if ((result = e->alloc_n(&bighuge, buf_elems / kOocWarpMax + 1)) != GS_OK) break;
     if ((result = e->alloc_n(&bigcnt, 2)) != GS_OK) break;
     if (tcap_g > 0 && (result = e->alloc_n(&gtab, 4 * tcap_g * nslab)) != GS_OK) break;
+    if (hsk && e->alloc_n(&skbuf, 4 * std::max<int64_t>(skbuf_units, 1)) != GS_OK) {
+      cudaFreeHost(hsk);  // the partition scratch does not fit the cap: no sketches
+      cudaFreeHost(hsk_off);
+      hsk = nullptr;
+      hsk_off = nullptr;
+      skbuf = nullptr;
+    }
 
     OocParams P;
     memset(&P, 0, sizeof(P));
@@ -692,12 +873,42 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     P.wq = wq;
     P.gtab = gtab;
     P.gtab_stride = 4 * tcap_g;
-    const size_t smem_warp = 8 * (4 * 256 + kStash + 4) * 4;
-    const size_t smem_cta = (size_t)kOocSmemBuckets * 16 + 1024 * 24;
-    const size_t smem_gta = 1024 * 24;
-    cudaFuncSetAttribute(k_ooc_warp<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_warp);
-    cudaFuncSetAttribute(k_ooc_cta<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cta);
-    cudaFuncSetAttribute(k_ooc_cta<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gta);
+    if (hsk) {
+      P.hsk = static_cast<const uint32_t*>(mapped_ptr(hsk));
+      P.hsk_off = static_cast<const uint32_t*>(mapped_ptr(hsk_off));
+      P.sk_lk = sk_lk;
+      P.sk_dmin = (int32_t)sk_dmin;
+      P.sk_gate = 1.0f;
+      if (const char* v = getenv("GS_SKETCH_GATE")) P.sk_gate = (float)atof(v);
+    }
+    const size_t smem_warp = 8 * (4 * 256 + kStash + 4 + kOocWarpSk) * 4;
+    const size_t smem_base = (size_t)kOocSmemBuckets * 16 + 1024 * 28;
+    const int64_t smem_opt = e->smem_optin - 1024;  // static shared memory
+    // b's sketch levels in shared memory, as many words as fit (else no sketch for that b)
+    const int64_t skw_cta =
+        hsk ? std::min<int64_t>(2 * sk_words(smem_max, sk_lk), (smem_opt - (int64_t)smem_base) / 4) : 0;
+    const int64_t skw_gta =
+        hsk ? std::min<int64_t>(2 * sk_words((int64_t)dmax, sk_lk), (smem_opt - 1024 * 28) / 4) : 0;
+    const size_t smem_cta = smem_base + 4 * (size_t)std::max<int64_t>(skw_cta, 0);
+    const size_t smem_gta = 1024 * 28 + 4 * (size_t)std::max<int64_t>(skw_gta, 0);
+    {
+      const cudaError_t e1 = cudaFuncSetAttribute(
+          k_ooc_warp<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_warp);
+      const cudaError_t e2 = cudaFuncSetAttribute(
+          k_ooc_cta<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cta);
+      const cudaError_t e3 = cudaFuncSetAttribute(
+          k_ooc_cta<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_gta);
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+        char buf[256];
+        snprintf(buf, sizeof(buf), "shared memory configuration failed (%zu/%zu/%zu bytes: %s)",
+                 smem_warp, smem_cta, smem_gta,
+                 cudaGetErrorString(e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3));
+        cudaGetLastError();
+        set_error(buf);
+        result = GS_ECUDA;
+        break;
+      }
+    }
     int occ_w = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, k_ooc_warp<256>, 256, smem_warp);
     if (occ_w < 1) occ_w = 1;
@@ -746,7 +957,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         Q.big = bigmid;
         Q.nbig = h_cnt[0];
         k_ooc_cta<1024, false><<<(unsigned)std::min<int>(h_cnt[0], e->sms), 1024, smem_cta, cs>>>(
-            Q, (uint32_t)kOocSmemBuckets, 1024);
+            Q, (uint32_t)kOocSmemBuckets, 1024, skw_cta);
         ++launches;
       }
       if (h_cnt[1] > 0) {
@@ -755,12 +966,29 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         Q.big = bighuge;
         Q.nbig = h_cnt[1];
         k_ooc_cta<1024, true><<<(unsigned)std::min<int>(h_cnt[1], nslab), 1024, smem_gta, cs>>>(
-            Q, (uint32_t)tcap_g, 1024);
+            Q, (uint32_t)tcap_g, 1024, skw_gta);
         ++launches;
       }
       GS_CUDA(cudaGetLastError());
       return GS_OK;
     };
+    // ---- sketch pre-pass: every vertex's row hashed from its streamed slice
+    if (hsk) {
+      auto sk_body = [&](const Partition& pt) -> int {
+        const uint32_t u0 = hsk_off[pt.lo], u1 = hsk_off[pt.hi];
+        if (u1 == u0) return GS_OK;
+        GS_CUDA(cudaMemsetAsync(skbuf, 0, 16 * (size_t)(u1 - u0), cs));
+        const int64_t nw = (pt.hi - pt.lo + 7) / 8;
+        k_ooc_sk_build<<<(unsigned)std::min<int64_t>(nw, (int64_t)e->sms * 8), 256, 0, cs>>>(
+            P, skbuf, u0);
+        ++launches;
+        GS_CUDA(cudaMemcpyAsync(hsk + 4 * (size_t)u0, skbuf, 16 * (size_t)(u1 - u0),
+                                cudaMemcpyDeviceToHost, cs));
+        GS_CUDA(cudaGetLastError());
+        return GS_OK;
+      };
+      if ((result = sweep(sk_body)) != GS_OK) break;
+    }
     // ---- pass 1: identify (Alg. 5 first loop)
     P.mode = OOC_IDENTIFY;
     if ((result = sweep(sim_body)) != GS_OK) break;
@@ -825,6 +1053,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       st->union_retries = (int64_t)hc[CTR_UNION_RETRIES];
       st->sim_decided_by_bound = (int64_t)hc[CTR_BOUND_DECIDED];
       st->sim_intersections = (int64_t)hc[CTR_INTERSECTIONS];
+      st->sim_decided_by_sketch = (int64_t)hc[CTR_SKETCH_DECIDED];
       st->n_clusters = (int64_t)hc[CTR_N_CLUSTERS];
       st->n_core = (int64_t)ncores;
       st->partitions = (int64_t)parts.size();
@@ -850,6 +1079,8 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   }
   cudaEventDestroy(t0); cudaEventDestroy(t1); cudaEventDestroy(t2);
   cudaEventDestroy(t3); cudaEventDestroy(t4);
+  if (hsk) cudaFreeHost(hsk);
+  if (hsk_off) cudaFreeHost(hsk_off);
   cleanup();
   return result;
 }

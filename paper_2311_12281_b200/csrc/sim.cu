@@ -699,7 +699,7 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
     GS_CUDA(cudaMemcpyAsync(&dlo, e->g.off + rhi - 1, 8, cudaMemcpyDeviceToHost, e->stream));
     GS_CUDA(cudaStreamSynchronize(e->stream));
     const int64_t want = 2 * sk_words(dhi - dlo, P.sk_lk);  // the class's largest degree
-    if (smem + (size_t)want * 4 <= (size_t)e->smem_optin) {
+    if (smem + (size_t)want * 4 + 1024 <= (size_t)e->smem_optin) {  // + static shared memory
       skw = want;
       smem += (size_t)want * 4;
     }

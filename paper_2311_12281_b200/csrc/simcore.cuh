@@ -399,6 +399,29 @@ __device__ __forceinline__ bool sk_rejects_fold4(const uint32_t* __restrict__ A,
   return da + acc < cmin;
 }
 
+// Warp form over a shared-memory level with 16-byte loads (lane l: words
+// 4l..4l+3 of each 128-word block) -- for rows read over PCIe (out-of-core),
+// where the request size matters more than the latency.
+__device__ __forceinline__ bool sk_rejects_lev4(const uint32_t* __restrict__ A,
+                                                const uint32_t* B, int64_t wa, int64_t da,
+                                                int32_t cmin, int lane) {
+  // U = d_a - sum popc(x & ~y) only decreases: stop after the first 512-byte
+  // block that takes it below c_min (bytes over PCIe are the cost here)
+  int64_t u = da;
+  for (int64_t j0 = 0; j0 < wa; j0 += 128) {
+    const int64_t j = j0 + 4 * lane;
+    int acc = 0;
+    if (j < wa) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + j));
+      const uint4 y = *reinterpret_cast<const uint4*>(B + j);
+      acc = __popc(x.x & ~y.x) + __popc(x.y & ~y.y) + __popc(x.z & ~y.z) + __popc(x.w & ~y.w);
+    }
+    u -= __reduce_add_sync(0xffffffffu, acc);
+    if (u < cmin) return true;
+  }
+  return false;
+}
+
 // Thread-per-survivor form of the sketch bound: one thread walks S_a in
 // 16-byte steps against b's level (B: wa words, shared or global) or S_b
 // folded on the fly (wb > wa), stopping as soon as U = d_a - sum popc(x & ~y)

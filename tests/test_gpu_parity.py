@@ -429,3 +429,27 @@ def test_sketch_default_is_on_and_exact(orc):
     np.testing.assert_array_equal(r_roles, roles)
     np.testing.assert_array_equal(r_cl, cl)
     assert s.extra["sim_decided_by_sketch"] > 0
+
+
+@pytest.mark.parametrize("k", ["4", "8"])
+def test_ooc_sketch_bound_forced_everywhere(orc, monkeypatch, k):
+    """Out-of-core sketches (rows in mapped pinned host memory, b's levels
+    hashed from the streamed slice) tried on every survivor: bit-exact."""
+    monkeypatch.setenv("GS_SKETCH", k)
+    monkeypatch.setenv("GS_SKETCH_DMIN", "1")
+    monkeypatch.setenv("GS_SKETCH_GATE", "1e30")
+    for n, e in (orc.rmat(15, seed=6), _chunglu(14, 2.1, 3000, 12 << 14, 7)):
+        c = orc.CSR(n, e)
+        g = make_graph(n, e)
+        dmax = int(np.diff(g.vertex_offsets).max())
+        budget = 13 * n + (2 << 20) + 8 * (dmax + 1) + max(2 * g.m // 2 * 4 * 4 // 3, 8 * 4 * dmax)
+        decided = 0
+        for eps, mu in (("0.2", 3), ("0.5", 2), ("0.8", 2)):
+            roles, cl = orc.serial_scan(c, mu, eps)
+            plan, r, s = _ooc(g, mu, eps, budget)
+            assert s.extra["partitions"] >= 2, s.extra
+            np.testing.assert_array_equal(r.role_codes, roles, err_msg=f"k{k} {eps} {mu}")
+            np.testing.assert_array_equal(r.cluster_ids, cl, err_msg=f"k{k} {eps} {mu}")
+            assert s.extra["peak_device_bytes"] <= budget
+            decided += s.extra["sim_decided_by_sketch"]
+        assert decided > 0
