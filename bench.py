@@ -449,12 +449,16 @@ def run_ours(args):
                          "dram_achieved": (traffic / t_sim / 1e9) if traffic and t_sim > 0 else None,
                          "dram_frac": (traffic / t_sim / 1e9 / peak) if traffic and t_sim > 0
                          else None,
-                         "kernel": "similarity pass (identify phase: k_sim_hash*/k_sim_warp/"
-                                   "k_sim_tiny + O(1) pre-pass)",
-                         "note": "achieved = SURVEY 8(d) W_sim (every intersected edge reads "
-                                 "4*min(d)) / identify time; the exact early exit and the O(1) "
-                                 "suffix skip read far less, so it can exceed peak -- dram_frac "
-                                 "(ncu DRAM bytes / same time) is the traffic actually moved",
+                         "kernel": "similarity pass (identify phase: sketch build + O(1) "
+                                   "pre-pass + k_sim_hash*/k_sim_warp/k_sim_tiny)",
+                         "note": "achieved = SURVEY 8(d) W_sim (every edge not decided by the "
+                                 "O(1) degree bounds reads 4*min(d)) / identify time.  The "
+                                 "sketch bound (k/8 bytes per neighbour of the low endpoint, "
+                                 "early exit), the scan's exact early exit and the O(1) suffix "
+                                 "skip read far less than W_sim, so achieved exceeds the peak: "
+                                 "dram_frac (ncu DRAM bytes of the same kernels / same time) is "
+                                 "the traffic actually moved; the pass is latency/issue bound "
+                                 "(DESIGN.md 3a-3b)",
                          "alg_bytes_per_step": w_sim, "t_ms": t_sim * 1000, "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -467,6 +471,7 @@ def run_ours(args):
             "counts": {"sim_evals": stats.sim_evals, "sim_evals_avoided": m - stats.sim_evals,
                        "decided_by_bound": stats.extra["sim_decided_by_bound"],
                        "intersections": stats.extra["sim_intersections"],
+                "decided_by_sketch": stats.extra["sim_decided_by_sketch"],
                        "adj_probes": stats.adj_probes, "cores": int(st.n_core),
                        "members": int(st.n_member), "hubs": int(st.n_hub),
                        "outliers": int(st.n_outlier), "clusters": int(st.n_clusters)},
