@@ -133,7 +133,6 @@ struct SimParams {
   int32_t sk_minscan;   //   and the scan would need at least this many misses
   int sk_thread;        // thread-per-survivor sketch pass before the warp scans
   int32_t sk_tmax;      //   for rows of at most this many words (longer: per warp)
-  int sk_dyn;           //   survivors claimed dynamically (else thread t: t, t + NT)
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;

@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   int2* surv_jc = surv_ad + chunk;
   // sketch levels of b: S_b, then folded to 1/2, 1/4, ... (2 wb words, 16-byte aligned)
   uint32_t* sk_lev = reinterpret_cast<uint32_t*>(surv_jc + chunk);
-  __shared__ int s_item, s_nsurv, s_next, s_nstash, s_nkeep, s_tnext;
+  __shared__ int s_item, s_nsurv, s_next, s_nstash, s_nkeep;
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ int64_t s_nlo;
   __shared__ uint32_t s_stash[kStash];
@@ -424,51 +424,13 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           sk_staged = true;
         }
         if (tpass) {
-          // thread-per-survivor sketch pass (survivors claimed dynamically:
-          // row lengths vary); decided ones are marked (da = -1), the rest
-          // compacted to the front for the warp scans
+          // thread-per-survivor sketch pass; the survivors it cannot decide
+          // are compacted to the front for the warp scans
           const int64_t wbx = sk_words(db, P.sk_lk);
-          if (tid == 0) { s_nkeep = 0; s_tnext = 0; }
-          __syncthreads();
-          for (;;) {
-            const int i = P.sk_dyn ? atomicAdd(&s_tnext, 1) : -1;
-            if (i < 0 || i >= ns) break;
-            const int2 ad = surv_ad[i], jc = surv_jc[i];
-            if (sk_words(ad.y, P.sk_lk) <= P.sk_tmax && sk_try(P, ad.y, db, jc.y)) {
-              const int64_t wa = sk_words(ad.y, P.sk_lk);
-              if (sk_thread_rejects(sk_row(P, ad.x, ad.y, wa), sk_lev + 2 * (wbx - wa), wa, wa,
-                                    ad.y, jc.y)) {
-                record_edge(P, e0 + jc.x, ad.x, (int32_t)b, false, false, lc);
-                lc.sketch++;
-                lc.bytes += 4ull * (unsigned long long)ad.y;
-                atomicAdd(&s_bdis, 1u);
-                surv_ad[i].y = -1;
-              }
-            }
-          }
           int2 kad[2], kjc[2];
           int64_t koa[2];
           bool keep[2] = {false, false};
-          if (!P.sk_dyn) {  // static mapping: survivors tid and tid + NT
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-              const int i = tid + r * NT;
-              if (i >= ns) continue;
-              const int2 ad = surv_ad[i], jc = surv_jc[i];
-              if (sk_words(ad.y, P.sk_lk) <= P.sk_tmax && sk_try(P, ad.y, db, jc.y)) {
-                const int64_t wa = sk_words(ad.y, P.sk_lk);
-                if (sk_thread_rejects(sk_row(P, ad.x, ad.y, wa), sk_lev + 2 * (wbx - wa), wa,
-                                      wa, ad.y, jc.y)) {
-                  record_edge(P, e0 + jc.x, ad.x, (int32_t)b, false, false, lc);
-                  lc.sketch++;
-                  lc.bytes += 4ull * (unsigned long long)ad.y;
-                  atomicAdd(&s_bdis, 1u);
-                  surv_ad[i].y = -1;
-                }
-              }
-            }
-          }
-          __syncthreads();
+          if (tid == 0) s_nkeep = 0;
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             const int i = tid + r * NT;
@@ -476,7 +438,18 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             kad[r] = surv_ad[i];
             kjc[r] = surv_jc[i];
             koa[r] = surv_oa[i];
-            keep[r] = kad[r].y >= 0;
+            keep[r] = true;
+            if (sk_words(kad[r].y, P.sk_lk) <= P.sk_tmax && sk_try(P, kad[r].y, db, kjc[r].y)) {
+              const int64_t wa = sk_words(kad[r].y, P.sk_lk);
+              if (sk_thread_rejects(sk_row(P, kad[r].x, kad[r].y, wa), sk_lev + 2 * (wbx - wa),
+                                    wa, wa, kad[r].y, kjc[r].y)) {
+                keep[r] = false;
+                record_edge(P, e0 + kjc[r].x, kad[r].x, (int32_t)b, false, false, lc);
+                lc.sketch++;
+                lc.bytes += 4ull * (unsigned long long)kad[r].y;
+                atomicAdd(&s_bdis, 1u);
+              }
+            }
           }
           __syncthreads();
 #pragma unroll
@@ -862,8 +835,6 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   if (const char* v = getenv("GS_SKETCH_MINSCAN")) P.sk_minscan = atoi(v);
   P.sk_thread = 1;
   if (const char* v = getenv("GS_SKETCH_THREAD")) P.sk_thread = atoi(v);
-  P.sk_dyn = 1;
-  if (const char* v = getenv("GS_SKETCH_DYN")) P.sk_dyn = atoi(v);
   P.sk_tmax = 1 << 30;
   if (const char* v = getenv("GS_SKETCH_TMAX")) P.sk_tmax = atoi(v);
   P.shard_rank = e->shard_rank;
