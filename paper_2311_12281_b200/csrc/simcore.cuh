@@ -428,6 +428,8 @@ __device__ __forceinline__ bool sk_rejects_lev4(const uint32_t* __restrict__ A,
 // drops below c_min (U only decreases).  Used where many survivors are
 // checked at once, so hundreds of rows are in flight per SM instead of one
 // per warp.
+// U = 16-byte steps in flight per early-exit check
+template <int SK_UNROLL = 2>
 __device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A,
                                                   const uint32_t* B, int64_t wa, int64_t wb,
                                                   int64_t da, int32_t cmin) {
@@ -435,10 +437,10 @@ __device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A
   const uint4* b4 = reinterpret_cast<const uint4*>(B);
   const int64_t q = wa >> 2, qb = wb >> 2;
   int64_t u = da;
-  for (int64_t j = 0; j < q; j += 2) {
-    uint4 x[2], y[2];
+  for (int64_t j = 0; j < q; j += SK_UNROLL) {
+    uint4 x[SK_UNROLL], y[SK_UNROLL];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < SK_UNROLL; ++t) {
       x[t] = j + t < q ? __ldg(a4 + j + t) : make_uint4(0u, 0u, 0u, 0u);
       y[t] = j + t < q ? b4[j + t] : make_uint4(0u, 0u, 0u, 0u);
       for (int64_t f = j + t + q; f < qb; f += q) {  // fold (global S_b only)
@@ -447,7 +449,7 @@ __device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A
       }
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < SK_UNROLL; ++t)
       u -= __popc(x[t].x & ~y[t].x) + __popc(x[t].y & ~y[t].y) + __popc(x[t].z & ~y[t].z) +
            __popc(x[t].w & ~y[t].w);
     if (u < cmin) return true;
