@@ -170,3 +170,23 @@ def test_product_package_never_imports_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "liborc" not in text, f
+
+
+def test_stats_struct_matches_header():
+    """The ctypes mirror of gs_stats lists the header's fields in order (a
+    field added on one side only would shift every later counter)."""
+    import re
+
+    from paper_2311_12281_b200 import _lib
+
+    hdr = open(os.path.join(ROOT, "include", "gscan.h")).read()
+    body = re.search(r"typedef struct gs_stats \{(.*?)\} gs_stats;", hdr, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        decl = re.sub(r"\[.*?\]", "", decl)
+        names += [v.strip() for v in decl.split(None, 1)[1].split(",")]
+    assert names == [f[0] for f in _lib.GsStats._fields_]
