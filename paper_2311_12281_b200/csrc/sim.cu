@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       const int ns = s_nsurv;
       if (ns > 0) {
         int ns_scan = ns;
-        const bool tpass = !GTAB && P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
+        const bool tpass = P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
                            2 * sk_words(db, P.sk_lk) <= skw;
-        if (!GTAB && !sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
+        if (!sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
             2 * sk_words(db, P.sk_lk) <= skw) {  // b's sketch and its folds, once per b
           const int64_t wb = sk_words(db, P.sk_lk);
           sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
@@ -514,10 +514,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           if ((!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
-            if (GTAB)  // huge b: long rows, folded from global with wide loads
-              skd = sk_rejects_fold4(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
-            else if (lev)
+            if (lev)
               skd = sk_rejects_lev(A, sk_lev + 2 * (wb - wa), wa, ad.y, jc.y, lane);
+            else if (GTAB)  // huge b beyond the staged levels: wide loads from global
+              skd = sk_rejects_fold4(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
             else
               skd = sk_rejects_fold(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
           }
@@ -692,17 +692,20 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
       (size_t)((P.bm_words + 4 + 3) & ~3u) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
   // b's sketch levels in shared memory when they fit (else folded from global)
   int64_t skw = 0;
-  if (P.sk != nullptr && !GTAB) {
+  if (P.sk != nullptr) {
     int64_t dhi = 0;
     GS_CUDA(cudaMemcpyAsync(&dhi, e->g.off + rhi, 8, cudaMemcpyDeviceToHost, e->stream));
     int64_t dlo = 0;
     GS_CUDA(cudaMemcpyAsync(&dlo, e->g.off + rhi - 1, 8, cudaMemcpyDeviceToHost, e->stream));
     GS_CUDA(cudaStreamSynchronize(e->stream));
     const int64_t want = 2 * sk_words(dhi - dlo, P.sk_lk);  // the class's largest degree
-    if (smem + (size_t)want * 4 + 1024 <= (size_t)e->smem_optin) {  // + static shared memory
+    const int64_t room = ((int64_t)e->smem_optin - 1024 - (int64_t)smem) / 4;  // static smem
+    if (want <= room) {
       skw = want;
-      smem += (size_t)want * 4;
+    } else if (GTAB && room >= 8) {  // one CTA per SM anyway: levels for the b's that fit
+      skw = room & ~int64_t(3);
     }
+    smem += (size_t)skw * 4;
   }
   auto kern = k_sim_hash<NT, GTAB>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
