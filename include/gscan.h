@@ -245,6 +245,14 @@ int gs_format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
 /* Number of visible CUDA devices (0 when there is no usable driver/device). */
 int gs_device_count(void);
 
+/* Pay the one-time costs of a process's first scan ahead of it: CUDA context
+ * creation on `device` (< 0: current), the stream-ordered memory pool and
+ * the lazy loading of the scan kernels (one scan of a 4-vertex graph).  The
+ * Python package calls it from a background thread at import (opt out with
+ * GS_NO_WARMUP=1), so a cold process's first scan_in_memory does not wait
+ * ~1 s for the driver.  Thread-safe; GS_ECUDA without a usable device. */
+int gs_warmup(int device);
+
 const char* gs_last_error(void);
 int gs_version(void);
 

@@ -117,6 +117,7 @@ SIGNATURES = [
     ("gs_device_count", ctypes.c_int, []),
     ("gs_last_error", ctypes.c_char_p, []),
     ("gs_version", ctypes.c_int, []),
+    ("gs_warmup", ctypes.c_int, [ctypes.c_int]),
 ]
 
 _lib = None
@@ -224,3 +225,25 @@ def thread_engine() -> Engine:
         eng = Engine()
         _tls.engine = eng
     return eng
+
+
+def warm_up_async() -> Optional[threading.Thread]:
+    """Create the CUDA context (and load the scan kernels) in a daemon thread,
+    overlapped with whatever the process does before its first scan
+    (gs_warmup).  Without a device or library it does nothing."""
+    if os.environ.get("GS_NO_WARMUP"):
+        return None
+
+    def run():
+        try:
+            lib = load()
+            count = lib.gs_device_count()
+            if count > 0:  # torchrun ranks warm their own device
+                local = os.environ.get("LOCAL_RANK")
+                lib.gs_warmup(int(local) % count if local and local.isdigit() else -1)
+        except Exception:  # no library / no device: the first real call reports it
+            pass
+
+    t = threading.Thread(target=run, name="gscan-warmup", daemon=True)
+    t.start()
+    return t

@@ -182,6 +182,21 @@ void gs_engine::free_state() {
 extern "C" {
 
 int gs_version(void) { return GS_ABI_VERSION; }
+
+int gs_warmup(int device) {
+  gs_engine* e = nullptr;
+  GS_TRY(gs_engine_create(device, 0, &e));
+  // triangle 0-1-2 plus the pendant edge 2-3 (reference CSR), eps 0.5, mu 2
+  static const int64_t off[5] = {0, 2, 4, 7, 8};
+  static const int32_t adj[8] = {1, 2, 0, 2, 0, 1, 3, 2};
+  uint8_t role[4];
+  int32_t cl[4];
+  gs_eps2 eps{1, 0, 4, 0};
+  int rc = gs_engine_load_csr(e, 4, 4, off, adj, 0);
+  if (rc == GS_OK) rc = gs_engine_scan(e, 2, &eps, role, cl, 0, nullptr);
+  gs_engine_destroy(e);
+  return rc;
+}
 int gs_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) { cudaGetLastError(); return 0; }
