@@ -401,6 +401,21 @@ __device__ __forceinline__ int64_t rank_of_degree(const int64_t* off, int64_t n,
   return lo;
 }
 
+// The runs a sort kernel handles: a contiguous rank range [rlo, rhi), or the
+// ranks listed in list[0, *count) (the host-streamed build sorts each chunk's
+// completed runs while later chunks are still in flight)
+struct RunSet {
+  int64_t rlo, rhi;
+  const int32_t* list;
+  const int* count;
+};
+__device__ __forceinline__ int64_t rs_size(const RunSet& R) {
+  return R.list ? (int64_t)*R.count : R.rhi - R.rlo;
+}
+__device__ __forceinline__ int64_t rs_at(const RunSet& R, int64_t i) {
+  return R.list ? (int64_t)R.list[i] : R.rlo + i;
+}
+
 __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t n,
                                int64_t* __restrict__ out) {
   const int64_t th[7] = {2, 33, 257, 513, 1025, 2049, 4096};
@@ -409,13 +424,13 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t n,
 }
 
 __global__ void __launch_bounds__(256) k_sort_runs_reg(const int64_t* __restrict__ off,
-                                                       int64_t rlo, int64_t rhi,
-                                                       int32_t* __restrict__ arcs,
+                                                       RunSet R, int32_t* __restrict__ arcs,
                                                        int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = rlo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); v < rhi;
-       v += nw) {
+  const int64_t nr = rs_size(R);
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < nr; it += nw) {
+    const int64_t v = rs_at(R, it);
     const int64_t o = off[v];
     const int d = (int)(off[v + 1] - o);
     int32_t x = lane < d ? arcs[o + lane] : kPad;
@@ -453,8 +468,7 @@ __device__ __forceinline__ void bitonic_smem(int32_t* s, int P, int t, int nt) {
 
 template <bool BLOCK, int CAP>
 __global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restrict__ off,
-                                                        int64_t rlo, int64_t rhi,
-                                                        int32_t* __restrict__ arcs,
+                                                        RunSet R, int32_t* __restrict__ arcs,
                                                         int* __restrict__ bad) {
   __shared__ int32_t buf[BLOCK ? CAP : 8 * CAP];
   const int nt = BLOCK ? blockDim.x : 32;
@@ -462,7 +476,9 @@ __global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restric
   int32_t* s = BLOCK ? buf : buf + (threadIdx.x >> 5) * CAP;
   const int64_t groups = BLOCK ? gridDim.x : ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t g0 = BLOCK ? blockIdx.x : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  for (int64_t v = rlo + g0; v < rhi; v += groups) {
+  const int64_t nr = rs_size(R);
+  for (int64_t it = g0; it < nr; it += groups) {
+    const int64_t v = rs_at(R, it);
     const int64_t o = off[v];
     const int d = (int)(off[v + 1] - o);
     int P = 1;
@@ -484,7 +500,7 @@ __global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restric
 // rank bits (+ one bit that sends the padding to the end)
 template <int NT, int ITEMS>
 __global__ void __launch_bounds__(NT) k_sort_runs_block(const int64_t* __restrict__ off,
-                                                         int64_t rlo, int64_t rhi, int endbit,
+                                                         RunSet R, int endbit,
                                                          int32_t* __restrict__ arcs,
                                                          int* __restrict__ bad) {
   using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
@@ -492,7 +508,9 @@ __global__ void __launch_bounds__(NT) k_sort_runs_block(const int64_t* __restric
   __shared__ int s_dup;
   const int t = threadIdx.x;
   if (t == 0) s_dup = 0;
-  for (int64_t v = rlo + blockIdx.x; v < rhi; v += gridDim.x) {
+  const int64_t nr = rs_size(R);
+  for (int64_t it = blockIdx.x; it < nr; it += gridDim.x) {
+    const int64_t v = rs_at(R, it);
     const int64_t o = off[v];
     const int d = (int)(off[v + 1] - o);
     uint32_t k[ITEMS];
@@ -545,7 +563,7 @@ __global__ void k_tail_extract(const uint64_t* __restrict__ keys, int64_t cnt, i
 
 // Sort every run of `arcs` (offsets g.off) in place.
 static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad,
-                     int64_t row_lo, int64_t row_hi) {
+                     int64_t row_lo, int64_t row_hi, bool classes_done = false) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
   if (slots == 0 || n == 0) return GS_OK;
@@ -567,34 +585,36 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
     return (unsigned)(runs < (int64_t)e->sms * 16 ? runs : (int64_t)e->sms * 16);
   };
   const int endbit = std::min(32, bits_for(n - 1) + 1);
-  if (r33 > r2) {
-    k_sort_runs_reg<<<warps_grid(r33 - r2), 256, 0, st>>>(g.off, r2, r33, arcs, d_bad);
+  if (classes_done) r[6] = std::max(r[6], r2);  // runs < 4096 sorted chunk by chunk
+  if (!classes_done && r33 > r2) {
+    k_sort_runs_reg<<<warps_grid(r33 - r2), 256, 0, st>>>(g.off, RunSet{r2, r33, nullptr, nullptr},
+                                                          arcs, d_bad);
     e->launches++;
   }
-  if (r257 > r33) {
-    k_sort_runs_smem<false, 256><<<warps_grid(r257 - r33), 256, 0, st>>>(g.off, r33, r257, arcs,
+  if (!classes_done && r257 > r33) {
+    k_sort_runs_smem<false, 256><<<warps_grid(r257 - r33), 256, 0, st>>>(g.off, RunSet{r33, r257, nullptr, nullptr}, arcs,
                                                                         d_bad);
     e->launches++;
   }
   // CTA classes sized to the run: (256,512] 128x4, (512,1024] 128x8, (1024,2048] 256x8,
   // (2048,4096) 256x16 slots
-  if (r[3] > r[2]) {
-    k_sort_runs_block<128, 4><<<blocks_grid(r[3] - r[2]), 128, 0, st>>>(g.off, r[2], r[3], endbit,
+  if (!classes_done && r[3] > r[2]) {
+    k_sort_runs_block<128, 4><<<blocks_grid(r[3] - r[2]), 128, 0, st>>>(g.off, RunSet{r[2], r[3], nullptr, nullptr}, endbit,
                                                                         arcs, d_bad);
     e->launches++;
   }
-  if (r[4] > r[3]) {
-    k_sort_runs_block<128, 8><<<blocks_grid(r[4] - r[3]), 128, 0, st>>>(g.off, r[3], r[4], endbit,
+  if (!classes_done && r[4] > r[3]) {
+    k_sort_runs_block<128, 8><<<blocks_grid(r[4] - r[3]), 128, 0, st>>>(g.off, RunSet{r[3], r[4], nullptr, nullptr}, endbit,
                                                                         arcs, d_bad);
     e->launches++;
   }
-  if (r[5] > r[4]) {
-    k_sort_runs_block<256, 8><<<blocks_grid(r[5] - r[4]), 256, 0, st>>>(g.off, r[4], r[5], endbit,
+  if (!classes_done && r[5] > r[4]) {
+    k_sort_runs_block<256, 8><<<blocks_grid(r[5] - r[4]), 256, 0, st>>>(g.off, RunSet{r[4], r[5], nullptr, nullptr}, endbit,
                                                                         arcs, d_bad);
     e->launches++;
   }
-  if (r[6] > r[5]) {
-    k_sort_runs_block<256, 16><<<blocks_grid(r[6] - r[5]), 256, 0, st>>>(g.off, r[5], r[6],
+  if (!classes_done && r[6] > r[5]) {
+    k_sort_runs_block<256, 16><<<blocks_grid(r[6] - r[5]), 256, 0, st>>>(g.off, RunSet{r[5], r[6], nullptr, nullptr},
                                                                          endbit, arcs, d_bad);
     e->launches++;
   }
@@ -796,8 +816,9 @@ static int arcs_buffer(gs_engine* e, int64_t slots, int32_t* adj_out, int32_t** 
 
 // after the scatter: sort this part's runs, then finish now or on finish_build
 static int finish_part(gs_engine* e, int64_t n, int64_t m, int32_t* arcs, const int64_t* h_cls,
-                       int* d_bad, int64_t row_lo, int64_t row_hi, bool defer) {
-  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, row_lo, row_hi));
+                       int* d_bad, int64_t row_lo, int64_t row_hi, bool defer,
+                       bool classes_done = false) {
+  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, row_lo, row_hi, classes_done));
   e->g.adj = arcs;
   if (!defer) return finish_rest(e, n, m, h_cls, d_bad);
   GS_CUDA(cudaStreamSynchronize(e->stream));  // the part is complete for the exchange
@@ -850,6 +871,64 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const
     e->launches += 2;
   }
   return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1);
+}
+
+// Per-run sort classes of the runs a host chunk completed (caller vertices
+// [ua, ub), their rank-space runs in [row_lo, row_hi)): ranks appended to
+// six class lists (the classes of sort_runs; runs >= 4096 and < 2 are left to
+// the final pass), one shared-memory count + one global reservation per
+// class per block.
+static constexpr int kChunkClasses = 6;
+__global__ void __launch_bounds__(256) k_chunk_classes(const int64_t* __restrict__ off, int64_t ua,
+                                                       int64_t ub, const int32_t* __restrict__ rank,
+                                                       int64_t row_lo, int64_t row_hi,
+                                                       int32_t* __restrict__ lists, int64_t stride,
+                                                       int* __restrict__ counts) {
+  __shared__ int s_cnt[kChunkClasses], s_base[kChunkClasses];
+  for (int64_t base = ua + (int64_t)blockIdx.x * blockDim.x; base < ub;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < kChunkClasses) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t u = base + threadIdx.x;
+    int cls = -1, pos = 0;
+    int32_t r = 0;
+    if (u < ub) {
+      const int64_t d = off[u + 1] - off[u];
+      r = rank[u];
+      if (r >= row_lo && r < row_hi && d >= 2 && d < 4096)
+        cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= 512 ? 2 : d <= 1024 ? 3 : d <= 2048 ? 4 : 5;
+      if (cls >= 0) pos = atomicAdd(&s_cnt[cls], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < kChunkClasses)
+      s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]) : 0;
+    __syncthreads();
+    if (cls >= 0) lists[cls * stride + s_base[cls] + pos] = r;
+    __syncthreads();
+  }
+}
+
+static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64_t ub,
+                           int64_t row_lo, int64_t row_hi, int32_t* lists, int64_t stride,
+                           int* counts, int endbit, int32_t* arcs, int* d_bad) {
+  cudaStream_t st = e->stream;
+  const DevGraph& g = e->g;
+  if (ub <= ua) return GS_OK;
+  GS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * kChunkClasses, st));
+  k_chunk_classes<<<(unsigned)std::min<int64_t>(grid_for(ub - ua, 256), (int64_t)e->sms * 8), 256,
+                    0, st>>>(d_off, ua, ub, g.rank, row_lo, row_hi, lists, stride, counts);
+  auto L = [&](int c) { return RunSet{0, 0, lists + c * stride, counts + c}; };
+  const unsigned wg = (unsigned)std::min<int64_t>((ub - ua + 7) / 8, (int64_t)e->sms * 16);
+  const unsigned bg = (unsigned)std::min<int64_t>(ub - ua, (int64_t)e->sms * 8);
+  k_sort_runs_reg<<<wg, 256, 0, st>>>(g.off, L(0), arcs, d_bad);
+  k_sort_runs_smem<false, 256><<<wg, 256, 0, st>>>(g.off, L(1), arcs, d_bad);
+  k_sort_runs_block<128, 4><<<bg, 128, 0, st>>>(g.off, L(2), endbit, arcs, d_bad);
+  k_sort_runs_block<128, 8><<<bg, 128, 0, st>>>(g.off, L(3), endbit, arcs, d_bad);
+  k_sort_runs_block<256, 8><<<bg, 256, 0, st>>>(g.off, L(4), endbit, arcs, d_bad);
+  k_sort_runs_block<256, 16><<<bg, 256, 0, st>>>(g.off, L(5), endbit, arcs, d_bad);
+  e->launches += 7;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
 }
 
 // Host CSR (the reference Graph in pinned or pageable memory): the offsets
@@ -958,6 +1037,27 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
   int32_t* arcs = nullptr;
   GS_TRY(arcs_buffer(e, slots, adj_out, &arcs));
   const int64_t rh = std::max<int64_t>(h_cls[2], row_lo);
+  // Runs completed by chunk c (caller vertices whose whole run has arrived)
+  // are sorted right after its scatter, while later chunks are in flight;
+  // only the hub runs (>= 4096) wait for the final pass.
+  std::vector<int64_t> done(nchunks + 1, 0);
+  int64_t maxv = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t end = std::min<int64_t>((c + 1) * kChunk, slots);
+    done[c + 1] = c + 1 == nchunks ? n
+                                   : std::upper_bound(off_host + 1, off_host + n + 1, end) -
+                                         (off_host + 1);
+    maxv = std::max(maxv, done[c + 1] - done[c]);
+  }
+  int32_t* clists = nullptr;
+  int* ccounts = nullptr;
+  bool chunk_sort = nchunks > 1 && !(getenv("GS_CHUNK_SORT") && atoi(getenv("GS_CHUNK_SORT")) == 0);
+  if (chunk_sort && (e->alloc_n(&clists, kChunkClasses * std::max<int64_t>(maxv, 1)) != GS_OK ||
+                     e->alloc_n(&ccounts, kChunkClasses) != GS_OK)) {
+    chunk_sort = false;  // no room (HBM cap): sort everything at the end
+    cudaGetLastError();
+  }
+  const int endbit = std::min(32, bits_for(n - 1) + 1);
   for (int64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
@@ -976,7 +1076,12 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     e->launches += 2;
     GS_CUDA(cudaEventRecord(freed[k], st));
     if (next < nchunks) GS_TRY(issue(next++));
+    if (chunk_sort)
+      GS_TRY(sort_chunk_runs(e, d_off, done[c], done[c + 1], row_lo, row_hi, clists,
+                             std::max<int64_t>(maxv, 1), ccounts, endbit, arcs, d_bad));
   }
+  e->release(clists);
+  e->release(ccounts);
   GS_CUDA(cudaGetLastError());
   GS_CUDA(cudaStreamSynchronize(cs));
   for (int k = 0; k < nring; ++k) e->release(ring[k]);
@@ -985,7 +1090,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     cudaEventDestroy(copied[k]);
     cudaEventDestroy(freed[k]);
   }
-  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1);
+  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, chunk_sort);
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ d, int64_t n, int64_t* __restrict__ o) {
