@@ -728,14 +728,14 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   const int32_t* hadj = static_cast<const int32_t*>(madj.dev);
 
   cudaStream_t copy = nullptr;
-  cudaEvent_t ev_copied[2], ev_free[2], t0, t1, t2, t3, t4;
+  cudaEvent_t ev_copied[2], ev_free[2], t0, t1, t2, t3, t4, t5;
   cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking);
   for (int i = 0; i < 2; ++i) {
     cudaEventCreateWithFlags(&ev_copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_free[i], cudaEventDisableTiming);
   }
   cudaEventCreate(&t0); cudaEventCreate(&t1); cudaEventCreate(&t2);
-  cudaEventCreate(&t3); cudaEventCreate(&t4);
+  cudaEventCreate(&t3); cudaEventCreate(&t4); cudaEventCreate(&t5);
   int result = GS_OK;
   int64_t launches = 0;
   uint32_t* hsk = nullptr;      // pinned host sketch rows
@@ -989,6 +989,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       };
       if ((result = sweep(sk_body)) != GS_OK) break;
     }
+    cudaEventRecord(t5, cs);  // end of the sketch pre-pass (== t0 without sketches)
     // ---- pass 1: identify (Alg. 5 first loop)
     P.mode = OOC_IDENTIFY;
     if ((result = sweep(sim_body)) != GS_OK) break;
@@ -1063,6 +1064,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       cudaEventElapsedTime(&ms, t1, t2); st->phase_ms[GS_PH_CLUSTER] = ms;
       cudaEventElapsedTime(&ms, t2, t3); st->phase_ms[GS_PH_CLASSIFY] = ms;
       cudaEventElapsedTime(&ms, t0, t3); st->phase_ms[GS_PH_TOTAL] = ms;
+      cudaEventElapsedTime(&ms, t0, t5); st->phase_ms[GS_PH_BUILD] = ms;  // sketch pre-pass
     }
     if (st) {
       st->n_member = (int64_t)hc[CTR_N_MEMBER];
@@ -1078,7 +1080,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     cudaEventDestroy(ev_free[i]);
   }
   cudaEventDestroy(t0); cudaEventDestroy(t1); cudaEventDestroy(t2);
-  cudaEventDestroy(t3); cudaEventDestroy(t4);
+  cudaEventDestroy(t3); cudaEventDestroy(t4); cudaEventDestroy(t5);
   if (hsk) cudaFreeHost(hsk);
   if (hsk_off) cudaFreeHost(hsk_off);
   cleanup();

@@ -100,9 +100,11 @@ def main():
         "partitions": int(st.partitions),
         "seconds": wall,
         "edges_per_s": m / wall,
-        "phases_ms": {"identify": st.phase_ms[2], "cluster": st.phase_ms[4],
+        "phases_ms": {"sketch_prepass": st.phase_ms[1], "identify": st.phase_ms[2],
+                      "cluster": st.phase_ms[4],
                       "classify": st.phase_ms[5], "total_device": st.phase_ms[7]},
         "counts": {"sim_evals": int(st.sim_evals), "decided_by_bound": int(st.sim_decided_by_bound),
+                   "decided_by_sketch": int(st.sim_decided_by_sketch),
                    "intersections": int(st.sim_intersections), "adj_probes": int(st.adj_probes),
                    "cores": int(st.n_core), "members": int(st.n_member), "hubs": int(st.n_hub),
                    "outliers": int(st.n_outlier), "clusters": int(st.n_clusters)},
