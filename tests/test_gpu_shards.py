@@ -176,3 +176,21 @@ def test_partitioned_build_rejects_invalid_part():
                                                g.adjacency.ctypes.data, 0, 0, 2, None, b))
     with pytest.raises(ValueError):
         _lib.check(lib.gs_engine_load_finish(eng.handle))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_with_sketch_forced(orc, monkeypatch, world):
+    """Every rank tries the sketch bound on every survivor it owns (rows built
+    by each rank for the whole graph): still the oracle's result."""
+    monkeypatch.setenv("GS_SKETCH", "4")
+    monkeypatch.setenv("GS_SKETCH_DMIN", "1")
+    monkeypatch.setenv("GS_SKETCH_MINSCAN", "-1000000")
+    monkeypatch.setenv("GS_SKETCH_GATE", "1e30")
+    n, e = orc.rmat(15, seed=8)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.2", 3), ("0.4", 2)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        for r_roles, r_cl, _ in sharded(g, mu, eps, world, partitioned=True):
+            np.testing.assert_array_equal(r_roles, roles, err_msg=f"w{world} {eps} {mu}")
+            np.testing.assert_array_equal(r_cl, cl, err_msg=f"w{world} {eps} {mu}")
