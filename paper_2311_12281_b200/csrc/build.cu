@@ -838,6 +838,10 @@ int finish_build(gs_engine* e) {
   return finish_rest(e, e->pend_n, e->pend_m, e->pend_cls, d_bad);
 }
 
+static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
+                              const int32_t* adj, int32_t* arcs, int* d_bad, int64_t row_lo,
+                              int64_t row_hi, int64_t r512);
+
 int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const int32_t* adj,
                    int part_rank, int part_world, int32_t* adj_out, int64_t* slot_bounds) {
   cudaStream_t st = e->stream;
@@ -859,6 +863,11 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const
   GS_TRY(part_rows(e, n, 2 * m, part_rank, part_world, &row_lo, &row_hi, slot_bounds));
   int32_t* arcs = nullptr;
   GS_TRY(arcs_buffer(e, 2 * m, adj_out, &arcs));
+  const bool fused = m > 0 && !(getenv("GS_FUSED_BUILD") && atoi(getenv("GS_FUSED_BUILD")) == 0);
+  if (fused) {
+    GS_TRY(fused_scatter_sort(e, n, m, off, adj, arcs, d_bad, row_lo, row_hi, h_cls[2]));
+    return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, true);
+  }
   if (m > 0) {
     k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
                     0, st>>>(off, n, 0, n, adj, 0, 2 * m, 0, g.rank, g.off, arcs, d_bad, row_lo,
@@ -927,6 +936,172 @@ static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64
   k_sort_runs_block<256, 8><<<bg, 256, 0, st>>>(g.off, L(4), endbit, arcs, d_bad);
   k_sort_runs_block<256, 16><<<bg, 256, 0, st>>>(g.off, L(5), endbit, arcs, d_bad);
   e->launches += 7;
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Fused relabel + sort for a device-resident reference CSR: each caller run is
+// read, relabelled, sorted where it is held (registers / shared memory) and
+// written once, sorted, to its rank-space run -- instead of scatter, then a
+// second read-sort-write pass.  Runs of 4096+ neighbours still go through the
+// scatter + the radix sort of (run, neighbour) keys (sort_runs' tail).
+
+// validate caller slot i of u (value v): ids, self-loops, strictly increasing runs
+__device__ __forceinline__ int32_t fused_check(const int32_t* __restrict__ adj, int64_t i,
+                                               int64_t ou, int64_t n, int64_t u, bool& b3,
+                                               bool& b4) {
+  int32_t v = adj[i];
+  if (v < 0 || v >= n || v == u) { b3 = true; v = (int32_t)u; }
+  if (i > ou && adj[i - 1] >= v) b4 = true;
+  return v;
+}
+
+// warp per caller vertex with d <= 32 (lane i holds element i): register
+// bitonic network; d in (32, 511]: warp per vertex, bitonic in a 2 KB
+// shared-memory slice.  Longer runs are skipped (CTA kernels below).
+__global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ off, int64_t n,
+                                                    const int32_t* __restrict__ adj,
+                                                    const int32_t* __restrict__ rank,
+                                                    const int64_t* __restrict__ noff,
+                                                    int32_t* __restrict__ out,
+                                                    int* __restrict__ bad, int64_t row_lo,
+                                                    int64_t row_hi) {
+  constexpr int CAP = 512;
+  __shared__ int32_t buf[8 * CAP];
+  const int lane = threadIdx.x & 31;
+  int32_t* sbuf = buf + (threadIdx.x >> 5) * CAP;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool b3 = false, b4 = false, b5 = false;
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
+    const int64_t ou = off[u];
+    const int d = (int)(off[u + 1] - ou);
+    if (d == 0 || d >= kHeavyScatter) continue;
+    const int64_t ru = rank[u];
+    if (ru < row_lo || ru >= row_hi) continue;
+    int32_t* o = out + noff[ru];
+    if (d <= 32) {
+      int32_t x = kPad;
+      if (lane < d) x = rank[fused_check(adj, ou + lane, ou, n, u, b3, b4)];
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+          const bool up = (lane & k) == 0, low = (lane & j) == 0;
+          x = (low == up) ? min(x, y) : max(x, y);
+        }
+      }
+      const int32_t nx = __shfl_down_sync(0xffffffffu, x, 1);
+      if (lane < d) {
+        o[lane] = x;
+        b5 |= lane + 1 < d && nx == x;
+      }
+    } else {
+      int P = 64;
+      while (P < d) P <<= 1;
+      for (int i = lane; i < P; i += 32)
+        sbuf[i] = i < d ? rank[fused_check(adj, ou + i, ou, n, u, b3, b4)] : kPad;
+      __syncwarp();
+      bitonic_smem<false>(sbuf, P, lane, 32);
+      for (int i = lane; i < d; i += 32) {
+        o[i] = sbuf[i];
+        b5 |= i + 1 < d && sbuf[i + 1] == sbuf[i];
+      }
+      __syncwarp();
+    }
+  }
+  if (b3) atomicExch(bad, 3);
+  if (b4) atomicExch(bad, 4);
+  if (b5) atomicExch(bad, 5);
+}
+
+// CTA per run of a rank range whose degrees lie in [kHeavyScatter, NT * ITEMS]:
+// block radix sort over the rank bits
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT) k_fused_block(const int64_t* __restrict__ off, int64_t n,
+                                                    int64_t rlo, int64_t rhi,
+                                                    const int32_t* __restrict__ orig,
+                                                    const int32_t* __restrict__ adj,
+                                                    const int32_t* __restrict__ rank,
+                                                    const int64_t* __restrict__ noff, int endbit,
+                                                    int32_t* __restrict__ out,
+                                                    int* __restrict__ bad) {
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
+  __shared__ typename Sort::TempStorage tmp;
+  const int t = threadIdx.x;
+  bool b3 = false, b4 = false, b5 = false;
+  for (int64_t r = rlo + blockIdx.x; r < rhi; r += gridDim.x) {
+    const int64_t u = orig[r];
+    const int64_t ou = off[u];
+    const int d = (int)(off[u + 1] - ou);
+    uint32_t k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      k[i] = idx < d ? (uint32_t)rank[fused_check(adj, ou + idx, ou, n, u, b3, b4)] : 0xFFFFFFFFu;
+    }
+    Sort(tmp).SortBlockedToStriped(k, 0, endbit);
+    int32_t* o = out + noff[r];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx < d) o[idx] = (int32_t)k[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx + 1 < d) b5 |= o[idx] == o[idx + 1];
+    }
+    __syncthreads();
+  }
+  if (b3) atomicExch(bad, 3);
+  if (b4) atomicExch(bad, 4);
+  if (b5) atomicExch(bad, 5);
+}
+
+// the device-CSR build's relabel + per-run sorts, fused (runs >= 4096 are
+// only scattered here; sort_runs sorts them afterwards)
+static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
+                              const int32_t* adj, int32_t* arcs, int* d_bad, int64_t row_lo,
+                              int64_t row_hi, int64_t r512) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  int64_t* d_cls = nullptr;
+  GS_TRY(e->alloc_n(&d_cls, 8));
+  k_sort_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
+  int64_t r[7];
+  GS_CUDA(cudaMemcpyAsync(r, d_cls, 7 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  e->release(d_cls);
+  e->launches++;
+  const int endbit = std::min(32, bits_for(n - 1) + 1);
+  k_fused_warp<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
+                 0, st>>>(off, n, adj, g.rank, g.off, arcs, d_bad, row_lo, row_hi);
+  e->launches++;
+  auto clip = [&](int64_t x) { return std::min(std::max(x, row_lo), row_hi); };
+  // rank ranges by degree (ranks ascend with the degree): [512, 1024], [1025, 2048],
+  // [2049, 4095], >= 4096 (r512 = first rank of degree >= 512, h_cls[2])
+  const int64_t h512 = clip(r512), h1025 = clip(r[4]), h2049 = clip(r[5]),
+                h4096 = clip(r[6]);
+  auto blocks = [&](int64_t runs) {
+    return (unsigned)std::min<int64_t>(std::max<int64_t>(runs, 1), (int64_t)e->sms * 16);
+  };
+  if (h1025 > h512)
+    k_fused_block<128, 8><<<blocks(h1025 - h512), 128, 0, st>>>(
+        off, n, h512, h1025, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+  if (h2049 > h1025)
+    k_fused_block<256, 8><<<blocks(h2049 - h1025), 256, 0, st>>>(
+        off, n, h1025, h2049, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+  if (h4096 > h2049)
+    k_fused_block<256, 16><<<blocks(h4096 - h2049), 256, 0, st>>>(
+        off, n, h2049, h4096, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+  if (row_hi > h4096)  // longest runs: scattered, sorted by sort_runs' radix tail
+    k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(row_hi - h4096, (int64_t)e->sms * 16), 256,
+                          0, st>>>(off, n, h4096, row_hi, g.orig, adj, 0, 2 * m, 0, g.rank,
+                                   g.off, arcs, d_bad);
+  e->launches += 4;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
 }

@@ -171,3 +171,69 @@ def test_vertex_count_sweep_sharded_and_out_of_core(orc, n):
     assert s.extra["partitions"] >= 2
     np.testing.assert_array_equal(r.role_codes, roles, err_msg=f"n={n} ooc")
     np.testing.assert_array_equal(r.cluster_ids, cl, err_msg=f"n={n} ooc")
+
+
+def _device_csr_scan(g, mu, eps):
+    """gs_engine_load_csr from DEVICE arrays (the fused relabel + sort build)."""
+    import ctypes
+
+    import torch
+
+    from paper_2311_12281_b200 import _lib
+
+    lib = _lib.load()
+    off = torch.from_numpy(np.asarray(g.vertex_offsets, dtype=np.int64)).cuda()
+    adj = torch.from_numpy(np.asarray(g.adjacency, dtype=np.int32)).cuda()
+    torch.cuda.synchronize()
+    eng = _lib.Engine()
+    try:
+        _lib.check(lib.gs_engine_load_csr(eng.handle, g.n, g.m, off.data_ptr(), adj.data_ptr(), 1))
+        roles = np.empty(g.n, np.uint8)
+        cl = np.empty(g.n, np.int32)
+        eps2 = _lib.eps2_struct(gs.epsilon_fraction(eps))
+        _lib.check(lib.gs_engine_scan(eng.handle, mu, ctypes.byref(eps2), roles.ctypes.data,
+                                      cl.ctypes.data, 0, None))
+        return roles, cl
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_device_csr_every_sort_class(orc, monkeypatch, fused):
+    """Device-resident reference CSR: fused relabel + per-run sort (and the
+    unfused scatter-then-sort order) in every size class incl. the hub tail."""
+    monkeypatch.setenv("GS_FUSED_BUILD", fused)
+    n, e = _degree_class_graph(seed=5)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    for eps, mu in (("0.1", 3), ("0.5", 5)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        r_roles, r_cl = _device_csr_scan(g, mu, eps)
+        np.testing.assert_array_equal(r_roles, roles, err_msg=f"{fused} {eps} {mu}")
+        np.testing.assert_array_equal(r_cl, cl, err_msg=f"{fused} {eps} {mu}")
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("deg", [5, 100, 700, 3000, 6000])
+def test_device_csr_invalid_runs_detected(monkeypatch, fused, deg):
+    """A duplicate, a self-loop or an unsorted run is rejected (ValueError) in
+    every size class of the device build."""
+    monkeypatch.setenv("GS_FUSED_BUILD", fused)
+    from paper_2311_12281_b200.graph import Graph
+
+    n = deg + 10
+    edges = [(0, v) for v in range(1, deg + 1)] + [(1, 2)]
+    base = make_graph(n, np.array(edges, dtype=np.int32))
+    for kind in ("dup", "self", "unsorted"):
+        adj = np.asarray(base.adjacency, dtype=np.int32).copy()
+        o = int(base.vertex_offsets[0])
+        if kind == "dup":
+            adj[o + 1] = adj[o]
+        elif kind == "self":
+            adj[o + deg // 2] = 0
+        else:
+            adj[o], adj[o + 1] = adj[o + 1], adj[o]
+        g = Graph(n=base.n, m=base.m, vertex_offsets=base.vertex_offsets, adjacency=adj,
+                  edge_ids=base.edge_ids, edge_list=base.edge_list, orig_ids=base.orig_ids)
+        with pytest.raises(ValueError):
+            _device_csr_scan(g, 2, "0.5")
