@@ -561,6 +561,23 @@ __global__ void k_tail_extract(const uint64_t* __restrict__ keys, int64_t cnt, i
   }
 }
 
+__global__ void k_rebase(const int64_t* __restrict__ in, int64_t k, int64_t base,
+                         int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i] - base;
+}
+
+// a repeated neighbour in a sorted run is a duplicate edge (bad = 5)
+__global__ void k_run_dups(const int64_t* __restrict__ off, int64_t rlo, int64_t rhi,
+                           const int32_t* __restrict__ arcs, int* __restrict__ bad) {
+  bool dup = false;
+  for (int64_t v = rlo + blockIdx.x; v < rhi; v += gridDim.x)
+    for (int64_t i = off[v] + 1 + threadIdx.x; i < off[v + 1]; i += blockDim.x)
+      dup |= arcs[i] == arcs[i - 1];
+  if (dup) atomicExch(bad, 5);
+}
+
 // Sort every run of `arcs` (offsets g.off) in place.
 static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad,
                      int64_t row_lo, int64_t row_hi, bool classes_done = false) {
@@ -626,7 +643,31 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
   GS_CUDA(cudaStreamSynchronize(st));
   const int64_t cnt = hend - hbig;
   (void)slots;
-  if (cnt > 0) {
+  const bool seg_tail = !(getenv("GS_SEG_TAIL") && atoi(getenv("GS_SEG_TAIL")) == 0);
+  if (cnt > 0 && seg_tail) {
+    // the long runs sorted as segments over the neighbour bits only (int32
+    // keys, B bits) instead of one radix sort of 64-bit (run, neighbour) keys
+    const int B = bits_for(n - 1);
+    const int64_t nseg = row_hi - rbig;
+    int64_t* segoff = nullptr;
+    int32_t* tmp = nullptr;
+    GS_TRY(e->alloc_n(&segoff, nseg + 1));
+    GS_TRY(e->alloc_n(&tmp, cnt));
+    k_rebase<<<grid_for(nseg + 1, 256), 256, 0, st>>>(g.off + rbig, nseg + 1, hbig, segoff);
+    cub::DoubleBuffer<int32_t> db(arcs + hbig, tmp);
+    GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+      return cub::DeviceSegmentedRadixSort::SortKeys(t, b, db, cnt, nseg, segoff, segoff + 1, 0,
+                                                     B, st);
+    }));
+    if (db.Current() != arcs + hbig)
+      GS_CUDA(cudaMemcpyAsync(arcs + hbig, db.Current(), sizeof(int32_t) * (size_t)cnt,
+                              cudaMemcpyDeviceToDevice, st));
+    k_run_dups<<<(unsigned)std::min<int64_t>(nseg, (int64_t)e->sms * 8), 256, 0, st>>>(
+        g.off, rbig, row_hi, arcs, d_bad);
+    e->launches += 3;
+    e->release(segoff);
+    e->release(tmp);
+  } else if (cnt > 0) {
     const int B = bits_for(n - 1);
     const int R = bits_for(row_hi - 1 - rbig);
     uint64_t *k1 = nullptr, *k2 = nullptr;
