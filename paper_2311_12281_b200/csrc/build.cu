@@ -568,13 +568,23 @@ __global__ void k_rebase(const int64_t* __restrict__ in, int64_t k, int64_t base
     out[i] = in[i] - base;
 }
 
-// a repeated neighbour in a sorted run is a duplicate edge (bad = 5)
+// a repeated neighbour in a sorted run is a duplicate edge (bad = 5): flat
+// over the slots [s0, s1) of runs [rlo, rhi); an equal pair is checked against
+// the run boundaries only when it occurs (rare), by binary search
 __global__ void k_run_dups(const int64_t* __restrict__ off, int64_t rlo, int64_t rhi,
-                           const int32_t* __restrict__ arcs, int* __restrict__ bad) {
+                           int64_t s0, int64_t s1, const int32_t* __restrict__ arcs,
+                           int* __restrict__ bad) {
   bool dup = false;
-  for (int64_t v = rlo + blockIdx.x; v < rhi; v += gridDim.x)
-    for (int64_t i = off[v] + 1 + threadIdx.x; i < off[v + 1]; i += blockDim.x)
-      dup |= arcs[i] == arcs[i - 1];
+  for (int64_t i = s0 + 1 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (arcs[i] != arcs[i - 1]) continue;
+    int64_t lo = rlo, hi = rhi;  // run holding slot i: last v with off[v] <= i
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= i) lo = mid; else hi = mid;
+    }
+    dup |= off[lo] < i;  // i - 1 in the same run
+  }
   if (dup) atomicExch(bad, 5);
 }
 
@@ -662,8 +672,8 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
     if (db.Current() != arcs + hbig)
       GS_CUDA(cudaMemcpyAsync(arcs + hbig, db.Current(), sizeof(int32_t) * (size_t)cnt,
                               cudaMemcpyDeviceToDevice, st));
-    k_run_dups<<<(unsigned)std::min<int64_t>(nseg, (int64_t)e->sms * 8), 256, 0, st>>>(
-        g.off, rbig, row_hi, arcs, d_bad);
+    k_run_dups<<<(unsigned)std::min<int64_t>(grid_for(cnt, 256), (int64_t)e->sms * 16), 256, 0,
+                 st>>>(g.off, rbig, row_hi, hbig, hend, arcs, d_bad);
     e->launches += 3;
     e->release(segoff);
     e->release(tmp);
