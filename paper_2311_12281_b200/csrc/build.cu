@@ -657,24 +657,47 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
   if (cnt > 0 && seg_tail) {
     // the long runs sorted as segments over the neighbour bits only (int32
     // keys, B bits) instead of one radix sort of 64-bit (run, neighbour) keys
+    // (batches of runs holding < 2^30 slots: the segmented sort counts items in int)
     const int B = bits_for(n - 1);
     const int64_t nseg = row_hi - rbig;
+    std::vector<int64_t> hoff(nseg + 1);
+    GS_CUDA(cudaMemcpyAsync(hoff.data(), g.off + rbig, sizeof(int64_t) * (size_t)(nseg + 1),
+                            cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    int64_t kBatch = (int64_t)1 << 30;
+    if (const char* v = getenv("GS_SEG_BATCH")) kBatch = std::max<int64_t>(1, atoll(v));  // tests
+    std::vector<int64_t> cut{0};  // batch boundaries (run indices); a batch holds >= 1 run
+    int64_t most = 0;
+    for (int64_t a = 0; a < nseg;) {
+      int64_t z = a + 1;
+      while (z < nseg && hoff[z + 1] - hoff[a] <= kBatch) ++z;
+      most = std::max(most, hoff[z] - hoff[a]);
+      cut.push_back(z);
+      a = z;
+    }
     int64_t* segoff = nullptr;
     int32_t* tmp = nullptr;
     GS_TRY(e->alloc_n(&segoff, nseg + 1));
-    GS_TRY(e->alloc_n(&tmp, cnt));
-    k_rebase<<<grid_for(nseg + 1, 256), 256, 0, st>>>(g.off + rbig, nseg + 1, hbig, segoff);
-    cub::DoubleBuffer<int32_t> db(arcs + hbig, tmp);
-    GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-      return cub::DeviceSegmentedRadixSort::SortKeys(t, b, db, cnt, nseg, segoff, segoff + 1, 0,
-                                                     B, st);
-    }));
-    if (db.Current() != arcs + hbig)
-      GS_CUDA(cudaMemcpyAsync(arcs + hbig, db.Current(), sizeof(int32_t) * (size_t)cnt,
-                              cudaMemcpyDeviceToDevice, st));
+    GS_TRY(e->alloc_n(&tmp, most));
+    for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
+      const int64_t a = cut[bi], z = cut[bi + 1];  // runs [a, z)
+      const int64_t base = hoff[a], items = hoff[z] - base;
+      k_rebase<<<grid_for(z - a + 1, 256), 256, 0, st>>>(g.off + rbig + a, z - a + 1, base,
+                                                          segoff);
+      cub::DoubleBuffer<int32_t> db(arcs + base, tmp);
+      GS_TRY(cub_call(e, [&](void* t, size_t& b) {
+        return cub::DeviceSegmentedRadixSort::SortKeys(t, b, db, (int)items, (int)(z - a), segoff,
+                                                       segoff + 1, 0, B, st);
+      }));
+      if (db.Current() != arcs + base)
+        GS_CUDA(cudaMemcpyAsync(arcs + base, db.Current(), sizeof(int32_t) * (size_t)items,
+                                cudaMemcpyDeviceToDevice, st));
+      e->launches += 2;
+    }
     k_run_dups<<<(unsigned)std::min<int64_t>(grid_for(cnt, 256), (int64_t)e->sms * 16), 256, 0,
                  st>>>(g.off, rbig, row_hi, hbig, hend, arcs, d_bad);
-    e->launches += 3;
+    e->launches++;
+    GS_CUDA(cudaStreamSynchronize(st));  // hoff / segoff reuse across batches is stream-ordered
     e->release(segoff);
     e->release(tmp);
   } else if (cnt > 0) {

@@ -237,3 +237,17 @@ def test_device_csr_invalid_runs_detected(monkeypatch, fused, deg):
                   edge_ids=base.edge_ids, edge_list=base.edge_list, orig_ids=base.orig_ids)
         with pytest.raises(ValueError):
             _device_csr_scan(g, 2, "0.5")
+
+
+@pytest.mark.parametrize("batch", ["5000", "1"])
+def test_hub_runs_sorted_in_batches(orc, monkeypatch, batch):
+    """The hub-run segmented sort split into many batches (large graphs need
+    batches below 2^31 items): same result, duplicates still caught."""
+    monkeypatch.setenv("GS_SEG_BATCH", batch)
+    n, e = _degree_class_graph(seed=7)
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    roles, cl = orc.serial_scan(c, 3, "0.1")
+    for r_roles, r_cl in (_run(g, 3, "0.1"), _device_csr_scan(g, 3, "0.1")):
+        np.testing.assert_array_equal(r_roles, roles)
+        np.testing.assert_array_equal(r_cl, cl)
