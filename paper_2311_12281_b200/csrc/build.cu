@@ -1031,6 +1031,52 @@ __device__ __forceinline__ int32_t fused_check(const int32_t* __restrict__ adj, 
   return v;
 }
 
+// W-lane segments of a warp each sort one run of <= W neighbours (register
+// bitonic network within the segment): 32 / W runs per round; `runs` is the
+// warp-uniform mask of the group's lanes whose vertex qualifies
+template <int W>
+__device__ __forceinline__ void segmented_runs(uint32_t runs, int lane, int64_t g0, int64_t myo,
+                                               int myd, int64_t myr,
+                                               const int32_t* __restrict__ adj,
+                                               const int32_t* __restrict__ rank,
+                                               const int64_t* __restrict__ noff,
+                                               int32_t* __restrict__ out, int64_t n, bool& b3,
+                                               bool& b4, bool& b5) {
+  const int seg = lane / W, sl = lane % W;
+  while (runs) {
+    uint32_t t = runs;
+    int src = -1;
+    for (int k = 0; k <= seg && t; ++k) {
+      const int b = __ffs(t) - 1;
+      t &= t - 1;
+      if (k == seg) src = b;
+    }
+    for (int k = 0; k < 32 / W && runs; ++k) runs &= runs - 1;  // consumed this round
+    const int sb = src < 0 ? 0 : src;
+    const int64_t ou = __shfl_sync(0xffffffffu, myo, sb);  // every lane shuffles
+    const int dsb = __shfl_sync(0xffffffffu, myd, sb);
+    const int64_t ru = __shfl_sync(0xffffffffu, myr, sb);
+    const int d = src < 0 ? 0 : dsb;
+    const int64_t u = g0 + sb;
+    int32_t x = kPad;
+    if (sl < d) x = rank[fused_check(adj, ou + sl, ou, n, u, b3, b4)];
+#pragma unroll
+    for (int k = 2; k <= W; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+        const bool up = (sl & k) == 0, low = (sl & j) == 0;
+        x = (low == up) ? min(x, y) : max(x, y);
+      }
+    }
+    const int32_t nx = __shfl_down_sync(0xffffffffu, x, 1);
+    if (sl < d) {
+      out[noff[ru] + sl] = x;
+      b5 |= sl + 1 < d && nx == x;
+    }
+  }
+}
+
 // warp per caller vertex with d <= 32 (lane i holds element i): register
 // bitonic network; d in (32, 511]: warp per vertex, bitonic in a 2 KB
 // shared-memory slice.  Longer runs are skipped (CTA kernels below).
@@ -1047,12 +1093,33 @@ __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ 
   int32_t* sbuf = buf + (threadIdx.x >> 5) * CAP;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   bool b3 = false, b4 = false, b5 = false;
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
-    const int64_t ou = off[u];
-    const int d = (int)(off[u + 1] - ou);
-    if (d == 0 || d >= kHeavyScatter) continue;
-    const int64_t ru = rank[u];
-    if (ru < row_lo || ru >= row_hi) continue;
+  // groups of 32 consecutive caller vertices per warp: runs of <= 8 are
+  // handled four at a time (8 lanes each: 4x the gathers in flight), the rest
+  // one by one
+  for (int64_t g0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; g0 < n;
+       g0 += nw * 32) {
+    const int64_t myu = g0 + lane;
+    int myd = 0;
+    int64_t myo = 0, myr = -1;
+    if (myu < n) {
+      myo = off[myu];
+      myd = (int)(off[myu + 1] - myo);
+      myr = rank[myu];
+      if (myr < row_lo || myr >= row_hi) myd = 0;
+    }
+    uint32_t rest = __ballot_sync(0xffffffffu, myd > 16 && myd < kHeavyScatter);
+    // runs of <= 8: four per round (8 lanes each), of 9..16: two per round
+    segmented_runs<8>(__ballot_sync(0xffffffffu, myd > 0 && myd <= 8), lane, g0, myo, myd, myr,
+                      adj, rank, noff, out, n, b3, b4, b5);
+    segmented_runs<16>(__ballot_sync(0xffffffffu, myd > 8 && myd <= 16), lane, g0, myo, myd,
+                       myr, adj, rank, noff, out, n, b3, b4, b5);
+    while (rest) {
+    const int src = __ffs(rest) - 1;
+    rest &= rest - 1;
+    const int64_t u = g0 + src;
+    const int64_t ou = __shfl_sync(0xffffffffu, myo, src);
+    const int d = __shfl_sync(0xffffffffu, myd, src);
+    const int64_t ru = __shfl_sync(0xffffffffu, myr, src);
     int32_t* o = out + noff[ru];
     if (d <= 32) {
       int32_t x = kPad;
@@ -1083,6 +1150,7 @@ __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ 
         b5 |= i + 1 < d && sbuf[i + 1] == sbuf[i];
       }
       __syncwarp();
+    }
     }
   }
   if (b3) atomicExch(bad, 3);
