@@ -65,7 +65,9 @@ __device__ __forceinline__ bool b_needed(const SimParams& P, int64_t b) {
 // Does edge (a, b) need a decision in this mode?
 __device__ __forceinline__ bool edge_needed(const SimParams& P, int64_t e, int32_t a,
                                             int32_t b) {
-  if (P.sim[e] != SIM_UNKNOWN) return false;
+  // identify visits every oriented edge once (by its high endpoint), so its
+  // status is still unknown there: no load
+  if (P.mode != MODE_IDENTIFY && P.sim[e] != SIM_UNKNOWN) return false;
   const uint8_t ra = ld_role(P.role, a), rb = ld_role(P.role, b);
   switch (P.mode) {
     case MODE_IDENTIFY:  // Alg. 2 line 2: defer if both roles are known
