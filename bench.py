@@ -173,7 +173,7 @@ def run_reference(args):
     csr = orc.PlainCSR(n, edges)
     prep = time.time() - t0
     m = csr.m
-    per_step = max(2.0, min(20.0, 150.0 / (args.steps + args.warmup)))
+    per_step = min(args.cpu_seconds, max(2.0, min(20.0, 150.0 / (args.steps + args.warmup))))
     vals = []
     tot_edges = 0
     tot_secs = 0.0

@@ -190,3 +190,19 @@ def test_stats_struct_matches_header():
         decl = re.sub(r"\[.*?\]", "", decl)
         names += [v.strip() for v in decl.split(None, 1)[1].split(",")]
     assert names == [f[0] for f in _lib.GsStats._fields_]
+
+
+def test_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the CPU port of the reference's hot loop the
+    driver times beside the engine) prints one JSON line, no GPU needed."""
+    import json
+    import subprocess
+    import sys
+
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--scale", "11", "--steps", "1", "--warmup", "3", "--cpu-seconds", "0.5"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["unit"] == "edges/s"
+    assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
