@@ -686,19 +686,15 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
 
 template <int NT, bool GTAB>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
-                       uint32_t tcap, int qi, int chunk) {
+                       uint32_t tcap, int qi, int chunk, int64_t dcls, cudaStream_t st) {
   if (rhi <= rlo) return GS_OK;
   size_t smem =
       (size_t)((P.bm_words + 4 + 3) & ~3u) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
   // b's sketch levels in shared memory when they fit (else folded from global)
   int64_t skw = 0;
   if (P.sk != nullptr) {
-    int64_t dhi = 0;
-    GS_CUDA(cudaMemcpyAsync(&dhi, e->g.off + rhi, 8, cudaMemcpyDeviceToHost, e->stream));
-    int64_t dlo = 0;
-    GS_CUDA(cudaMemcpyAsync(&dlo, e->g.off + rhi - 1, 8, cudaMemcpyDeviceToHost, e->stream));
-    GS_CUDA(cudaStreamSynchronize(e->stream));
-    const int64_t want = 2 * sk_words(dhi - dlo, P.sk_lk);  // the class's largest degree
+    // dcls bounds the class's degrees (no device read, no host sync)
+    const int64_t want = 2 * sk_words(dcls, P.sk_lk);
     const int64_t room = ((int64_t)e->smem_optin - 1024 - (int64_t)smem) / 4;  // static smem
     if (want <= room) {
       skw = want;
@@ -715,14 +711,15 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   int64_t grid = (int64_t)occ * e->sms;
   if (grid > rhi - rlo) grid = rhi - rlo;
   if (GTAB && grid > e->sms * 2) grid = e->sms * 2;
-  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, tcap, qi, chunk, P.hub_lo,
-                                                P.bm_words, skw);
+  kern<<<(unsigned)grid, NT, smem, st>>>(P, rlo, rhi, tcap, qi, chunk, P.hub_lo, P.bm_words,
+                                         skw);
   e->launches++;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
 
-static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi, int qi) {
+static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi, int qi,
+                       cudaStream_t st) {
   if (rhi <= rlo) return GS_OK;
   constexpr int NT = 256;
   const size_t smem = (size_t)(NT / 32) * kWarpWords * 4;
@@ -735,7 +732,7 @@ static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   int64_t grid = (int64_t)occ * e->sms;
   const int64_t nw = (rhi - rlo + NT / 32 - 1) / (NT / 32);
   if (grid > nw) grid = nw;
-  kern<<<(unsigned)grid, NT, smem, e->stream>>>(P, rlo, rhi, qi);
+  kern<<<(unsigned)grid, NT, smem, st>>>(P, rlo, rhi, qi);
   e->launches++;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
@@ -849,6 +846,17 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   }
   GS_CUDA(cudaMemsetAsync(s.wq, 0, 8 * sizeof(int32_t), e->stream));
   const int64_t* rc = g.rclass;
+  // largest degree of the large / medium classes (sizes their sketch levels):
+  // one host sync here instead of one per launch
+  int64_t dcls[2] = {0, 0};
+  {
+    int64_t o[4] = {0, 0, 0, 0};
+    if (rc[4] > rc[3]) GS_CUDA(cudaMemcpyAsync(o, g.off + rc[4] - 1, 16, cudaMemcpyDeviceToHost, e->stream));
+    if (rc[3] > rc[2]) GS_CUDA(cudaMemcpyAsync(o + 2, g.off + rc[3] - 1, 16, cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    dcls[0] = o[1] - o[0];
+    dcls[1] = o[3] - o[2];
+  }
   // huge b first (longest work items), with an L2-resident table per CTA
   const int64_t rhuge = rc[4];
   if (g.n > rhuge) {
@@ -856,14 +864,15 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     const int64_t nblk = (int64_t)e->sms * 2;
     GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
     P.gtab_stride = 4 * tcap_g;
-    GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024)));
+    GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, g.dmax,
+                                     e->stream)));
   }
   // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB) + cuckoo table
   // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
   // per candidate of a chunk); the small class runs warp-per-b
-  GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024)));
-  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024)));
-  GS_TRY(launch_warp(e, P, rc[1], rc[2], 1));
+  GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
+  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024, dcls[1], e->stream)));
+  GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
