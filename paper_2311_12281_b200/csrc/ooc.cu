@@ -770,7 +770,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     size_t fixed = e->live + (size_t)nslab * 16 * (size_t)tcap_g + (2u << 20);
     size_t avail = e->cap ? (e->cap > fixed ? e->cap - fixed : 0) : ((size_t)1 << 30);
     // sketch resolution as in sim.cu (k = 2^sk_lk bits per neighbour; -1: off)
-    int sk_lk = sqrt(eps.ratio) >= 0.45 ? 2 : 3;
+    int sk_lk = sqrt(eps.ratio) >= 0.33 ? 2 : 3;
     int64_t sk_dmin = 48;
     if (const char* v = getenv("GS_SKETCH")) {
       const int k = atoi(v);
