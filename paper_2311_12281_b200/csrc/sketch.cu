@@ -47,20 +47,46 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
   const int lane = threadIdx.x & 31;
   uint32_t* s = sm[threadIdx.x >> 5];
   const int64_t nw = ((int64_t)gridDim.x * NT) >> 5;
-  for (int64_t v = r0 + ((blockIdx.x * (int64_t)NT + threadIdx.x) >> 5); v < r1; v += nw) {
-    const int64_t o = off[v], d = off[v + 1] - o;
-    const int64_t W = sk_words(d, lk);
-    const uint32_t mask = (uint32_t)(W * 32 - 1);
-    for (int64_t j = lane; j < W; j += 32) s[j] = 0u;
-    __syncwarp();
-    for (int64_t i = lane; i < d; i += 32) {
-      const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-      atomicOr(&s[h >> 5], 1u << (h & 31));
+  // two neighbouring ranks per round (similar degrees): rows of <= WMAX/2
+  // words are built by the two half-warps side by side, longer ones in turn
+  for (int64_t v0 = r0 + 2 * ((blockIdx.x * (int64_t)NT + threadIdx.x) >> 5); v0 < r1;
+       v0 += 2 * nw) {
+    const bool two = v0 + 1 < r1;
+    const int64_t dlast = two ? off[v0 + 2] - off[v0 + 1] : off[v0 + 1] - off[v0];
+    if (two && sk_words(dlast, lk) <= WMAX / 2) {  // degrees ascend: both rows fit
+      const int hf = lane >> 4, hl = lane & 15;
+      const int64_t v = v0 + hf;
+      const int64_t o = off[v], d = off[v + 1] - o;
+      const int64_t W = sk_words(d, lk);
+      const uint32_t mask = (uint32_t)(W * 32 - 1);
+      uint32_t* t = s + hf * (WMAX / 2);
+      for (int64_t j = hl; j < W; j += 16) t[j] = 0u;
+      __syncwarp();
+      for (int64_t i = hl; i < d; i += 16) {
+        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+        atomicOr(&t[h >> 5], 1u << (h & 31));
+      }
+      __syncwarp();
+      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
+      for (int64_t j = hl; j < W; j += 16) out[j] = t[j];
+      __syncwarp();
+      continue;
     }
-    __syncwarp();
-    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
-    for (int64_t j = lane; j < W; j += 32) out[j] = s[j];
-    __syncwarp();
+    for (int64_t v = v0; v < v0 + 2 && v < r1; ++v) {
+      const int64_t o = off[v], d = off[v + 1] - o;
+      const int64_t W = sk_words(d, lk);
+      const uint32_t mask = (uint32_t)(W * 32 - 1);
+      for (int64_t j = lane; j < W; j += 32) s[j] = 0u;
+      __syncwarp();
+      for (int64_t i = lane; i < d; i += 32) {
+        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+        atomicOr(&s[h >> 5], 1u << (h & 31));
+      }
+      __syncwarp();
+      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
+      for (int64_t j = lane; j < W; j += 32) out[j] = s[j];
+      __syncwarp();
+    }
   }
 }
 
