@@ -16,6 +16,7 @@ additionally bit-exact against ``serial_scan``.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, field
 from enum import Enum
 from fractions import Fraction
@@ -304,25 +305,43 @@ def scan_edges(n: int, edges: np.ndarray, mu: int, epsilon: EpsilonLike,
     return ClusteringResult(n, roles, cids, orig), stats_from_native(st, n, m, 1)
 
 
-_loaded: dict = {}
+# check_sim has its own engine per host thread (scan_in_memory loads other
+# graphs into the scan engine) and remembers the graph it holds by identity:
+# the cache keeps the graph object and the exact arrays it loaded alive, so
+# neither an address reused after a free nor a temporary conversion can make a
+# different graph look loaded.
+_check_tls = threading.local()
 
 
-def _ensure_loaded(eng: _lib.Engine, g) -> None:
+def _check_engine(g) -> _lib.Engine:
     n, m, off, adj = graph_arrays(g)
-    key = (n, m, off.ctypes.data, adj.ctypes.data)
-    if _loaded.get(id(eng)) != key:
-        lib = _lib.load()
-        _lib.check(lib.gs_engine_load_csr(eng.handle, n, m, off.ctypes.data, adj.ctypes.data, 0))
-        _loaded[id(eng)] = key
+    eng = getattr(_check_tls, "engine", None)
+    if eng is None:
+        eng = _check_tls.engine = _lib.Engine()
+        _check_tls.held = None
+    held = _check_tls.held
+    # Same graph object (held alive, so its id cannot be reused) and the same
+    # buffers (the held arrays keep them alive, so their addresses cannot be
+    # reused either): the engine already holds this graph.
+    if (held is None or held[0] is not g or held[1].ctypes.data != off.ctypes.data
+            or held[2].ctypes.data != adj.ctypes.data):
+        _check_tls.held = None
+        _lib.check(_lib.load().gs_engine_load_csr(eng.handle, n, m, off.ctypes.data,
+                                                  adj.ctypes.data, 0))
+        _check_tls.held = (g, off, adj)
+    return eng
 
 
 def check_sim(g, u: int, v: int, epsilon: EpsilonLike) -> bool:
-    """scan.py:241-258: exact similarity test of an existing edge (device)."""
+    """scan.py:241-258: exact similarity test of an existing edge (device).
+    Out-of-range ids raise IndexError (edge_index, graph.py:268-269); u == v
+    and non-adjacent pairs raise ValueError."""
     f = epsilon_fraction(epsilon)
-    if not (0 <= u < g.n and 0 <= v < g.n) or u == v:
+    if not (0 <= u < g.n and 0 <= v < g.n):
+        raise IndexError(f"vertex id out of range: ({u}, {v})")
+    if u == v:
         raise ValueError(f"({u}, {v}) is not an edge")
-    eng = _lib.thread_engine()
-    _ensure_loaded(eng, g)
+    eng = _check_engine(g)
     uu = np.array([u], dtype=np.int32)
     vv = np.array([v], dtype=np.int32)
     out = np.empty(1, dtype=np.int8)
@@ -534,14 +553,15 @@ def classify_hub_outlier(g, st: ClusterState, *, workers: int = 1,
 
 def resolve_roles_from_bounds(st: ClusterState, mu: int, strict: bool = False) -> bool:
     """scan.py:390-412 over the host snapshot: Core if lower >= mu, NonCore if
-    upper < mu; True when no role is left open (``strict`` raises instead)."""
+    upper < mu; True when some role is still open, as in the reference
+    (``strict`` raises instead)."""
     open_ = st.role == ROLE_UNKNOWN
     st.role[open_ & (st.lower >= mu)] = ROLE_CORE
     st.role[open_ & (st.lower < mu) & (st.upper < mu)] = ROLE_NONCORE
     left = int(np.count_nonzero(st.role == ROLE_UNKNOWN))
     if left and strict:
         raise RuntimeError(f"{left} vertices have unresolved roles")
-    return left == 0
+    return left > 0
 
 
 def _chase(parent, u: int) -> int:

@@ -111,7 +111,7 @@ def test_resolve_roles_from_bounds_and_build_result_errors():
     st = gs.init_vertex_state(3, [4, 1, 4], m=0, with_sim=False)
     st.lower[:] = [5, 1, 2]
     st.upper[:] = [5, 2, 6]
-    assert not gs.resolve_roles_from_bounds(st, 3)
+    assert gs.resolve_roles_from_bounds(st, 3)  # vertex 2 still open (scan.py:390-412)
     assert list(st.role) == [ROLE_CORE, ROLE_NONCORE, 0]
     with pytest.raises(RuntimeError):
         gs.resolve_roles_from_bounds(st, 3, strict=True)
