@@ -186,6 +186,24 @@ static int64_t lower_bound_i32(const int32_t* a, int64_t lo, int64_t hi, int32_t
   return lo;
 }
 
+typedef struct eid_ctx {
+  const int64_t* off; const int32_t* adj; const int32_t* el; int32_t* eid;
+} eid_ctx;
+
+/* Eid by binary search of each endpoint in the other's run (graph.py:233-240);
+ * every slot is written by exactly one edge, so edges run in parallel. */
+static void eid_body(int64_t lo, int64_t hi, void* p, int tid) {
+  (void)tid;
+  eid_ctx* c = (eid_ctx*)p;
+  for (int64_t e = lo; e < hi; ++e) {
+    int32_t a = c->el[2 * e], b = c->el[2 * e + 1];
+    int64_t sa = lower_bound_i32(c->adj, c->off[a], c->off[a + 1], b);
+    int64_t sb = lower_bound_i32(c->adj, c->off[b], c->off[b + 1], a);
+    c->eid[sa] = (int32_t)e;
+    c->eid[sb] = (int32_t)e;
+  }
+}
+
 int orc_build_graph(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev,
                     int64_t* offsets, int32_t* adjacency, int32_t* edge_ids,
                     int32_t* edge_list) {
@@ -231,13 +249,8 @@ int orc_build_graph(int64_t n, int64_t m, const int32_t* eu, const int32_t* ev,
       }
     }
   }
-  for (int64_t e = 0; e < m; ++e) {   /* graph.py:233-240 */
-    int32_t a = edge_list[2 * e], b = edge_list[2 * e + 1];
-    int64_t sa = lower_bound_i32(adjacency, offsets[a], offsets[a + 1], b);
-    int64_t sb = lower_bound_i32(adjacency, offsets[b], offsets[b + 1], a);
-    edge_ids[sa] = (int32_t)e;
-    edge_ids[sb] = (int32_t)e;
-  }
+  eid_ctx ec = {offsets, adjacency, edge_list, edge_ids};  /* graph.py:233-240 */
+  par_for(m, 4096, 0, eid_body, &ec);
   free(deg);
   return 0;
 }
@@ -309,16 +322,106 @@ static int32_t uf_find(int32_t* p, int32_t x) {
   return x;
 }
 
+/* Common-neighbour counts of every edge (edge_list order) by marking instead
+ * of merging: per high endpoint b (the larger (degree, id) side, graph.py:226)
+ * N(b) is set in a thread-private bitmap of n bits and every lower neighbour
+ * a counts N(a) against it.  Same numbers as merge_common (checked against it
+ * in tests/test_oracle_golden.py); sum_k min(d) work instead of sum_k (da+db),
+ * which is what makes R-MAT s24 (sum d^2 = 3.6e12) a minutes-long check. */
+typedef struct marks_ctx {
+  const int64_t* off; const int32_t* adj; const int32_t* eid; int32_t* out;
+  uint64_t** bits;
+} marks_ctx;
+
+static void marks_body(int64_t lo, int64_t hi, void* p, int tid) {
+  marks_ctx* c = (marks_ctx*)p;
+  uint64_t* bm = c->bits[tid];
+  for (int64_t b = lo; b < hi; ++b) {
+    int64_t b0 = c->off[b], b1 = c->off[b + 1], db = b1 - b0;
+    int any = 0;
+    for (int64_t s = b0; s < b1; ++s) {
+      int32_t a = c->adj[s];
+      int64_t da = c->off[a + 1] - c->off[a];
+      if (da < db || (da == db && a < b)) { any = 1; break; }
+    }
+    if (!any) continue;
+    for (int64_t s = b0; s < b1; ++s) { uint32_t w = (uint32_t)c->adj[s]; bm[w >> 6] |= 1ull << (w & 63); }
+    for (int64_t s = b0; s < b1; ++s) {
+      int32_t a = c->adj[s];
+      int64_t a0 = c->off[a], a1 = c->off[a + 1], da = a1 - a0;
+      if (!(da < db || (da == db && a < b))) continue;
+      int64_t cm = 0;
+      for (int64_t i = a0; i < a1; ++i) {
+        uint32_t w = (uint32_t)c->adj[i];
+        cm += (int64_t)((bm[w >> 6] >> (w & 63)) & 1u);
+      }
+      c->out[c->eid[s]] = (int32_t)cm;
+    }
+    for (int64_t s = b0; s < b1; ++s) { uint32_t w = (uint32_t)c->adj[s]; bm[w >> 6] = 0; }
+  }
+}
+
+void orc_edge_commons_marked(int64_t n, int64_t m, const int64_t* offsets,
+                             const int32_t* adjacency, const int32_t* edge_ids,
+                             int32_t* commons) {
+  (void)m;
+  int threads = orc_max_threads();
+  if (threads > 256) threads = 256;
+  uint64_t* bits[256];
+  size_t words = (size_t)((n + 63) / 64 + 1);
+  for (int t = 0; t < threads; ++t) bits[t] = (uint64_t*)calloc(words, sizeof(uint64_t));
+  marks_ctx c = {offsets, adjacency, edge_ids, commons, bits};
+  par_for(n, 256, threads, marks_body, &c);
+  for (int t = 0; t < threads; ++t) free(bits[t]);
+}
+
+typedef struct thr_ctx {
+  const int64_t* off; const int32_t* el; const int32_t* cm; uint8_t* sim; orc_eps2 e;
+} thr_ctx;
+
+static void thr_body(int64_t lo, int64_t hi, void* p, int tid) {
+  (void)tid;
+  thr_ctx* c = (thr_ctx*)p;
+  for (int64_t k = lo; k < hi; ++k) {
+    int32_t u = c->el[2 * k], v = c->el[2 * k + 1];
+    c->sim[k] = (uint8_t)is_similar(c->cm[k], c->off[u + 1] - c->off[u],
+                                    c->off[v + 1] - c->off[v], c->e);
+  }
+}
+
+static int serial_scan_core(int64_t n, int64_t m, const int64_t* off, const int32_t* adj,
+                            const int32_t* el, int32_t mu, uint8_t* similar,
+                            uint8_t* role_out, int32_t* cluster_out);
+
 int orc_serial_scan(int64_t n, int64_t m, const int64_t* off,
                     const int32_t* adj, const int32_t* el, int32_t mu,
                     orc_eps2 eps2, uint8_t* role_out, int32_t* cluster_out) {
   if (mu < 2) return -1;
   uint8_t* similar = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
-  int64_t* simcnt = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
   {                                               /* oracle.py:118-127 */
     commons_ctx cc = {off, adj, el, NULL, similar, eps2};
     par_for(m, 1024, 0, commons_body, &cc);
   }
+  return serial_scan_core(n, m, off, adj, el, mu, similar, role_out, cluster_out);
+}
+
+/* serial_scan with the common-neighbour counts given (one count pass serves
+ * every (eps, mu) of a sweep); identical output to orc_serial_scan. */
+int orc_serial_scan_commons(int64_t n, int64_t m, const int64_t* off,
+                            const int32_t* adj, const int32_t* el, const int32_t* commons,
+                            int32_t mu, orc_eps2 eps2, uint8_t* role_out,
+                            int32_t* cluster_out) {
+  if (mu < 2) return -1;
+  uint8_t* similar = (uint8_t*)malloc((size_t)(m > 0 ? m : 1));
+  thr_ctx tc = {off, el, commons, similar, eps2};
+  par_for(m, 4096, 0, thr_body, &tc);
+  return serial_scan_core(n, m, off, adj, el, mu, similar, role_out, cluster_out);
+}
+
+static int serial_scan_core(int64_t n, int64_t m, const int64_t* off, const int32_t* adj,
+                            const int32_t* el, int32_t mu, uint8_t* similar,
+                            uint8_t* role_out, int32_t* cluster_out) {
+  int64_t* simcnt = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
   for (int64_t k = 0; k < m; ++k)
     if (similar[k]) { simcnt[el[2 * k]]++; simcnt[el[2 * k + 1]]++; }
   uint8_t* core = (uint8_t*)malloc((size_t)(n > 0 ? n : 1));

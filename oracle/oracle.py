@@ -73,6 +73,10 @@ def load():
     lib.orc_sample_eval_slots.argtypes = [I64, P, P, Eps2, P, I64, ctypes.c_int,
                                           ctypes.POINTER(I64), ctypes.POINTER(I64)]
     lib.orc_sample_eval_slots.restype = ctypes.c_double
+    lib.orc_edge_commons_marked.argtypes = [I64, I64, P, P, P, P]
+    lib.orc_edge_commons_marked.restype = None
+    lib.orc_serial_scan_commons.argtypes = [I64, I64, P, P, P, P, ctypes.c_int32, Eps2, P, P]
+    lib.orc_serial_scan_commons.restype = ctypes.c_int
     lib.orc_max_threads.argtypes = []
     lib.orc_max_threads.restype = ctypes.c_int
     lib.orc_set_threads.argtypes = [ctypes.c_int]
@@ -148,12 +152,30 @@ def commons(g: CSR) -> np.ndarray:
     return out
 
 
-def serial_scan(g: CSR, mu: int, epsilon) -> tuple[np.ndarray, np.ndarray]:
-    """Canonical (roles {1,3,5,6}, cluster ids) of oracle.serial_scan."""
+def commons_marked(g: CSR) -> np.ndarray:
+    """Same counts as commons() (oracle.py:27-44), by per-vertex marking:
+    sum of min degrees instead of sum of degree pairs (large-scale checks)."""
+    out = np.empty(g.m, dtype=np.int32)
+    load().orc_edge_commons_marked(g.n, g.m, g.vertex_offsets.ctypes.data,
+                                   g.adjacency.ctypes.data, g.edge_ids.ctypes.data,
+                                   out.ctypes.data)
+    return out
+
+
+def serial_scan(g: CSR, mu: int, epsilon, commons: np.ndarray | None = None
+                ) -> tuple[np.ndarray, np.ndarray]:
+    """Canonical (roles {1,3,5,6}, cluster ids) of oracle.serial_scan.  With
+    ``commons`` (per edge_list edge) the count pass is skipped."""
     roles = np.empty(g.n, dtype=np.uint8)
     cl = np.empty(g.n, dtype=np.int32)
-    rc = load().orc_serial_scan(g.n, g.m, *g._p(), mu, eps2(epsilon), roles.ctypes.data,
-                                cl.ctypes.data)
+    if commons is not None:
+        cm = np.ascontiguousarray(commons, dtype=np.int32)
+        assert cm.shape == (g.m,)
+        rc = load().orc_serial_scan_commons(g.n, g.m, *g._p(), cm.ctypes.data, mu,
+                                            eps2(epsilon), roles.ctypes.data, cl.ctypes.data)
+    else:
+        rc = load().orc_serial_scan(g.n, g.m, *g._p(), mu, eps2(epsilon), roles.ctypes.data,
+                                    cl.ctypes.data)
     if rc != 0:
         raise ValueError("serial_scan failed")
     return roles, cl
