@@ -29,6 +29,8 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import glob
+import hashlib
 import json
 import os
 import statistics
@@ -56,9 +58,13 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--input", choices=["csr", "edges"], default="csr",
-                    help="csr: scan_in_memory's call on the reference CSR (default); edges: "
-                         "build from the device edge list inside the step (large scales)")
+    ap.add_argument("--input", choices=["csr", "edges"], default=None,
+                    help="csr: scan_in_memory's call on the reference CSR (default below "
+                         "scale 27); edges: build from the device edge list inside the step "
+                         "(default from scale 27: the CSR copy would not fit beside the engine)")
+    ap.add_argument("--python-ref-seconds", type=float, default=8.0,
+                    help="seconds of the reference's own Python _eval_edge (baseline/_ref) "
+                         "timed on sampled edges of the same graph (0: skip)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU phase path even with one process")
     return ap.parse_args()
@@ -69,6 +75,101 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: re-launch this command as N
+    ranks (one per GPU, NCCL) through torch.distributed.run.  Fails loudly when
+    fewer GPUs are visible -- never falls back to fewer ranks."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}; "
+              "refusing to run fewer ranks", file=sys.stderr)
+        return 2
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator log (nranks) for the record
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
+def source_hash() -> str:
+    """Hash of the engine's sources: a traffic record taken on other sources is stale."""
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2311_12281_b200", "csrc", "*.cu")) +
+                   glob.glob(os.path.join(ROOT, "paper_2311_12281_b200", "csrc", "*.cuh")))
+    for f in files + [os.path.join(ROOT, "include", "gscan.h")]:
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def workload_config(args, n: int, m: int) -> dict:
+    """The `config` object, identical in both arms (the driver compares them)."""
+    return {
+        "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, eps={args.eps} "
+                    f"mu={args.mu} (BASELINE configs[1])" if args.scale == 24 else
+                    f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, eps={args.eps} "
+                    f"mu={args.mu}",
+        "n": n, "m": m, "seed": args.seed,
+        "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
+        "step": "one clustering call (scan_in_memory, scan.py:965-982): degree-rank relabel "
+                "+ identify + cluster + classify, roles and cluster ids out",
+    }
+
+
+def python_reference_rate(csr, eps, seconds: float):
+    """The reference's own hot loop -- graphscan.scan._eval_edge from
+    baseline/_ref, unmodified -- on uniformly sampled edges of the same graph,
+    one core (the GIL), for about `seconds`.  None when baseline/_ref is absent."""
+    import random
+    from array import array
+
+    import numpy as np
+
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if seconds <= 0 or not os.path.isdir(os.path.join(ref, "graphscan")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        from graphscan.scan import _epsilon_squared, _eval_edge
+    except ImportError:
+        return None
+    off_np = np.asarray(csr.vertex_offsets, dtype=np.int64)
+    adj = array("i", np.asarray(csr.adjacency, dtype=np.int32).tobytes())
+    p, q = _epsilon_squared(eps)
+    rng = random.Random(0)
+    n_edges = probes = 0
+    secs = 0.0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        slot = rng.randrange(len(adj))
+        v = adj[slot]
+        u = int(np.searchsorted(off_np, slot, side="right") - 1)
+        ou, ov = int(off_np[u]), int(off_np[v])
+        du, dv = int(off_np[u + 1]) - ou, int(off_np[v + 1]) - ov
+        if (dv, v) < (du, u):  # the low-(degree, id) side probes (scan.py:252-254)
+            ou, du, ov, dv = ov, dv, ou, du
+        t1 = time.perf_counter()
+        _, pr = _eval_edge(adj, ou, ou + du, ov, ov + dv, p, q)
+        secs += time.perf_counter() - t1  # the reference call alone, not the sampling
+        probes += pr
+        n_edges += 1
+    return {"edges_per_s": n_edges / secs, "probes_per_s": probes / secs, "cores": 1,
+            "sample": f"{n_edges} uniformly sampled edges in {secs:.1f}s, {probes} probes: "
+                      "graphscan.scan._eval_edge (scan.py:203-233) from baseline/_ref, "
+                      "unmodified, one core (GIL)",
+            "ms_per_step_extrapolated": 1000.0 * csr.m * secs / max(n_edges, 1)}
 
 
 def peaks():
@@ -184,6 +285,7 @@ def run_reference(args):
             tot_edges += cnt
             tot_secs += secs
     value = tot_edges / tot_secs
+    pyref = python_reference_rate(csr, args.eps, args.python_ref_seconds)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -197,15 +299,18 @@ def run_reference(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "int32",
-        "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05), generated on the host",
-        "config": {"workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
-                   f"eps={args.eps} mu={args.mu}", "n": n, "m": m,
-                   "parallelism": f"{threads} host threads"},
+        "data": "synthetic R-MAT (Graph500 a,b,c,d=.57,.19,.19,.05, scrambled ids), generated "
+                "on the host by the same counter-based generator as the device",
+        "config": workload_config(args, n, m),
+        "parallelism": f"{threads} host threads",
         "cpu_baseline": {
             "value": value, "unit": "edges/s", "cores": threads, "kind": "port",
-            "sample": f"{tot_edges} uniformly sampled edges per {args.steps} steps; reference "
-                      f"_eval_edge (scan.py:203-233) binary-search probing, C port in oracle/; "
-                      f"ms_per_step extrapolates the full m={m} edges",
+            "sample": f"{tot_edges} uniformly sampled edges over {args.steps} timed steps; the "
+                      f"reference's hot loop _eval_edge (scan.py:203-233, 99.5% of its runtime) "
+                      f"restated in C (oracle/), all {threads} host threads; value and "
+                      f"ms_per_step are EXTRAPOLATED from the sample to all m={m} edges "
+                      "(the full reference call would take days at this scale)",
+            "reference_python": pyref,
         },
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -328,6 +433,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step_device()
     sim_ms, ident_ms, launches, phase = [], [], 0, {}
+    cls_ms = [[] for _ in range(6)]
     barrier()
     with ClockSampler(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
@@ -336,6 +442,8 @@ def run_ours(args):
         for _ in range(args.steps):
             step_device()
             ident_ms.append(st.phase_ms[_lib.GS_PH_IDENTIFY])
+            for c in range(6):
+                cls_ms[c].append(st.phase_ms[_lib.GS_PH_K_PREP + c])
             launches += int(st.kernel_launches)
         e1.record(stream)
         barrier()
@@ -345,18 +453,38 @@ def run_ours(args):
     for k in range(_lib.GS_PH_COUNT):
         phase[k] = round(st.phase_ms[k], 3)
 
-    # ---- roofline of the dominant kernel (similarity pass of identify)
+    # ---- roofline: identify-pass kernel classes (algorithmic bytes counted on
+    # the device, per class, over the class's own CUDA-event time)
     peak, peak_src = peaks()
-    w_sim = stats.extra["hbm_bytes_alg"]
     t_sim = statistics.median(ident_ms) / 1000.0
-    achieved = w_sim / t_sim / 1e9 if t_sim > 0 else 0.0
-    traffic = None
+    kernels = []
+    for c in range(6):
+        t = statistics.median(cls_ms[c]) / 1000.0
+        b = int(st.kernel_bytes[c])
+        kernels.append({"kernel": _lib.KERNEL_CLASSES[c], "ms": round(t * 1000, 3), "bytes": b,
+                        "achieved_gbs": b / t / 1e9 if t > 0 else None,
+                        "frac": b / t / 1e9 / peak if t > 0 else None})
+    dom = max(range(6), key=lambda c: kernels[c]["ms"])
+    pass_bytes = sum(k["bytes"] for k in kernels)
+    traffic, traffic_note = None, "no ncu record for these sources (tools/ncu_traffic.py)"
     tf = os.path.join(ROOT, "profiles", "sim_traffic.json")
     if os.path.exists(tf):
         with open(tf) as fh:
             td = json.load(fh)
-        if td.get("config") == f"s{args.scale} eps={args.eps} mu={args.mu}":
-            traffic = td.get("dram_bytes_per_step")
+        want = f"s{args.scale} eps={args.eps} mu={args.mu}"
+        if td.get("source_hash") != source_hash() or td.get("config") != want:
+            traffic_note = (f"stale: profiles/sim_traffic.json is for sources "
+                            f"{td.get('source_hash')} / {td.get('config')}, not "
+                            f"{source_hash()} / {want}")
+        else:
+            tk = td.get("classes", {}).get(str(dom))
+            traffic = tk.get("dram_bytes") if tk else None
+            traffic_note = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of the {dom}-th "
+                            f"class's launches, {td.get('when')}, sources {td.get('source_hash')}")
+            for c in range(6):
+                tc = td.get("classes", {}).get(str(c))
+                if tc:
+                    kernels[c]["dram_bytes_ncu"] = tc.get("dram_bytes")
 
     # ---- the edge-list -> CSR build, timed on its own (build_graph's job)
     eb = []
@@ -397,7 +525,42 @@ def run_ours(args):
         assert torch.equal(role_h, role_d.cpu()) and torch.equal(clus_h, clus_d.cpu())
         e2e = {"value": m / (ms_e2e / 1000.0), "unit": "edges/s",
                "ms_per_step": ms_e2e, "h2d_bytes_per_step": 8 * (n + 1) + 8 * m,
-               "d2h_bytes_per_step": 5 * n}
+               "d2h_bytes_per_step": 5 * n,
+               "input": "the reference Graph's CSR in pinned host memory (scan_in_memory's input)"}
+        del off_h, adj_h
+
+    # ---- e2e from a pinned (m, 2) edge array (SURVEY 8(d)'s definition):
+    # build_graph + scan_in_memory in one call (gs_engine_load_edges from host)
+    if not args.no_e2e and shard is None:
+        uv_h = torch.empty(2 * m, dtype=torch.int32, pin_memory=True)
+        uv_h.copy_(uv)
+        role_h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        clus_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        st3 = _lib.GsStats()
+
+        def step_edges_host():
+            _lib.check(lib.gs_engine_load_edges(eng.handle, n, m, uv_h.data_ptr(), 0))
+            scan_call(role_h.data_ptr(), clus_h.data_ptr(), 0, st3)
+
+        for _ in range(max(1, args.warmup)):
+            step_edges_host()
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_edges_host()
+        e1.record(stream)
+        barrier()
+        ms_e = e0.elapsed_time(e1) / args.steps
+        assert torch.equal(role_h, role_d.cpu()) and torch.equal(clus_h, clus_d.cpu())
+        ee = {"value": m / (ms_e / 1000.0), "unit": "edges/s", "ms_per_step": ms_e,
+              "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": 5 * n,
+              "input": "normalised (m, 2) int32 edge array in pinned host memory (build_graph "
+                       "+ scan_in_memory)"}
+        if e2e is None:
+            e2e = ee
+        else:
+            e2e["from_edge_array"] = ee
+        del uv_h
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -410,7 +573,9 @@ def run_ours(args):
         cpu = {"value": count / secs, "unit": "edges/s", "cores": threads, "kind": "port",
                "sample": f"{count} uniformly sampled edges of the same s{args.scale} graph, "
                          f"reference _eval_edge (scan.py:203-233) C port, {secs:.1f}s; "
-                         f"{probes / max(count, 1):.0f} probes/edge"}
+                         f"{probes / max(count, 1):.0f} probes/edge; edges/s extrapolates the "
+                         f"sample to the whole call",
+               "reference_python": python_reference_rate(csr, args.eps, args.python_ref_seconds)}
 
     if rank == 0:
         line = {
@@ -429,37 +594,38 @@ def run_ours(args):
                     "generated + normalised on the device" + (
                         "; the reference-layout CSR built once on the device "
                         "(gs_build_csr_device) before timing" if args.input == "csr" else ""),
-            "config": {
-                "workload": f"R-MAT scale-{args.scale} edgefactor {args.edgefactor}, "
-                            f"eps={args.eps} mu={args.mu} (BASELINE configs[1])",
-                "n": n, "m": m, "seed": args.seed,
-                "parallelism": (f"edge-sharded x{world} (b % world), build partitioned by "
-                                f"rank-space rows; {backend.upper()} broadcast/all-reduce/all-gather"
-                                + ("" if backend == "nccl" else
-                                   f" (ranks sharing {torch.cuda.device_count()} GPU(s): "
-                                   "functional check, not a scaling number)")
-                                if shard is not None else "single"),
-                "l2": "inputs larger than L2 (CSR 8(n+1) + 8m bytes), no flush",
-                "step": ("scan_in_memory's C-ABI call on the reference CSR: degree-rank "
-                         "relabel + identify + cluster + classify") if args.input == "csr" else
-                        "device edge list -> rank-space CSR build + identify + cluster + classify",
-            },
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "dram_achieved": (traffic / t_sim / 1e9) if traffic and t_sim > 0 else None,
-                         "dram_frac": (traffic / t_sim / 1e9 / peak) if traffic and t_sim > 0
-                         else None,
-                         "kernel": "similarity pass (identify phase: sketch build + O(1) "
-                                   "pre-pass + k_sim_hash*/k_sim_warp/k_sim_tiny)",
-                         "note": "achieved = SURVEY 8(d) W_sim (every edge not decided by the "
-                                 "O(1) degree bounds reads 4*min(d)) / identify time.  The "
-                                 "sketch bound (k/8 bytes per neighbour of the low endpoint, "
-                                 "early exit), the scan's exact early exit and the O(1) suffix "
-                                 "skip read far less than W_sim, so achieved exceeds the peak: "
-                                 "dram_frac (ncu DRAM bytes of the same kernels / same time) is "
-                                 "the traffic actually moved; the pass is latency/issue bound "
-                                 "(DESIGN.md 3a-3b)",
-                         "alg_bytes_per_step": w_sim, "t_ms": t_sim * 1000, "peak_source": peak_src},
+            "config": workload_config(args, n, m),
+            "parallelism": (f"edge-sharded x{world} (b % world), build partitioned by "
+                            f"rank-space rows; {backend.upper()} broadcast/all-reduce/all-gather"
+                            + ("" if backend == "nccl" else
+                               f" (ranks sharing {torch.cuda.device_count()} GPU(s): "
+                               "functional check, not a scaling number)")
+                            if shard is not None else "single GPU"),
+            "input": ("the reference CSR resident in HBM (gs_engine_load_csr: relabel + "
+                      "per-run sort inside the step)") if args.input == "csr" else
+                     "the normalised device edge list (gs_engine_load_edges: CSR build inside "
+                     "the step)",
+            "roofline": {"bound": "hbm", "achieved": kernels[dom]["achieved_gbs"], "peak": peak,
+                         "unit": "GB/s", "frac": kernels[dom]["frac"], "traffic": traffic,
+                         "kernel": kernels[dom]["kernel"],
+                         "traffic_source": traffic_note,
+                         "alg_bytes_per_launch": kernels[dom]["bytes"],
+                         "t_ms": kernels[dom]["ms"],
+                         "note": "achieved = algorithmic bytes counted on the device for this "
+                                 "kernel class (every global element of graph, sketch and "
+                                 "state data it reads or writes, at its size, early exits "
+                                 "where they stop; DESIGN.md 5) / the class's CUDA-event time "
+                                 "inside the timed steps",
+                         "identify_pass": {"ms": t_sim * 1000, "bytes": pass_bytes,
+                                           "achieved_gbs": pass_bytes / t_sim / 1e9,
+                                           "frac": pass_bytes / t_sim / 1e9 / peak},
+                         "kernels": kernels,
+                         "w_sim_survey": {"bytes": int(st.wsim_bytes),
+                                          "note": "SURVEY 8(d) W_sim (4 min(d) per edge the O(1) "
+                                                  "bounds leave): NOT what the kernels read -- "
+                                                  "the sketch bound and the early exit read ~3% "
+                                                  "of it; kept for comparison with round 1"},
+                         "peak_source": peak_src},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -484,6 +650,14 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.input is None:
+        args.input = "csr" if args.scale < 27 else "edges"
+    rank, world, _ = dist_env()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

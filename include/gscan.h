@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 1
+#define GS_ABI_VERSION 2
 
 #define GS_OK 0
 #define GS_EINVAL 1
@@ -78,6 +78,13 @@ enum {
   GS_PH_D2H = 6,      /* result copy back */
   GS_PH_TOTAL = 7,
   GS_PH_SIM_KERNELS = 8, /* summed duration of the similarity kernels */
+  /* identify pass by kernel class (CUDA events between the launches): */
+  GS_PH_K_PREP = 9,    /* thresholds, degree tables, hub split, sketch build, Lemma-1 pre-pass */
+  GS_PH_K_HUGE = 10,   /* k_sim_hash<1024, L2 table>  (deg b >= 28672) */
+  GS_PH_K_LARGE = 11,  /* k_sim_hash<1024>            (4096 <= deg b < 28672) */
+  GS_PH_K_MEDIUM = 12, /* k_sim_hash<512>             (512 <= deg b < 4096) */
+  GS_PH_K_SMALL = 13,  /* k_sim_warp                  (64 <= deg b < 512) */
+  GS_PH_K_TINY = 14,   /* k_sim_tiny                  (deg b < 64) */
   GS_PH_COUNT = 16
 };
 
@@ -97,6 +104,16 @@ typedef struct gs_stats {
   int64_t peak_device_bytes;      /* high-water mark of engine allocations */
   int64_t sim_decided_by_sketch;  /* decided dissimilar by the sketch bound (no scan) */
   double phase_ms[GS_PH_COUNT];
+  /* (ABI 2) algorithmic bytes of the identify pass per kernel class, in the
+   * order of GS_PH_K_PREP .. GS_PH_K_TINY: every global element of graph,
+   * sketch and state data the kernels read or write, at its size (early
+   * exits counted where they stop; scratch tables excluded).  Divided by the
+   * class's phase_ms this is the roofline's achieved bandwidth. */
+  int64_t kernel_bytes[6];
+  int64_t wsim_bytes;    /* SURVEY 8(d) W_sim: 4 min(d) per edge left by the O(1)
+                          * bounds + 4 d_b per staged b (the accounting of
+                          * round 1, reported for comparison only) */
+  int64_t pcie_bytes;    /* out of core: bytes moved over PCIe (slices + zero-copy) */
 } gs_stats;
 
 typedef struct gs_engine gs_engine;

@@ -26,6 +26,15 @@ GS_EPARSE = 6
 GS_PH_H2D, GS_PH_BUILD, GS_PH_IDENTIFY, GS_PH_CLEANUP = 0, 1, 2, 3
 GS_PH_CLUSTER, GS_PH_CLASSIFY, GS_PH_D2H, GS_PH_TOTAL = 4, 5, 6, 7
 GS_PH_SIM_KERNELS = 8
+ABI_VERSION = 2  # GS_ABI_VERSION of include/gscan.h
+# identify pass by kernel class (gs_stats.phase_ms / kernel_bytes order)
+GS_PH_K_PREP, GS_PH_K_HUGE, GS_PH_K_LARGE, GS_PH_K_MEDIUM, GS_PH_K_SMALL, GS_PH_K_TINY = range(9, 15)
+KERNEL_CLASSES = ("prep: thresholds + degree tables + hub split + sketch build + Lemma-1 pre-pass",
+                  "k_sim_hash<1024,L2 table> (deg b >= 28672)",
+                  "k_sim_hash<1024> (4096 <= deg b < 28672)",
+                  "k_sim_hash<512> (512 <= deg b < 4096)",
+                  "k_sim_warp (64 <= deg b < 512)",
+                  "k_sim_tiny (deg b < 64)")
 GS_PH_COUNT = 16
 
 
@@ -59,6 +68,9 @@ class GsStats(ctypes.Structure):
         ("peak_device_bytes", ctypes.c_int64),
         ("sim_decided_by_sketch", ctypes.c_int64),
         ("phase_ms", ctypes.c_double * GS_PH_COUNT),
+        ("kernel_bytes", ctypes.c_int64 * 6),
+        ("wsim_bytes", ctypes.c_int64),
+        ("pcie_bytes", ctypes.c_int64),
     ]
 
 
@@ -141,6 +153,9 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.gs_version() != ABI_VERSION:  # a stale build would misread gs_stats
+            raise ImportError(f"{LIB_PATH} has ABI {lib.gs_version()}, this package needs "
+                              f"{ABI_VERSION}: rebuild (make -C paper_2311_12281_b200/csrc)")
         _lib = lib
         return lib
 

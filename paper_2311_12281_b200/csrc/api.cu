@@ -125,6 +125,15 @@ int gs_engine::alloc(void** p, size_t bytes) {
   return GS_OK;
 }
 
+void gs_engine::kev_mark(int i) {
+  if (!kev_on) return;
+  if (kev[i] == nullptr && cudaEventCreate(&kev[i]) != cudaSuccess) {
+    kev[i] = nullptr;
+    return;
+  }
+  cudaEventRecord(kev[i], stream);
+}
+
 void gs_engine::release(void* p) {
   if (!p) return;
   auto it = sizes.find(p);
@@ -247,6 +256,8 @@ void gs_engine_destroy(gs_engine* e) {
   cudaStreamSynchronize(e->stream);
   cudaStreamSynchronize(e->cstream);
   if (e->hstage) cudaFreeHost(e->hstage);
+  for (auto& x : e->kev)
+    if (x) cudaEventDestroy(x);
   cudaStreamDestroy(e->cstream);
   cudaStreamDestroy(e->stream);
   // hand the pool's reserved memory back (the release threshold keeps it

@@ -338,6 +338,7 @@ int phase_begin(gs_engine* e, int32_t mu, const Eps2& eps) {
   e->eps = eps;
   e->ncores = 0;
   e->free_state();
+  e->kev_mark(0);
   GS_TRY(e->alloc_n(&s.sim, m));
   GS_TRY(e->alloc_n(&s.bounds, n));
   GS_TRY(e->alloc_n(&s.role, n));
@@ -351,7 +352,9 @@ int phase_begin(gs_engine* e, int32_t mu, const Eps2& eps) {
   GS_CUDA(cudaMemsetAsync(s.ctr, 0, sizeof(unsigned long long) * CTR_COUNT, str));
   GS_CUDA(cudaMemsetAsync(s.label, 0x7f, sizeof(int32_t) * (size_t)(n > 0 ? n : 1), str));
   GS_TRY(prepare_similarity(e, eps));
-  return run_prepass(e, mu);  // initial Lemma-1 bounds incl. every O(1)-decided edge
+  GS_TRY(run_prepass(e, mu));  // initial Lemma-1 bounds incl. every O(1)-decided edge
+  e->kev_mark(1);
+  return GS_OK;
 }
 
 // phase 1 on this shard's edges (Alg. 2)
@@ -663,6 +666,19 @@ void fill_counters(gs_stats* st, int64_t n, int64_t m, const unsigned long long*
     st->n_outlier = (int64_t)h[CTR_N_OUTLIER];
     st->n_clusters = (int64_t)h[CTR_N_CLUSTERS];
     st->sim_decided_by_sketch = (int64_t)h[CTR_SKETCH_DECIDED];
+    int64_t tot = 0;
+    for (int c = 0; c < kKernelClasses; ++c) {
+      st->kernel_bytes[c] = (int64_t)h[CTR_B_PREP + c];
+      tot += st->kernel_bytes[c];
+    }
+    // the state initialisation of phase_begin (memset of sim[m] and label[n])
+    if (h[CTR_B_PREP]) {
+      st->kernel_bytes[0] += m + 4 * n;
+      tot += m + 4 * n;
+    }
+    st->alg_bytes_sim = tot;
+    st->wsim_bytes = h[CTR_WSIM] ? (int64_t)h[CTR_WSIM] + 9 * st->sim_evals + 8 * (n + 1) : 0;
+    st->pcie_bytes = (int64_t)h[CTR_PCIE];
 }
 
 int read_counters(gs_engine* e, gs_stats* st) {
@@ -679,6 +695,7 @@ int read_counters(gs_engine* e, gs_stats* st) {
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
              int32_t* cluster_out, int out_on_device, gs_stats* st) {
   PhaseTimer tm(e);
+  e->kev_on = st != nullptr;
   tm.mark();  // 0
   GS_TRY(phase_begin(e, mu, eps));
   GS_TRY(phase_identify(e));
@@ -698,7 +715,13 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     st->phase_ms[GS_PH_CLEANUP] = tm.ms(1, 2);
     st->phase_ms[GS_PH_CLUSTER] = tm.ms(2, 3);
     st->phase_ms[GS_PH_CLASSIFY] = tm.ms(4, 5) - st->phase_ms[GS_PH_D2H];
+    for (int c = 0; c < kKernelClasses; ++c) {
+      float t = 0;
+      if (e->g.m > 0 && e->kev[c] && e->kev[c + 1]) cudaEventElapsedTime(&t, e->kev[c], e->kev[c + 1]);
+      st->phase_ms[GS_PH_K_PREP + c] = t;
+    }
   }
+  e->kev_on = false;
   return GS_OK;
 }
 

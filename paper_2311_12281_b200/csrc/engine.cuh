@@ -96,8 +96,21 @@ enum Ctr {
   CTR_N_CLUSTERS,
   CTR_CORES_PRE,
   CTR_SKETCH_DECIDED,
+  // Algorithmic bytes of the identify pass per kernel class (DESIGN 5): every
+  // global element the kernels read or write as graph / sketch / state data,
+  // at its size (scratch tables excluded).  The roofline's numerator.
+  CTR_B_PREP,   // thresholds, degree tables, hub split, sketch build, Lemma-1 pre-pass
+  CTR_B_HUGE,   // k_sim_hash<1024, true>
+  CTR_B_LARGE,  // k_sim_hash<1024, false>
+  CTR_B_MED,    // k_sim_hash<512, false>
+  CTR_B_SMALL,  // k_sim_warp
+  CTR_B_TINY,   // k_sim_tiny
+  CTR_B_OTHER,  // the same kernels in the cleanup / union / attach passes
+  CTR_WSIM,     // SURVEY 8(d) W_sim terms counted on the device (4 min(d) per intersected edge)
+  CTR_PCIE,     // out of core: bytes read zero-copy from mapped host memory
   CTR_COUNT
 };
+static constexpr int kKernelClasses = 6;  // CTR_B_PREP .. CTR_B_TINY
 
 enum SimMode : int {
   MODE_IDENTIFY = 0,  // identifyCore (Alg. 2): skip if both roles decided
@@ -133,6 +146,7 @@ struct SimParams {
   int32_t sk_minscan;   //   and the scan would need at least this many misses
   int sk_thread;        // thread-per-survivor sketch pass before the warp scans
   int32_t sk_tmax;      //   for rows of at most this many words (longer: per warp)
+  int bslot;            // counter slot of this launch's algorithmic bytes (CTR_B_*)
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;
@@ -174,6 +188,12 @@ struct gs_engine {
   // host-side pinned staging for counters
   unsigned long long* h_ctr = nullptr;
   std::vector<cudaEvent_t> ev;
+  // identify-pass kernel-class timing: kev[0] before the preparation, kev[1 + c]
+  // after class c (prep, huge, large, medium, small, tiny); recorded when
+  // kev_on, read by run_scan into gs_stats.phase_ms[GS_PH_K_PREP ..]
+  cudaEvent_t kev[gs::kKernelClasses + 1] = {};
+  bool kev_on = false;
+  void kev_mark(int i);
 
   int alloc(void** p, size_t bytes);
   void release(void* p);

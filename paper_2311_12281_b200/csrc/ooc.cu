@@ -192,6 +192,7 @@ __device__ __forceinline__ void ooc_record(const OocParams& P, int32_t a, int32_
 __device__ __forceinline__ void ooc_flush(const OocParams& P, LocalCtr& lc) {
   SimParams S;
   S.ctr = P.ctr;
+  S.bslot = CTR_PCIE;  // the out-of-core kernels count their zero-copy bytes
   flush_ctr(S, lc);
 }
 

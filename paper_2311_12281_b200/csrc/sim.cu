@@ -39,9 +39,11 @@ __device__ __forceinline__ int64_t rdeg_at(const int32_t* rdeg, int64_t dmax, in
 // first index of b's owned prefix that can survive the O(1) bounds: the
 // survivors are the suffix with deg(a) >= max(xmin - 1, simmax + 1)
 __device__ __forceinline__ int64_t survivor_start(const SimParams& P, const int32_t* nb,
-                                                  int64_t nlow, int2 th, int64_t dmax) {
+                                                  int64_t nlow, int2 th, int64_t dmax,
+                                                  unsigned long long& bytes) {
   if (P.mode > MODE_CLEANUP) return 0;  // union / attach re-decide O(1) edges too
   const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
+  bytes += 4ull * (unsigned long long)(64 - __clzll((unsigned long long)nlow));  // probes
   return lower_bound_run(nb, 0, nlow, rdeg_at(P.rdeg, dmax, dstart));
 }
 
@@ -50,7 +52,8 @@ __device__ __forceinline__ int64_t survivor_start(const SimParams& P, const int3
 // answer, so two rounds of parallel loads replace ~log2(nlow) dependent ones.
 template <int NT>
 __device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const int32_t* nb,
-                                                      int64_t nlow, int2 th, int64_t dmax) {
+                                                      int64_t nlow, int2 th, int64_t dmax,
+                                                      unsigned long long& bytes) {
   if (P.mode > MODE_CLEANUP || nlow == 0) return 0;
   const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
   const int64_t key = rdeg_at(P.rdeg, dmax, dstart);
@@ -58,6 +61,7 @@ __device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const 
   while (hi > lo) {
     const int64_t step = (hi - lo + NT - 1) / NT;
     const int64_t idx = lo + (int64_t)threadIdx.x * step;  // probes lo, lo+step, ...
+    if (threadIdx.x == 0) bytes += 4ull * (unsigned long long)min((int64_t)NT, (hi - lo + step - 1) / step);
     const int cnt = __syncthreads_count(idx < hi && (int64_t)nb[idx] < key);
     // nb[lo + (cnt-1) step] < key <= nb[lo + cnt step] (if in range)
     const int64_t nlo = cnt == 0 ? lo : lo + (int64_t)(cnt - 1) * step + 1;
@@ -71,7 +75,7 @@ __device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const 
 // ... and by one warp
 __device__ __forceinline__ int64_t survivor_start_warp(const SimParams& P, const int32_t* nb,
                                                        int64_t nlow, int2 th, int64_t dmax,
-                                                       int lane) {
+                                                       int lane, unsigned long long& bytes) {
   if (P.mode > MODE_CLEANUP || nlow == 0) return 0;
   const int64_t dstart = max((int64_t)th.x - 1, (int64_t)th.y + 1);
   const int64_t key = rdeg_at(P.rdeg, dmax, dstart);
@@ -79,6 +83,7 @@ __device__ __forceinline__ int64_t survivor_start_warp(const SimParams& P, const
   while (hi > lo) {
     const int64_t step = (hi - lo + 31) / 32;
     const int64_t idx = lo + (int64_t)lane * step;
+    if (lane == 0) bytes += 4ull * (unsigned long long)min((int64_t)32, (hi - lo + step - 1) / step);
     const int cnt = __popc(__ballot_sync(0xffffffffu, idx < hi && (int64_t)nb[idx] < key));
     const int64_t nlo = cnt == 0 ? lo : lo + (int64_t)(cnt - 1) * step + 1;
     const int64_t nhi = min(hi, lo + (int64_t)cnt * step);
@@ -104,8 +109,11 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
     if (e0 == e1) continue;
     if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
     const int64_t ob = P.off[b], eb = P.off[b + 1], db = eb - ob;
-    const int64_t j0 = survivor_start(P, P.adj + ob, e1 - e0, P.thr[db], P.dmax);
+    lc.bytes += kBytesB;
+    const int64_t j0 = survivor_start(P, P.adj + ob, e1 - e0, P.thr[db], P.dmax, lc.bytes);
+    bool staged = false;
     for (int64_t e = e0 + j0; e < e1; ++e) {
+      lc.bytes += kBytesCand;
       const int32_t a = P.adj[ob + (e - e0)];
       const int64_t ia0 = P.off[a], ea = P.off[a + 1];
       const int64_t da = ea - ia0;
@@ -131,8 +139,11 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
         }
         lc.probes += (unsigned long long)(ia - ia0);
         lc.inters++;
-        lc.bytes += 4ull * (unsigned long long)(da + db);
+        lc.bytes += 4ull * (unsigned long long)((ia - ia0) + (ib - ob));  // the merge's reads
+        lc.wsim += 4ull * (unsigned long long)da + (staged ? 0ull : 4ull * (unsigned long long)db);
+        staged = true;
       }
+      lc.bytes += kBytesRec + 16;  // + b's bounds (applied per edge here)
       record_edge(P, e, a, (int32_t)b, res, true, lc, !(bdis || bsim));
     }
   }
@@ -230,11 +241,12 @@ __global__ void k_prepass_bs(int64_t n, int64_t own_lo, int64_t own_hi, int64_t 
                              const int32_t* __restrict__ rdeg, const int2* __restrict__ dxs,
                              int32_t mu, uint64_t* __restrict__ bounds,
                              uint8_t* __restrict__ role, unsigned long long* __restrict__ ctr) {
-  unsigned long long decided = 0;
+  unsigned long long decided = 0, bytes = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = off[v], dv = off[v + 1] - o;
     uint32_t sim = 0, dis = 0;
+    bytes += 16 + 9;  // off[v..v+1]; bounds + role written
     if (v >= own_lo && v < own_hi && dv > 0) {
       const int64_t p0 = eoff[v + 1] - eoff[v];  // neighbours below v (v is their high end)
       const int2 th = thr[dv];
@@ -248,15 +260,23 @@ __global__ void k_prepass_bs(int64_t n, int64_t own_lo, int64_t own_hi, int64_t 
       dis = (uint32_t)(dl + dh);
       sim = (uint32_t)(slo + (sh > 0 ? sh : 0));
       decided += (unsigned long long)(dl + slo);
+      // eoff pair, thr, dxs, 4 rdeg entries + the four binary searches' probes
+      const unsigned lp = 64 - __clzll((unsigned long long)p0),
+                     lh = 64 - __clzll((unsigned long long)(dv - p0));
+      bytes += 16 + 8 + 8 + 16 + 8ull * (lp + lh);
     }
     prepass_finish(v, (uint32_t)dv, sim, dis, mu, bounds, role);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) decided += __shfl_xor_sync(0xffffffffu, decided, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    decided += __shfl_xor_sync(0xffffffffu, decided, o);
+    bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+  }
   if ((threadIdx.x & 31) == 0 && decided) {
     atomicAdd(&ctr[CTR_SIM_EVALS], decided);
     atomicAdd(&ctr[CTR_BOUND_DECIDED], decided);
   }
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(&ctr[CTR_B_PREP], bytes);
 }
 
 __global__ void k_prepass_thread(int64_t rlo, int64_t rhi, int64_t own_lo, int64_t own_hi,
@@ -331,17 +351,24 @@ __global__ void k_degrees(const int64_t* __restrict__ off, int64_t n, uint32_t* 
 
 // per-vertex split of the adjacency run at hub_lo (runs are sorted)
 __global__ void k_hubsplit(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
-                           int64_t n, uint32_t hub_lo, int32_t* __restrict__ nlo) {
+                           int64_t n, uint32_t hub_lo, int32_t* __restrict__ nlo,
+                           unsigned long long* __restrict__ ctr) {
+  unsigned long long bytes = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     int64_t l = off[v], h = off[v + 1];
     const int64_t lo0 = l;
+    bytes += 16 + 4 + 4ull * (64 - __clzll((unsigned long long)(h - l)));
     while (l < h) {
       const int64_t mid = (l + h) >> 1;
       if ((uint32_t)adj[mid] < hub_lo) l = mid + 1; else h = mid;
     }
     nlo[v] = (int32_t)(l - lo0);
   }
+  if (ctr == nullptr) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(&ctr[CTR_B_PREP], bytes);
 }
 
 template <int NT, bool GTAB>
@@ -363,8 +390,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ int64_t s_nlo;
   __shared__ uint32_t s_stash[kStash];
+  __shared__ unsigned long long s_ctr[LC_N];
   const int tid = threadIdx.x, lane = tid & 31;
-  LocalCtr lc;
+  SharedCtr lc{s_ctr};
+  shared_ctr_init(s_ctr);
   Cuckoo C;
   C.tab = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : tab_s;
   C.nstash = &s_nstash;
@@ -385,12 +414,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int32_t* __restrict__ nb = P.adj + ob;
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
-    bool built = false, sk_staged = false;
-    const int64_t j0 = survivor_start_cta<NT>(P, nb, nlow, th, P.dmax);
+    bool built = false, sk_staged = false, wsim_b = false;
+    unsigned long long sb = kBytesB;
+    const int64_t j0 = survivor_start_cta<NT>(P, nb, nlow, th, P.dmax, sb);
+    if (tid == 0) ctr_add(lc, LC_BYTES, sb);
     for (int64_t base = j0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
       __syncthreads();
       const int64_t lim = base + chunk < nlow ? base + chunk : nlow;
+      if (tid == 0) ctr_add(lc, LC_BYTES, (unsigned long long)(lim - base) * kBytesCand);
       // filter + O(1) bounds, one candidate a per thread
       for (int64_t j = base + tid; j < lim; j += NT) {
         const int64_t e = e0 + j;
@@ -406,6 +438,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           record_edge(P, e, a, (int32_t)b, true, false, lc, false);
         } else {
           const int slot = atomicAdd(&s_nsurv, 1);
+          ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)da);  // SURVEY W_sim: 4 min(d)
           surv_oa[slot] = oa;
           surv_ad[slot] = make_int2(a, (int32_t)da);
           surv_jc[slot] = make_int2((int32_t)j, (int32_t)c_min_exact(da, db, da - 1, P.eps));
@@ -414,6 +447,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       __syncthreads();
       const int ns = s_nsurv;
       if (ns > 0) {
+        if (tid == 0 && !wsim_b) ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)db);  // once
+        wsim_b = true;
         int ns_scan = ns;
         const bool tpass = P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
                            2 * sk_words(db, P.sk_lk) <= skw;
@@ -421,6 +456,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             2 * sk_words(db, P.sk_lk) <= skw) {  // b's sketch and its folds, once per b
           const int64_t wb = sk_words(db, P.sk_lk);
           sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
+          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)wb);
           sk_staged = true;
         }
         if (tpass) {
@@ -441,12 +477,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             keep[r] = true;
             if (sk_words(kad[r].y, P.sk_lk) <= P.sk_tmax && sk_try(P, kad[r].y, db, kjc[r].y)) {
               const int64_t wa = sk_words(kad[r].y, P.sk_lk);
-              if (sk_thread_rejects(sk_row(P, kad[r].x, kad[r].y, wa), sk_lev + 2 * (wbx - wa),
-                                    wa, wa, kad[r].y, kjc[r].y)) {
+              unsigned long long words = 0;
+              const bool rej = sk_thread_rejects(sk_row(P, kad[r].x, kad[r].y, wa),
+                                                 sk_lev + 2 * (wbx - wa), wa, wa, kad[r].y,
+                                                 kjc[r].y, false, words);
+              ctr_add(lc, LC_BYTES, 4ull * words + (rej ? kBytesRec : 0u));
+              if (rej) {
                 keep[r] = false;
                 record_edge(P, e0 + kjc[r].x, kad[r].x, (int32_t)b, false, false, lc);
-                lc.sketch++;
-                lc.bytes += 4ull * (unsigned long long)kad[r].y;
+                ctr_add(lc, LC_SKETCH, 1);
                 atomicAdd(&s_bdis, 1u);
               }
             }
@@ -487,7 +526,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           }
           __syncthreads();
           built = true;
-          if (tid == 0) lc.bytes += 4ull * (unsigned long long)db;  // N(b) read once
+          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull + 4ull * (unsigned long long)db);  // nlo[b], N(b)
         }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
@@ -510,9 +549,11 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           const int2 ad = surv_ad[s];
           int32_t scanned = 0;
           bool skd = false;
+          unsigned long long skbytes = 0;
           // long rows are left to the warp (thread-pass imbalance)
           if ((!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
+            skbytes = 4ull * (unsigned long long)(lev ? wa : wa + wb);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
             if (lev)
               skd = sk_rejects_lev(A, sk_lev + 2 * (wb - wa), wa, ad.y, jc.y, lane);
@@ -525,10 +566,9 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
                                                        rmax, C, nstash, nb, nlo, lane, scanned,
                                                        first);
           if (lane == 0) {
-            lc.probes += (unsigned long long)scanned;
-            lc.inters += !skd;
-            lc.sketch += skd;
-            lc.bytes += 4ull * (unsigned long long)ad.y;
+            ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
+            ctr_add(lc, skd ? LC_SKETCH : LC_INTERS, 1);
+            ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)scanned + kBytesRec + skbytes);
             record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
           }
@@ -538,8 +578,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       }
       __syncthreads();
       if (tid == 0 && (s_bsim | s_bdis) &&
-          (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP))
+          (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP)) {
         apply_bounds(P.bounds, P.role, b, s_bsim, s_bdis, P.mu);
+        ctr_add(lc, LC_BYTES, 16);
+      }
       __syncthreads();
     }
     if (built) {  // clear the bitmap words this b set (O(deg b), not O(R))
@@ -547,7 +589,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     }
     __syncthreads();  // bitmap clean and s_item read by all before the next b
   }
-  flush_ctr(P, lc);
+  shared_ctr_flush(P, s_ctr);
 }
 
 // ---------------------------------------------------------------------------
@@ -568,7 +610,9 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
   C.tab = tab;
   C.stash = tab + 4 * kWarpBuckets;
   C.nstash = reinterpret_cast<int*>(C.stash + kStash);
-  LocalCtr lc;
+  __shared__ unsigned long long s_ctr[LC_N];
+  SharedCtr lc{s_ctr};
+  shared_ctr_init(s_ctr);
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
@@ -583,9 +627,13 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     bool built = false;
     uint32_t bsim = 0, bdis = 0;
     int64_t wb = 0;
-    const int64_t j0 = survivor_start_warp(P, nb, nlow, th, P.dmax, lane);
+    unsigned long long sb = kBytesB;
+    const int64_t j0 = survivor_start_warp(P, nb, nlow, th, P.dmax, lane, sb);
+    if (lane == 0) ctr_add(lc, LC_BYTES, sb);
     for (int64_t base = j0; base < nlow; base += 32) {
       const int64_t j = base + lane;
+      if (lane == 0)
+        ctr_add(lc, LC_BYTES, (unsigned long long)min((int64_t)32, nlow - base) * kBytesCand);
       int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
       int32_t a = 0, da = 0, cmin = 0;
       int64_t oa = 0;
@@ -600,15 +648,18 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
           else {
             st = 3;
             cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
+            ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)da);  // SURVEY W_sim: 4 min(d)
             // thread-per-candidate sketch bound (S_b folded from global, L1-resident)
             if (P.sk_thread && P.sk != nullptr && db >= P.sk_dmin && sk_try(P, da, db, cmin)) {
               const int64_t wa = sk_words(da, P.sk_lk), wbb = sk_words(db, P.sk_lk);
-              if (sk_thread_rejects(sk_row(P, a, da, wa), sk_row(P, b, db, wbb), wa, wbb, da,
-                                    cmin)) {
+              unsigned long long words = 0;
+              const bool rej = sk_thread_rejects(sk_row(P, a, da, wa), sk_row(P, b, db, wbb), wa,
+                                                 wbb, da, cmin, true, words);
+              ctr_add(lc, LC_BYTES, 4ull * words + (rej ? kBytesRec : 0u));
+              if (rej) {
                 st = 4;
                 record_edge(P, e0 + j, a, (int32_t)b, false, false, lc);
-                lc.sketch++;
-                lc.bytes += 4ull * (unsigned long long)da;
+                ctr_add(lc, LC_SKETCH, 1);
               }
             }
           }
@@ -631,7 +682,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
         if (P.sk != nullptr && db >= P.sk_dmin) wb = sk_words(db, P.sk_lk);
         __syncwarp();
         built = true;
-        if (lane == 0) lc.bytes += 4ull * (unsigned long long)db;
+        if (lane == 0) {
+          ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)db);
+          ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)db);  // larger list once
+        }
       }
       const int nstash = built ? *C.nstash : 0;
       // survivors of this batch, software-pipelined like the CTA kernel
@@ -654,8 +708,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
         const uint32_t first2 = smask ? first_element(P.adj + oa2, da2, lane) : kPast;
         int32_t scanned = 0;
         bool skd = false;
+        unsigned long long skbytes = 0;
         if (!P.sk_thread && sk_try(P, sda, db, scm)) {
           const int64_t wa = sk_words(sda, P.sk_lk);
+          skbytes = 4ull * (unsigned long long)(wa + wb);
           // S_b (<= 128 words at k <= 8) folded from global: L1-resident
           skd = sk_rejects_fold(sk_row(P, sa, sda, wa), sk_row(P, b, db, wb), wa, wb, sda, scm,
                                 lane);
@@ -664,21 +720,22 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
                                                       0, C, nstash, nb, db, lane, scanned, first);
         if (res) ++bsim; else ++bdis;
         if (lane == 0) {
-          lc.probes += (unsigned long long)scanned;
-          lc.inters += !skd;
-          lc.sketch += skd;
-          lc.bytes += 4ull * (unsigned long long)sda;
+          ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
+          ctr_add(lc, skd ? LC_SKETCH : LC_INTERS, 1);
+          ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)scanned + kBytesRec + skbytes);
           record_edge(P, e0 + base + src, sa, (int32_t)b, res, false, lc);
         }
         src = src2;
         first = first2;
       }
     }
-    if (lane == 0 && (bsim | bdis) && (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP))
+    if (lane == 0 && (bsim | bdis) && (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP)) {
       apply_bounds(P.bounds, P.role, b, bsim, bdis, P.mu);
+      ctr_add(lc, LC_BYTES, 16);
+    }
     __syncwarp();
   }
-  flush_ctr(P, lc);
+  shared_ctr_flush(P, s_ctr);
 }
 
 // ---------------------------------------------------------------------------
@@ -794,7 +851,8 @@ int prepare_similarity(gs_engine* e, const Eps2& eps) {
   const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
   const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
   if (g.n > 0) {
-    k_hubsplit<<<grid_for(g.n, 256), 256, 0, e->stream>>>(g.off, g.adj, g.n, hub_lo, s.nlo);
+    k_hubsplit<<<grid_for(g.n, 256), 256, 0, e->stream>>>(g.off, g.adj, g.n, hub_lo, s.nlo,
+                                                          s.ctr);
     e->launches += 2;
   }
   GS_CUDA(cudaGetLastError());
@@ -839,6 +897,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   if (const char* v = getenv("GS_SKETCH_TMAX")) P.sk_tmax = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
+  const bool ident = mode == MODE_IDENTIFY;
+  auto slot = [&](int c) { P.bslot = ident ? c : CTR_B_OTHER; };
   {
     const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
     P.hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
@@ -864,15 +924,24 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     const int64_t nblk = (int64_t)e->sms * 2;
     GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
     P.gtab_stride = 4 * tcap_g;
+    slot(CTR_B_HUGE);
     GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, g.dmax,
                                      e->stream)));
   }
+  if (ident) e->kev_mark(2);
   // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB) + cuckoo table
   // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
   // per candidate of a chunk); the small class runs warp-per-b
+  slot(CTR_B_LARGE);
   GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
+  if (ident) e->kev_mark(3);
+  slot(CTR_B_MED);
   GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024, dcls[1], e->stream)));
+  if (ident) e->kev_mark(4);
+  slot(CTR_B_SMALL);
   GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
+  if (ident) e->kev_mark(5);
+  slot(CTR_B_TINY);
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
@@ -880,6 +949,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     e->launches++;
     GS_CUDA(cudaGetLastError());
   }
+  if (ident) e->kev_mark(6);
   if (P.gtab) {
     GS_CUDA(cudaStreamSynchronize(e->stream));
     e->release(P.gtab);

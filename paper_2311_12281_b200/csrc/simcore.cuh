@@ -82,34 +82,94 @@ __device__ __forceinline__ bool edge_needed(const SimParams& P, int64_t e, int32
   }
 }
 
+// Work counters of the similarity kernels.  LocalCtr lives in registers
+// (thread-level kernels); SharedCtr is one CTA-wide array in shared memory,
+// updated with shared atomics -- the persistent CTA / warp kernels sit at their
+// register limit, and eight 64-bit register counters per thread cost spills.
+enum LCtrIdx { LC_EVALS, LC_PROBES, LC_BOUND, LC_INTERS, LC_BYTES, LC_RETRIES, LC_SKETCH, LC_WSIM,
+               LC_N };
+
 struct LocalCtr {
   unsigned long long evals = 0, probes = 0, bound = 0, inters = 0, bytes = 0, retries = 0,
-                     sketch = 0;
+                     sketch = 0, wsim = 0;
 };
+
+struct SharedCtr {
+  unsigned long long* v;  // [LC_N], shared memory
+};
+
+__device__ __forceinline__ void ctr_add(LocalCtr& c, int i, unsigned long long x) {
+  switch (i) {
+    case LC_EVALS: c.evals += x; break;
+    case LC_PROBES: c.probes += x; break;
+    case LC_BOUND: c.bound += x; break;
+    case LC_INTERS: c.inters += x; break;
+    case LC_BYTES: c.bytes += x; break;
+    case LC_RETRIES: c.retries += x; break;
+    case LC_SKETCH: c.sketch += x; break;
+    default: c.wsim += x; break;
+  }
+}
+
+__device__ __forceinline__ void ctr_add(const SharedCtr& c, int i, unsigned long long x) {
+  if (x) atomicAdd(c.v + i, x);
+}
+
+// global counter of each LC_* index (bytes go to the launch's class slot)
+__device__ __forceinline__ int ctr_slot(const SimParams& P, int i) {
+  switch (i) {
+    case LC_EVALS: return CTR_SIM_EVALS;
+    case LC_PROBES: return CTR_PROBES;
+    case LC_BOUND: return CTR_BOUND_DECIDED;
+    case LC_INTERS: return CTR_INTERSECTIONS;
+    case LC_BYTES: return P.bslot;
+    case LC_RETRIES: return CTR_UNION_RETRIES;
+    case LC_SKETCH: return CTR_SKETCH_DECIDED;
+    default: return CTR_WSIM;
+  }
+}
+
+// zero / flush a SharedCtr: every thread of the CTA calls both (barriers inside)
+__device__ __forceinline__ void shared_ctr_init(unsigned long long* v) {
+  if (threadIdx.x < LC_N) v[threadIdx.x] = 0ull;
+  __syncthreads();
+}
+__device__ __forceinline__ void shared_ctr_flush(const SimParams& P, const unsigned long long* v) {
+  __syncthreads();
+  if (threadIdx.x < LC_N && v[threadIdx.x]) atomicAdd(&P.ctr[ctr_slot(P, threadIdx.x)], v[threadIdx.x]);
+}
+
+// Algorithmic bytes (CTR_B_*, DESIGN 5) charged per unit of work:
+static constexpr unsigned kBytesB = 40;     // per b: off[b..b+1], eoff[b..b+1], thr[deg b]
+static constexpr unsigned kBytesCand = 22;  // per filtered candidate a: nb[j], off[a..a+1], 2 roles
+static constexpr unsigned kBytesRec = 17;   // per decided edge: sim[e] + a's bounds (atomic RMW)
 
 // Record one decided edge.  b's bound update is returned to the caller
 // (aggregated per CTA for the shared-b kernels) unless apply_b is set.
 // `count` is false for O(1)-decided edges re-met by the union / attach passes:
 // the identify pre-pass already counted their decision (sim_evals).
+template <class Ctr>
 __device__ __forceinline__ void record_edge(const SimParams& P, int64_t e, int32_t a,
                                             int32_t b, bool similar, bool apply_b,
-                                            LocalCtr& lc, bool count = true) {
+                                            Ctr& lc, bool count = true) {
   P.sim[e] = similar ? SIM_SIMILAR : SIM_DISSIMILAR;
-  lc.evals += count;
+  ctr_add(lc, LC_EVALS, count ? 1ull : 0ull);
   if (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP) {
     apply_bounds(P.bounds, P.role, a, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
     if (apply_b) apply_bounds(P.bounds, P.role, b, similar ? 1u : 0u, similar ? 0u : 1u, P.mu);
   } else if (P.mode == MODE_UNION && similar) {
-    uf_union(P.parent, a, b, lc.retries);
+    unsigned long long r = 0;
+    uf_union(P.parent, a, b, r);
+    ctr_add(lc, LC_RETRIES, r);
   }
 }
 
 __device__ __forceinline__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
   // warp reduce then one atomic per warp
-  unsigned long long v[7] = {lc.evals, lc.probes, lc.bound, lc.inters, lc.bytes, lc.retries,
-                             lc.sketch};
+  unsigned long long v[8] = {lc.evals, lc.probes, lc.bound, lc.inters, lc.bytes, lc.retries,
+                             lc.sketch, lc.wsim};
 #pragma unroll
-  for (int i = 0; i < 7; ++i) {
+  for (int i = 0; i < 8; ++i) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
   }
@@ -118,9 +178,10 @@ __device__ __forceinline__ void flush_ctr(const SimParams& P, LocalCtr& lc) {
     if (v[1]) atomicAdd(&P.ctr[CTR_PROBES], v[1]);
     if (v[2]) atomicAdd(&P.ctr[CTR_BOUND_DECIDED], v[2]);
     if (v[3]) atomicAdd(&P.ctr[CTR_INTERSECTIONS], v[3]);
-    if (v[4]) atomicAdd(&P.ctr[CTR_ALG_BYTES], v[4]);
+    if (v[4]) atomicAdd(&P.ctr[P.bslot], v[4]);
     if (v[5]) atomicAdd(&P.ctr[CTR_UNION_RETRIES], v[5]);
     if (v[6]) atomicAdd(&P.ctr[CTR_SKETCH_DECIDED], v[6]);
+    if (v[7]) atomicAdd(&P.ctr[CTR_WSIM], v[7]);
   }
 }
 
@@ -431,15 +492,19 @@ __device__ __forceinline__ bool sk_rejects_lev4(const uint32_t* __restrict__ A,
 // checked at once, so hundreds of rows are in flight per SM instead of one
 // per warp.
 // U = 16-byte steps in flight per early-exit check
+// `gwords` += the global words read (S_a, plus S_b's slices when bglobal).
 template <int SK_UNROLL = 2>
 __device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A,
                                                   const uint32_t* B, int64_t wa, int64_t wb,
-                                                  int64_t da, int32_t cmin) {
+                                                  int64_t da, int32_t cmin, bool bglobal,
+                                                  unsigned long long& gwords) {
   const uint4* __restrict__ a4 = reinterpret_cast<const uint4*>(A);
   const uint4* b4 = reinterpret_cast<const uint4*>(B);
   const int64_t q = wa >> 2, qb = wb >> 2;
   int64_t u = da;
   for (int64_t j = 0; j < q; j += SK_UNROLL) {
+    gwords += 4ull * (unsigned long long)min((int64_t)SK_UNROLL, q - j) *
+              (unsigned long long)(1 + (bglobal ? qb / q : 0));
     uint4 x[SK_UNROLL], y[SK_UNROLL];
 #pragma unroll
     for (int t = 0; t < SK_UNROLL; ++t) {

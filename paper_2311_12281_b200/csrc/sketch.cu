@@ -117,6 +117,15 @@ __global__ void __launch_bounds__(512) k_sk_cta(const int64_t* __restrict__ off,
   }
 }
 
+// algorithmic bytes of the build (CTR_B_PREP): the arcs of every sketched
+// vertex read once, its row written once, its offsets read
+__global__ void k_sk_bytes(const int64_t* __restrict__ off, int64_t n, int64_t r0,
+                           const int64_t* __restrict__ skbase, int64_t dmax,
+                           unsigned long long* __restrict__ ctr) {
+  const int64_t arcs = off[n] - off[r0];
+  atomicAdd(&ctr[CTR_B_PREP], (unsigned long long)(4 * arcs + 4 * skbase[dmax + 1] + 16 * (n - r0)));
+}
+
 int build_sketch(gs_engine* e, int lk, int64_t dmin) {
   DevGraph& g = e->g;
   DevState& s = e->s;
@@ -192,6 +201,10 @@ int build_sketch(gs_engine* e, int lk, int64_t dmin) {
     const int64_t grid = std::min<int64_t>(n - r2, (int64_t)e->sms * 2);
     kern<<<(unsigned)grid, 512, smem_words * 4, st>>>(g.off, g.adj, r2, n, s.rdeg, g.skbase, lk,
                                                       g.sk, smem_words);
+    e->launches++;
+  }
+  if (s.ctr && n > r0) {
+    k_sk_bytes<<<1, 1, 0, st>>>(g.off, n, r0, g.skbase, g.dmax, s.ctr);
     e->launches++;
   }
   GS_CUDA(cudaGetLastError());
