@@ -226,6 +226,25 @@ int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets,
                         uint64_t hbm_cap_bytes, uint8_t* role_out, int32_t* cluster_out,
                         gs_stats* stats);
 
+/* The partition plan (scan_out_of_core's PartitionPlan, partition.py:231-333):
+ * host only, no device needed.  Contiguous ranges of b (vertex ids) whose
+ * adjacency slice fits one of the two streaming buffers the cap leaves after
+ * the resident state; part_bounds [nparts + 1] receives the range starts and n
+ * (when max_parts >= nparts; call with NULL first to size it), stream_elems the
+ * buffer size in adjacency elements.  GS_EBUDGET if the state or the largest
+ * list cannot fit (InfeasibleBudgetError, partition.py:79-89). */
+int gs_plan_partitions(int64_t n, const int64_t* offsets, uint64_t hbm_cap_bytes,
+                       int64_t* part_bounds, int64_t max_parts, int64_t* nparts,
+                       int64_t* stream_elems);
+/* gs_scan_partitioned executing the caller's plan (partition.py:666-757 iterates
+ * plan.partitions): part_bounds [nparts + 1] from gs_plan_partitions or any
+ * cut whose slices fit the buffers (GS_EBUDGET names the partition that does
+ * not).  gs_scan_partitioned = this call with the plan gs_plan_partitions makes. */
+int gs_scan_partitioned_plan(int64_t n, int64_t m, const int64_t* offsets,
+                             const int32_t* adjacency, int32_t mu, const gs_eps2* eps2,
+                             uint64_t hbm_cap_bytes, int64_t nparts, const int64_t* part_bounds,
+                             uint8_t* role_out, int32_t* cluster_out, gs_stats* stats);
+
 /* Deterministic R-MAT workload generator (bench/test input; same stream as
  * the CPU generator in oracle/): raw samples, device pointers. */
 int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,

@@ -3,6 +3,7 @@
 // returns a GS_* code and leaves a message in gs_last_error().
 #include <cstdio>
 #include <cstring>
+#include <new>
 #include <string>
 
 #include "engine.cuh"
@@ -29,7 +30,11 @@ int normalize_edges(gs_engine* e, int64_t count, const int32_t* src, const int32
                     int32_t* uv, int64_t* m_out);
 int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
                      const int32_t* adj, int32_t mu, const Eps2& eps, uint8_t* role_out,
-                     int32_t* cluster_out, gs_stats* st);
+                     int32_t* cluster_out, gs_stats* st, const int64_t* bounds, int64_t nb);
+int plan_partitions(int64_t n, const int64_t* off, uint64_t cap, int64_t* bounds_out,
+                    int64_t max_parts, int64_t* nparts, int64_t* stream_elems);
+int validate_plan(int64_t n, const int64_t* off, uint64_t cap, const int64_t* bounds,
+                  int64_t nb);
 int check_sim_batch(gs_engine* e, int64_t k, const int32_t* u, const int32_t* v,
                     const Eps2& eps, int8_t* out);
 
@@ -623,21 +628,61 @@ int gs_engine_check_sim(gs_engine* e, int64_t k, const int32_t* u, const int32_t
   return check_sim_batch(e, k, u, v, to_eps(eps2), out);
 }
 
-int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
-                        int32_t mu, const gs_eps2* eps2, uint64_t hbm_cap_bytes,
-                        uint8_t* role_out, int32_t* cluster_out, gs_stats* stats) {
+int gs_scan_partitioned_plan(int64_t n, int64_t m, const int64_t* offsets,
+                             const int32_t* adjacency, int32_t mu, const gs_eps2* eps2,
+                             uint64_t hbm_cap_bytes, int64_t nparts, const int64_t* part_bounds,
+                             uint8_t* role_out, int32_t* cluster_out, gs_stats* stats) {
   if (mu < 2) { set_error("mu must be >= 2"); return GS_EINVAL; }
   GS_TRY(check_eps(eps2));
+  if (part_bounds && nparts < 1) { set_error("a plan needs at least one partition"); return GS_EINVAL; }
+  if (n < 0 || m < 0 || (n > 0 && (!offsets || offsets[n] != 2 * m))) {
+    set_error("invalid graph: vertex_offsets must end at 2m");
+    return GS_EINVAL;
+  }
+  if (n > 0 && part_bounds) {  // a plan that cannot run fails before any device work
+    try {
+      GS_TRY(validate_plan(n, offsets, hbm_cap_bytes, part_bounds, nparts));
+    } catch (const std::bad_alloc&) {
+      set_error("host memory exhausted while validating the plan");
+      return GS_ENOMEM;
+    }
+  }
   gs_engine* e = nullptr;
   GS_TRY(gs_engine_create(-1, hbm_cap_bytes, &e));
   int rc = load_common(e, n, m);
   if (stats) memset(stats, 0, sizeof(*stats));
-  if (rc == GS_OK)
-    rc = scan_partitioned(e, n, m, offsets, adjacency, mu, to_eps(eps2), role_out, cluster_out,
-                          stats);
+  if (rc == GS_OK) {
+    try {
+      rc = scan_partitioned(e, n, m, offsets, adjacency, mu, to_eps(eps2), role_out, cluster_out,
+                            stats, part_bounds, part_bounds ? nparts : 0);
+    } catch (const std::bad_alloc&) {
+      set_error("host memory exhausted in the partitioned scan");
+      rc = GS_ENOMEM;
+    }
+  }
   if (stats) stats->peak_device_bytes = (int64_t)e->peak;
   gs_engine_destroy(e);
   return rc;
+}
+
+int gs_scan_partitioned(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
+                        int32_t mu, const gs_eps2* eps2, uint64_t hbm_cap_bytes,
+                        uint8_t* role_out, int32_t* cluster_out, gs_stats* stats) {
+  return gs_scan_partitioned_plan(n, m, offsets, adjacency, mu, eps2, hbm_cap_bytes, 0, nullptr,
+                                  role_out, cluster_out, stats);
+}
+
+int gs_plan_partitions(int64_t n, const int64_t* offsets, uint64_t hbm_cap_bytes,
+                       int64_t* part_bounds, int64_t max_parts, int64_t* nparts,
+                       int64_t* stream_elems) {
+  if (n < 0 || (n > 0 && !offsets)) { set_error("invalid graph"); return GS_EINVAL; }
+  try {
+    return plan_partitions(n, offsets, hbm_cap_bytes, part_bounds, max_parts, nparts,
+                           stream_elems);
+  } catch (const std::bad_alloc&) {
+    set_error("host memory exhausted while planning");
+    return GS_ENOMEM;
+  }
 }
 
 int gs_rmat_generate(int scale, int edgefactor, uint64_t seed, int32_t* src_dev,

@@ -247,7 +247,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
         }
       }
       uint32_t sku = 0;  // the candidate's sketch row (16-byte units), read here in parallel
-      if (want) sku = P.hsk_off[a];
+      if (want) {
+        sku = P.hsk_off[a];  // zero-copy
+        lc.bytes += 4;
+      }
       if (__any_sync(0xffffffffu, want) && !skb) {
         ooc_sk_levels(nb, db, P.sk_lk, lev, lane, 32, [] { __syncwarp(); });
         skb = true;
@@ -277,7 +280,11 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
         if (__shfl_sync(0xffffffffu, want, src)) {  // sketch bound: the warp reads a's row
           const uint32_t u = __shfl_sync(0xffffffffu, sku, src);
           const int64_t wa = sk_words(sda, P.sk_lk), wb = sk_words(db, P.sk_lk);
-          if (sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, sda, scm, lane)) {
+          unsigned long long skb_read = 0;
+          const bool rej = sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, sda,
+                                           scm, lane, skb_read);
+          if (lane == 0) lc.bytes += skb_read;
+          if (rej) {
             if (P.mode == OOC_IDENTIFY) ++bdis;
             if (lane == 0) {
               lc.sketch++;
@@ -296,6 +303,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT / 2) k_ooc_warp(OocParams P) {
         if (P.mode == OOC_IDENTIFY) { if (res) ++bsim; else ++bdis; }
         if (lane == 0) {
           lc.probes += (unsigned long long)scanned;
+          lc.bytes += 8ull + 4ull * (unsigned long long)scanned;  // hoff[a] + N(a), zero-copy
           lc.inters++;
           ooc_record(P, sa, (int32_t)b, res, lc);
         }
@@ -365,7 +373,9 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
           surv_oa[slot] = P.hoff[a];  // zero-copy
           surv_ad[slot] = make_int2(a, (int32_t)da);
           surv_jc[slot] = make_int2((int32_t)j, cm);
-          surv_sk[slot] = bsk && ooc_sk_try(P, da, db, cm) ? P.hsk_off[a] : 0xFFFFFFFFu;
+          const bool tsk = bsk && ooc_sk_try(P, da, db, cm);
+          surv_sk[slot] = tsk ? P.hsk_off[a] : 0xFFFFFFFFu;
+          lc.bytes += tsk ? 12u : 8u;
         }
       }
       __syncthreads();
@@ -396,8 +406,11 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
           const uint32_t u = surv_sk[s];
           if (u != 0xFFFFFFFFu) {  // sketch bound: the warp reads a's row
             const int64_t wa = sk_words(ad.y, P.sk_lk), wb = sk_words(db, P.sk_lk);
-            if (sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, ad.y, jc.y,
-                                lane)) {
+            unsigned long long skb_read = 0;
+            const bool rej = sk_rejects_lev4(P.hsk + 4 * (int64_t)u, lev + 2 * (wb - wa), wa, ad.y,
+                                             jc.y, lane, skb_read);
+            if (lane == 0) lc.bytes += skb_read;
+            if (rej) {
               if (lane == 0) {
                 lc.sketch++;
                 ooc_record(P, ad.x, b, false, lc);
@@ -412,6 +425,7 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
                                                first_element(P.hadj + surv_oa[s], ad.y, lane));
           if (lane == 0) {
             lc.probes += (unsigned long long)scanned;
+            lc.bytes += 4ull * (unsigned long long)scanned;  // N(a), zero-copy
             lc.inters++;
             ooc_record(P, ad.x, b, res, lc);
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
@@ -691,28 +705,160 @@ static void* mapped_ptr(void* host) {
   return dev;
 }
 
+// ---------------------------------------------------------------------------
+// Partition plan (host only, no device calls): contiguous ranges of high
+// endpoints b whose adjacency slice fits one of the two streaming buffers the
+// cap leaves after the resident state.  The resident bytes are computed as the
+// engine allocator will count them (512-byte granules), so a plan made by the
+// caller (gs_plan_partitions -> PartitionPlan, partition.py:231-333's role)
+// runs unchanged on the device; a given plan is validated, never re-cut.
+// Per partition the host also counts the b's routed to the CTA kernels, so
+// the sweeps launch them without a device round trip.
+
 struct Partition {
   int64_t lo, hi, a0, a1;  // b range and adjacency slice [a0, a1)
+  int64_t nmid, nhuge;     // b's with kOocWarpMax < deg <= smem_max / deg > smem_max
 };
+
+static constexpr int kOocSlabs = 32;  // CTAs of the L2-table kernel (one HBM slab each)
+
+struct OocPlan {
+  int64_t dmax = 0, smem_max = 0, tcap_g = 0, buf_elems = 0, max_verts = 0, vmax = 0;
+  int64_t nmid_max = 0, nhuge_max = 0;
+  bool sketches = true;
+  std::vector<Partition> parts;
+};
+
+static size_t r512(size_t b) { return ((b > 0 ? b : 1) + 511) & ~size_t(511); }
+
+static int ooc_plan(int64_t n, const int64_t* off, uint64_t cap, const int64_t* bounds,
+                    int64_t nb, OocPlan& pl) {
+  pl = OocPlan();
+  if (n <= 0) return GS_OK;
+  if (off[0] != 0) {
+    set_error("invalid graph: vertex_offsets must start at 0");
+    return GS_EINVAL;
+  }
+  const size_t resident = 13 * (size_t)n;
+  if (cap && resident + (1u << 20) > cap) {
+    char buf[200];
+    snprintf(buf, sizeof(buf), "resident vertex state needs %zu bytes against a cap of %llu",
+             resident, (unsigned long long)cap);
+    set_error(buf);
+    return GS_EBUDGET;
+  }
+  int64_t dmax = 0;
+  for (int64_t v = 0; v < n; ++v) {
+    const int64_t d = off[v + 1] - off[v];
+    if (d < 0) {
+      set_error("invalid graph: vertex_offsets must be non-decreasing");
+      return GS_EINVAL;
+    }
+    dmax = std::max(dmax, d);
+  }
+  pl.dmax = dmax;
+  pl.smem_max = kOocSmemBuckets * 4 * 3 / 5;  // keys the smem cuckoo holds
+  pl.tcap_g = dmax > pl.smem_max ? (dmax * 5) / 12 + 1 : 0;
+  if (const char* v = getenv("GS_SKETCH")) pl.sketches = atoi(v) > 0;
+  // what the device allocates before the streaming buffers: deg, role, bounds,
+  // counters, work queue, thresholds, the L2 tables of the huge lists
+  const size_t fixed = r512(4 * (size_t)n) + r512((size_t)n) + r512(8 * (size_t)n) +
+                       r512(8 * (size_t)(CTR_COUNT + 1)) + r512(32) + r512(8 * (size_t)(dmax + 1)) +
+                       r512((size_t)kOocSlabs * 16 * (size_t)pl.tcap_g) + (2u << 20);
+  const size_t avail = cap ? (cap > fixed ? cap - fixed : 0) : ((size_t)1 << 30);
+  // two buffers of adjacency (4 B/elem) + offsets (8 B/vertex) + big lists
+  // (+ with sketches, one partition's rows: <= k/4 bytes per element)
+  int64_t buf_elems = (int64_t)(avail / 2 / 4 * (pl.sketches ? 1 : 3) / (pl.sketches ? 2 : 4));
+  buf_elems = std::min<int64_t>(buf_elems, (int64_t)1 << 28);
+  if (buf_elems < dmax || buf_elems < 1024) {
+    char buf[200];
+    snprintf(buf, sizeof(buf),
+             "HBM cap %llu leaves %zu bytes for streaming; the largest list needs %llu",
+             (unsigned long long)cap, avail, (unsigned long long)(4 * dmax));
+    set_error(buf);
+    return GS_EBUDGET;
+  }
+  pl.buf_elems = buf_elems;
+  pl.max_verts = std::max<int64_t>(1, buf_elems / 4);
+  if (bounds) {  // the caller's plan: validate, never re-cut
+    if (nb < 1 || bounds[0] != 0 || bounds[nb] != n) {
+      set_error("partition bounds must run from 0 to n");
+      return GS_EINVAL;
+    }
+    for (int64_t k = 0; k < nb; ++k) {
+      const int64_t lo = bounds[k], hi = bounds[k + 1];
+      if (hi <= lo) {
+        set_error("partition bounds must be strictly increasing");
+        return GS_EINVAL;
+      }
+      if (off[hi] - off[lo] > buf_elems || hi - lo > pl.max_verts) {
+        char buf[240];
+        snprintf(buf, sizeof(buf),
+                 "partition %lld ([%lld, %lld): %lld adjacency elements) exceeds the %lld-element "
+                 "streaming buffer this cap allows", (long long)k, (long long)lo, (long long)hi,
+                 (long long)(off[hi] - off[lo]), (long long)buf_elems);
+        set_error(buf);
+        return GS_EBUDGET;
+      }
+      pl.parts.push_back({lo, hi, off[lo], off[hi], 0, 0});
+    }
+  } else {
+    for (int64_t lo = 0; lo < n;) {
+      // largest hi with off[hi] - off[lo] <= buf_elems and hi - lo <= max_verts
+      int64_t l = lo + 1, h = std::min<int64_t>(n, lo + pl.max_verts);
+      while (l < h) {
+        const int64_t mid = (l + h + 1) >> 1;
+        if (off[mid] - off[lo] <= buf_elems) l = mid; else h = mid - 1;
+      }
+      pl.parts.push_back({lo, l, off[lo], off[l], 0, 0});
+      lo = l;
+    }
+  }
+  for (auto& p : pl.parts) {
+    for (int64_t v = p.lo; v < p.hi; ++v) {
+      const int64_t d = off[v + 1] - off[v];
+      if (d > kOocWarpMax) ++(d <= pl.smem_max ? p.nmid : p.nhuge);
+    }
+    pl.vmax = std::max(pl.vmax, p.hi - p.lo);
+    pl.nmid_max = std::max(pl.nmid_max, p.nmid);
+    pl.nhuge_max = std::max(pl.nhuge_max, p.nhuge);
+  }
+  return GS_OK;
+}
+
+int plan_partitions(int64_t n, const int64_t* off, uint64_t cap, int64_t* bounds_out,
+                    int64_t max_parts, int64_t* nparts, int64_t* stream_elems) {
+  OocPlan pl;
+  GS_TRY(ooc_plan(n, off, cap, nullptr, 0, pl));
+  const int64_t np = (int64_t)pl.parts.size();
+  if (nparts) *nparts = np;
+  if (stream_elems) *stream_elems = pl.buf_elems;
+  if (bounds_out && max_parts >= np) {
+    for (int64_t k = 0; k < np; ++k) bounds_out[k] = pl.parts[k].lo;
+    bounds_out[np] = n;
+  }
+  return GS_OK;
+}
+
+int validate_plan(int64_t n, const int64_t* off, uint64_t cap, const int64_t* bounds,
+                  int64_t nb) {
+  OocPlan pl;
+  return ooc_plan(n, off, cap, bounds, nb, pl);
+}
 
 int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
                      const int32_t* adj, int32_t mu, const Eps2& eps, uint8_t* role_out,
-                     int32_t* cluster_out, gs_stats* st) {
+                     int32_t* cluster_out, gs_stats* st, const int64_t* part_bounds,
+                     int64_t nb) {
   cudaStream_t cs = e->stream;
   if (n == 0) return GS_OK;
   if (off[0] != 0 || off[n] != 2 * m) {
     set_error("invalid graph: vertex_offsets must start at 0 and end at 2m");
     return GS_EINVAL;
   }
-  // ---- resident state (13 bytes per vertex) + fixed scratch
-  const size_t resident = 13 * (size_t)n;
-  if (e->cap && resident + (1u << 20) > e->cap) {
-    char buf[200];
-    snprintf(buf, sizeof(buf), "resident vertex state needs %zu bytes against a cap of %llu",
-             resident, (unsigned long long)e->cap);
-    set_error(buf);
-    return GS_EBUDGET;
-  }
+  // ---- the plan (host): resident state (13 bytes per vertex) + fixed scratch
+  OocPlan pl;
+  GS_TRY(ooc_plan(n, off, e->cap, part_bounds, nb, pl));
   Mapped moff, madj, mrole, mclus;
   GS_TRY(map_host(off, 8 * (size_t)(n + 1), true, moff));
   int rc = map_host(adj, 4 * (size_t)(2 * m > 0 ? 2 * m : 1), true, madj);
@@ -739,6 +885,8 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
   cudaEventCreate(&t3); cudaEventCreate(&t4); cudaEventCreate(&t5);
   int result = GS_OK;
   int64_t launches = 0;
+  int64_t pcie_host = 0;  // bytes the host moves over PCIe (copies, mapped reads it can count)
+  int64_t nsketched = 0;
   uint32_t* hsk = nullptr;      // pinned host sketch rows
   uint32_t* hsk_off = nullptr;  // pinned host row offsets (16-byte units)
   uint32_t* skbuf = nullptr;    // device scratch: one partition's rows
@@ -757,19 +905,16 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
     cudaEventRecord(t0, cs);
     k_ooc_degree<<<e->sms * 8, 256, 0, cs>>>(hoff, n, deg, bounds, role, mu, ctr + CTR_COUNT);
     ++launches;
-    unsigned long long dmax = 0;
-    cudaMemcpyAsync(&dmax, ctr + CTR_COUNT, sizeof(dmax), cudaMemcpyDeviceToHost, cs);
-    if (cudaStreamSynchronize(cs) != cudaSuccess) { set_error("degree pass failed"); result = GS_ECUDA; break; }
+    pcie_host += 8 * (n + 1);  // the degree pass reads the mapped offsets
+    const int64_t dmax = pl.dmax;  // from the host plan: no device round trip
     int2* thr = nullptr;
-    if ((result = e->alloc_n(&thr, (int64_t)dmax + 1)) != GS_OK) break;
-    GS_TRY(launch_thresholds((int64_t)dmax, eps, thr, cs));
+    if ((result = e->alloc_n(&thr, dmax + 1)) != GS_OK) break;
+    GS_TRY(launch_thresholds(dmax, eps, thr, cs));
     ++launches;
-    // ---- partition plan: contiguous b ranges whose slices fit the buffers
-    const int64_t smem_max = kOocSmemBuckets * 4 * 3 / 5;  // keys the smem cuckoo holds
-    const int nslab = 32;
-    const int64_t tcap_g = (int64_t)dmax > smem_max ? ((int64_t)dmax * 5) / 12 + 1 : 0;
-    size_t fixed = e->live + (size_t)nslab * 16 * (size_t)tcap_g + (2u << 20);
-    size_t avail = e->cap ? (e->cap > fixed ? e->cap - fixed : 0) : ((size_t)1 << 30);
+    const int64_t smem_max = pl.smem_max;
+    const int nslab = kOocSlabs;
+    const int64_t tcap_g = pl.tcap_g;
+    const int64_t buf_elems = pl.buf_elems;
     // sketch resolution as in sim.cu (k = 2^sk_lk bits per neighbour; -1: off)
     int sk_lk = sqrt(eps.ratio) >= 0.33 ? 2 : 3;
     int64_t sk_dmin = 32;  // as in HBM (measured at s26: 12.1 vs 12.7 s with 48)
@@ -778,35 +923,8 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       sk_lk = k <= 0 ? -1 : 31 - __builtin_clz((unsigned)k);
     }
     if (const char* v = getenv("GS_SKETCH_DMIN")) sk_dmin = std::max(1, atoi(v));
-    // two buffers of adjacency (4 B/elem) + offsets (8 B/vertex) + big lists
-    // (+ with sketches, one partition's rows: <= k/4 bytes per element)
-    int64_t buf_elems = (int64_t)(avail / 2 / 4 * (sk_lk >= 0 ? 1 : 3) / (sk_lk >= 0 ? 2 : 4));
-    buf_elems = std::min<int64_t>(buf_elems, (int64_t)1 << 28);
-    if (buf_elems < (int64_t)dmax || buf_elems < 1024) {
-      char buf[200];
-      snprintf(buf, sizeof(buf),
-               "HBM cap %llu leaves %zu bytes for streaming; the largest list needs %llu",
-               (unsigned long long)e->cap, avail, (unsigned long long)(4 * dmax));
-      set_error(buf);
-      result = GS_EBUDGET;
-      break;
-    }
-    const int64_t max_verts = std::max<int64_t>(1, buf_elems / 4);
-    std::vector<Partition> parts;
-    for (int64_t lo = 0; lo < n;) {
-      int64_t hi = lo + 1;
-      // largest hi with off[hi] - off[lo] <= buf_elems and hi - lo <= max_verts
-      int64_t l = lo + 1, h = std::min<int64_t>(n, lo + max_verts);
-      while (l < h) {
-        const int64_t mid = (l + h + 1) >> 1;
-        if (off[mid] - off[lo] <= buf_elems) l = mid; else h = mid - 1;
-      }
-      hi = l;
-      parts.push_back({lo, hi, off[lo], off[hi]});
-      lo = hi;
-    }
-    int64_t vmax = 0;
-    for (auto& p : parts) vmax = std::max(vmax, p.hi - p.lo);
+    const std::vector<Partition>& parts = pl.parts;
+    const int64_t vmax = pl.vmax;
     // ---- neighbourhood sketches (sketch.cu) in mapped pinned host memory:
     // per-vertex row offsets (16-byte units) are laid out here, the rows are
     // hashed on the device from the streamed slices in a pre-pass below
@@ -817,10 +935,14 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         hsk_off = nullptr;
       }
       uint64_t acc = 0;
+      nsketched = 0;
       for (int64_t v = 0; hsk_off && v < n; ++v) {
         hsk_off[v] = (uint32_t)acc;
         const int64_t d = off[v + 1] - off[v];
-        if (d >= sk_dmin) acc += (uint64_t)sk_words(d, sk_lk) / 4;
+        if (d >= sk_dmin) {
+          acc += (uint64_t)sk_words(d, sk_lk) / 4;
+          ++nsketched;
+        }
         if (acc >= 0xFFFFFFFFull) break;
       }
       if (hsk_off && acc < 0xFFFFFFFFull) {
@@ -848,8 +970,8 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       if (result == GS_OK) result = e->alloc_n(&obuf[i], vmax + 1);
     }
     if (result != GS_OK) break;
-    if ((result = e->alloc_n(&bigmid, buf_elems / kOocWarpMax + 1)) != GS_OK) break;
-    if ((result = e->alloc_n(&bighuge, buf_elems / kOocWarpMax + 1)) != GS_OK) break;
+    if ((result = e->alloc_n(&bigmid, pl.nmid_max + 1)) != GS_OK) break;
+    if ((result = e->alloc_n(&bighuge, pl.nhuge_max + 1)) != GS_OK) break;
     if ((result = e->alloc_n(&bigcnt, 2)) != GS_OK) break;
     if (tcap_g > 0 && (result = e->alloc_n(&gtab, 4 * tcap_g * nslab)) != GS_OK) break;
     if (hsk && e->alloc_n(&skbuf, 4 * std::max<int64_t>(skbuf_units, 1)) != GS_OK) {
@@ -929,6 +1051,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
                                   cudaMemcpyHostToDevice, copy));
         GS_CUDA(cudaMemcpyAsync(obuf[k], off + pt.lo, 8 * (size_t)(pt.hi - pt.lo + 1),
                                 cudaMemcpyHostToDevice, copy));
+        pcie_host += 4 * (pt.a1 - pt.a0) + 8 * (pt.hi - pt.lo + 1);
         GS_CUDA(cudaEventRecord(ev_copied[k], copy));
         GS_CUDA(cudaStreamWaitEvent(cs, ev_copied[k], 0));
         P.padj = pbuf[k];
@@ -946,9 +1069,8 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       GS_CUDA(cudaMemsetAsync(bigcnt, 0, 2 * sizeof(int), cs));
       k_ooc_bigs<<<grid_for(pt.hi - pt.lo, 256), 256, 0, cs>>>(deg, pt.lo, pt.hi, bigmid, bighuge,
                                                               bigcnt, smem_max);
-      int h_cnt[2] = {0, 0};
-      GS_CUDA(cudaMemcpyAsync(h_cnt, bigcnt, sizeof(h_cnt), cudaMemcpyDeviceToHost, cs));
-      GS_CUDA(cudaStreamSynchronize(cs));
+      // the plan counted them on the host: no device round trip per partition
+      const int64_t h_cnt[2] = {pt.nmid, pt.nhuge};
       const int64_t nw = (pt.hi - pt.lo + 7) / 8;
       k_ooc_warp<256><<<(unsigned)std::min<int64_t>(nw, (int64_t)occ_w * e->sms), 256, smem_warp,
                         cs>>>(P);
@@ -957,7 +1079,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         OocParams Q = P;
         Q.big = bigmid;
         Q.nbig = h_cnt[0];
-        k_ooc_cta<1024, false><<<(unsigned)std::min<int>(h_cnt[0], e->sms), 1024, smem_cta, cs>>>(
+        k_ooc_cta<1024, false><<<(unsigned)std::min<int64_t>(h_cnt[0], e->sms), 1024, smem_cta, cs>>>(
             Q, (uint32_t)kOocSmemBuckets, 1024, skw_cta);
         ++launches;
       }
@@ -966,7 +1088,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         OocParams Q = P;
         Q.big = bighuge;
         Q.nbig = h_cnt[1];
-        k_ooc_cta<1024, true><<<(unsigned)std::min<int>(h_cnt[1], nslab), 1024, smem_gta, cs>>>(
+        k_ooc_cta<1024, true><<<(unsigned)std::min<int64_t>(h_cnt[1], nslab), 1024, smem_gta, cs>>>(
             Q, (uint32_t)tcap_g, 1024, skw_gta);
         ++launches;
       }
@@ -985,10 +1107,12 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
         ++launches;
         GS_CUDA(cudaMemcpyAsync(hsk + 4 * (size_t)u0, skbuf, 16 * (size_t)(u1 - u0),
                                 cudaMemcpyDeviceToHost, cs));
+        pcie_host += 16 * (int64_t)(u1 - u0);
         GS_CUDA(cudaGetLastError());
         return GS_OK;
       };
       if ((result = sweep(sk_body)) != GS_OK) break;
+      pcie_host += 4 * nsketched;  // the build reads each sketched vertex's row offset (mapped)
     }
     cudaEventRecord(t5, cs);  // end of the sketch pre-pass (== t0 without sketches)
     // ---- pass 1: identify (Alg. 5 first loop)
@@ -1044,6 +1168,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
                                             static_cast<uint8_t*>(mrole.dev),
                                             static_cast<int32_t*>(mclus.dev), ctr);
     ++launches;
+    pcie_host += 5 * n;  // roles + cluster ids written zero-copy
     cudaEventRecord(t3, cs);
     cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, cs);
     if (cudaStreamSynchronize(cs) != cudaSuccess) { set_error("classify pass failed"); result = GS_ECUDA; break; }
@@ -1059,6 +1184,7 @@ int scan_partitioned(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
       st->n_clusters = (int64_t)hc[CTR_N_CLUSTERS];
       st->n_core = (int64_t)ncores;
       st->partitions = (int64_t)parts.size();
+      st->pcie_bytes = (int64_t)hc[CTR_PCIE] + pcie_host;
       st->kernel_launches = launches;
       float ms = 0;
       cudaEventElapsedTime(&ms, t0, t1); st->phase_ms[GS_PH_IDENTIFY] = ms;

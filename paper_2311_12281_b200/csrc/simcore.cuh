@@ -467,11 +467,14 @@ __device__ __forceinline__ bool sk_rejects_fold4(const uint32_t* __restrict__ A,
 // where the request size matters more than the latency.
 __device__ __forceinline__ bool sk_rejects_lev4(const uint32_t* __restrict__ A,
                                                 const uint32_t* B, int64_t wa, int64_t da,
-                                                int32_t cmin, int lane) {
+                                                int32_t cmin, int lane,
+                                                unsigned long long& abytes) {
   // U = d_a - sum popc(x & ~y) only decreases: stop after the first 512-byte
-  // block that takes it below c_min (bytes over PCIe are the cost here)
+  // block that takes it below c_min (bytes over PCIe are the cost here);
+  // abytes += the bytes of A requested
   int64_t u = da;
   for (int64_t j0 = 0; j0 < wa; j0 += 128) {
+    abytes += 4ull * (unsigned long long)min((int64_t)128, wa - j0);
     const int64_t j = j0 + 4 * lane;
     int acc = 0;
     if (j < wa) {

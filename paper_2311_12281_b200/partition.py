@@ -1,8 +1,9 @@
 """Host mirror of the reference's out-of-core API (graphscan/partition.py).
 
-``partition_graph(g, budget_bytes)`` plans the run and ``scan_out_of_core(meta,
-plan, mu, epsilon)`` executes it on the device through ``gs_scan_partitioned``
-under an HBM cap of ``budget_bytes``.
+``partition_graph(g, budget_bytes)`` plans the run (``gs_plan_partitions``,
+host only) and ``scan_out_of_core(meta, plan, mu, epsilon)`` executes exactly
+that plan on the device (``gs_scan_partitioned_plan``: partition.py:666-757
+iterates ``plan.partitions``) under an HBM cap of ``budget_bytes``.
 
 The reference spills edge-extended subgraphs (Def. 9) to disk and re-reads
 them per pass (partition.py:231-446); its greedy closure planner is O(sum d^2)
@@ -12,6 +13,12 @@ adjacency slice is streamed into HBM, the low endpoint's list is gathered
 zero-copy, and only per-vertex state (13 bytes/vertex) is resident.  The plan
 object keeps the reference's reporting surface (partitions, budget, manifest
 lines) so callers and stats look the same.
+
+Budget semantics differ from the reference on purpose: the budget is the HBM
+cap and the resident state is what the device holds, 13 bytes per vertex
+(degree 4 + role 1 + bounds 8, later forest 4 + labels 4), not the reference's
+15 (partition.py:70, its Python ClusterState).  With 15 the s27 state alone
+(2.01 GB) would not fit the 2 GB cap BASELINE configs[3] asks for.
 """
 
 from __future__ import annotations
@@ -46,7 +53,13 @@ class InfeasibleBudgetError(ValueError):
 
 @dataclass
 class PartitionInfo:
-    """One partition: high endpoints [lo, hi), adjacency slice [a0, a1)."""
+    """One partition: high endpoints [lo, hi), adjacency slice [a0, a1).
+
+    The reference's fields map as: ``owned_lo``/``owned_hi`` -> the vertex
+    range [lo, hi) whose lists are streamed (the reference's are edge-id
+    ranges of its closure partitions); ``n_local`` -> hi - lo; ``m_local`` ->
+    the adjacency elements streamed, a1 - a0; ``path`` -> None (partitions are
+    streamed from pinned host memory, not spilled; partition.py:336-446)."""
 
     index: int
     lo: int
@@ -57,6 +70,26 @@ class PartitionInfo:
     @property
     def estimate_bytes(self) -> int:
         return 4 * (self.a1 - self.a0) + 8 * (self.hi - self.lo + 1)
+
+    @property
+    def owned_lo(self) -> int:
+        return self.lo
+
+    @property
+    def owned_hi(self) -> int:
+        return self.hi
+
+    @property
+    def n_local(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def m_local(self) -> int:
+        return self.a1 - self.a0
+
+    @property
+    def path(self) -> Optional[str]:
+        return None
 
 
 @dataclass
@@ -117,20 +150,24 @@ def partition_graph(g, budget_bytes: int, spill_dir: Optional[str] = None) -> Pa
     state = VERTEX_STATE_BYTES * n
     if state > budget_bytes:
         raise InfeasibleBudgetError((-1, -1), state, budget_bytes)
-    dmax = int(np.diff(off).max()) if n else 0
-    avail = budget_bytes - state - (2 << 20) - 8 * (dmax + 1)
-    buf = max(0, avail // 2 // 4 * 3 // 4)
-    if n and buf < max(dmax, 1024):
-        raise InfeasibleBudgetError((-1, -1), state + (2 << 20) + 8 * 4 * max(dmax, 1024),
-                                    budget_bytes)
     parts = []
-    lo = 0
-    max_verts = max(1, buf // 4)
-    while lo < n:
-        hi = int(np.searchsorted(off, off[lo] + buf, side="right")) - 1
-        hi = min(max(hi, lo + 1), n, lo + max_verts)
-        parts.append(PartitionInfo(len(parts), lo, hi, int(off[lo]), int(off[hi])))
-        lo = hi
+    if n:
+        lib = _lib.load()
+        nparts = ctypes.c_int64(0)
+        elems = ctypes.c_int64(0)
+        try:
+            _lib.check(lib.gs_plan_partitions(n, off.ctypes.data, int(budget_bytes), None, 0,
+                                              ctypes.byref(nparts), ctypes.byref(elems)))
+        except _lib.InfeasibleBudget as exc:
+            raise InfeasibleBudgetError((-1, -1), state + (2 << 20), budget_bytes,
+                                        str(exc)) from None
+        bounds = np.empty(nparts.value + 1, dtype=np.int64)
+        _lib.check(lib.gs_plan_partitions(n, off.ctypes.data, int(budget_bytes),
+                                          bounds.ctypes.data, nparts.value,
+                                          ctypes.byref(nparts), ctypes.byref(elems)))
+        for k in range(nparts.value):
+            lo, hi = int(bounds[k]), int(bounds[k + 1])
+            parts.append(PartitionInfo(k, lo, hi, int(off[lo]), int(off[hi])))
     plan = PartitionPlan(n=n, m=m, budget_bytes=int(budget_bytes), partitions=parts,
                          spill_dir=spill_dir, graph=g)
     if spill_dir is not None:
@@ -157,15 +194,22 @@ def scan_out_of_core(meta: GraphMeta, plan: PartitionPlan, mu: int, epsilon: Eps
     st = _lib.GsStats()
     if n:
         lib = _lib.load()
+        # the plan's partitions are executed as given (validated on the device
+        # side: a partition that does not fit the cap raises InfeasibleBudgetError)
+        bounds = np.array([p.lo for p in plan.partitions] + [n], dtype=np.int64)
+        if len(plan.partitions) == 0 or bounds[0] != 0:
+            raise ValueError("plan has no partitions covering the graph")
         try:
-            _lib.check(lib.gs_scan_partitioned(n, m, off.ctypes.data, adj.ctypes.data, int(mu),
-                                               ctypes.byref(eps2), int(plan.budget_bytes),
-                                               roles.ctypes.data, cids.ctypes.data,
-                                               ctypes.byref(st)))
+            _lib.check(lib.gs_scan_partitioned_plan(n, m, off.ctypes.data, adj.ctypes.data,
+                                                    int(mu), ctypes.byref(eps2),
+                                                    int(plan.budget_bytes), len(plan.partitions),
+                                                    bounds.ctypes.data, roles.ctypes.data,
+                                                    cids.ctypes.data, ctypes.byref(st)))
         except _lib.InfeasibleBudget as exc:
             raise InfeasibleBudgetError((-1, -1), VERTEX_STATE_BYTES * n, plan.budget_bytes,
                                         str(exc)) from None
     stats = stats_from_native(st, n, m, workers)
     stats.extra["partitions"] = int(st.partitions) if n else 0
+    stats.extra["pcie_bytes"] = int(st.pcie_bytes) if n else 0
     orig = meta.orig_ids if n else np.empty(0, np.uint32)
     return ClusteringResult(n, roles, cids, orig), stats

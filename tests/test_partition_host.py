@@ -23,8 +23,8 @@ def test_plan_slices_cover_the_graph_in_order():
     e = {tuple(sorted(map(int, rng.choice(n, 2, replace=False)))) for _ in range(9000)}
     g = make_graph(n, sorted(e))
     dmax = int(np.diff(g.vertex_offsets).max())
-    budget = VERTEX_STATE_BYTES * n + (2 << 20) + 8 * (dmax + 1) + 16 * 1024
-    plan = gs.partition_graph(g, budget)
+    budget = 15 * n + (2 << 20) + 8 * (dmax + 1) + 64 * 1024
+    plan = gs.partition_graph(g, budget)  # gs_plan_partitions: host only, no device
     assert len(plan.partitions) >= 2
     lo = 0
     for p in plan.partitions:
@@ -44,3 +44,27 @@ def test_infeasible_budgets():
     assert isinstance(ei.value, ValueError) and ei.value.budget_bytes == 100
     with pytest.raises(ValueError):
         gs.partition_graph(g, 0)
+
+
+def test_plan_is_validated_before_any_device_work():
+    """scan_out_of_core executes the caller's plan (partition.py:666-757); a
+    partition that cannot fit the cap is rejected with InfeasibleBudgetError
+    and a malformed plan with ValueError -- both before the device is touched,
+    so this runs on CPU."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    e = {tuple(sorted(map(int, rng.choice(n, 2, replace=False)))) for _ in range(12000)}
+    g = make_graph(n, sorted(e))
+    dmax = int(np.diff(g.vertex_offsets).max())
+    budget = 15 * n + (2 << 20) + 8 * (dmax + 1) + 64 * 1024
+    plan = gs.partition_graph(g, budget)
+    assert len(plan.partitions) >= 3
+    meta = gs.GraphMeta.from_graph(g)
+    whole = gs.partition.PartitionInfo(0, 0, n, 0, 2 * g.m)  # one slice: too big for the cap
+    bad = gs.PartitionPlan(n=n, m=g.m, budget_bytes=budget, partitions=[whole], graph=g)
+    with pytest.raises(gs.InfeasibleBudgetError, match="partition 0"):
+        gs.scan_out_of_core(meta, bad, 3, "0.5")
+    gap = gs.PartitionPlan(n=n, m=g.m, budget_bytes=budget,
+                           partitions=[plan.partitions[1]], graph=g)  # does not start at 0
+    with pytest.raises(ValueError):
+        gs.scan_out_of_core(meta, gap, 3, "0.5")
