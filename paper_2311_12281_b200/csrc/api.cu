@@ -139,6 +139,19 @@ void gs_engine::kev_mark(int i) {
   cudaEventRecord(kev[i], stream);
 }
 
+void gs_engine::kev_class_ms(double* out) {
+  for (int c = 0; c < kKernelClasses; ++c) {
+    const int a = c == 0 ? 0 : c + 1, b = c == 0 ? 1 : c + 2;
+    float t = 0;
+    if (g.m > 0 && kev[a] && kev[b] && cudaEventSynchronize(kev[b]) == cudaSuccess &&
+        cudaEventElapsedTime(&t, kev[a], kev[b]) != cudaSuccess) {
+      cudaGetLastError();  // an event of this class was not recorded in this scan
+      t = 0;
+    }
+    out[c] = t;
+  }
+}
+
 void gs_engine::release(void* p) {
   if (!p) return;
   auto it = sizes.find(p);
@@ -444,6 +457,7 @@ int gs_engine_phase_begin(gs_engine* e, int32_t mu, const gs_eps2* eps2) {
   GS_TRY(check_eps(eps2));
   e->launches = 0;
   for (auto& x : e->phase_ms) x = 0;
+  e->kev_on = true;  // per-class identify timing, read at gs_engine_phase_finish
   return timed(e, GS_PH_IDENTIFY, [&] { return phase_begin(e, mu, to_eps(eps2)); });
 }
 
@@ -495,6 +509,10 @@ int gs_engine_phase_attach(gs_engine* e, int32_t* labels_dev) {
 
 int gs_engine_phase_finish(gs_engine* e, const int32_t* labels_dev, uint8_t* role_out,
                            int32_t* cluster_out, int out_on_device, gs_stats* stats) {
+  struct KevOff {  // class timing ends with the scan, whichever way this returns
+    gs_engine* e;
+    ~KevOff() { if (e) e->kev_on = false; }
+  } kev_off{e};
   GS_TRY(phase_guard(e));
   if (stats) memset(stats, 0, sizeof(*stats));
   if (labels_dev) GS_TRY(phase_import_labels(e, labels_dev));
@@ -507,6 +525,7 @@ int gs_engine_phase_finish(gs_engine* e, const int32_t* labels_dev, uint8_t* rol
     const double d2h = stats->phase_ms[GS_PH_D2H];
     for (int i = 0; i < GS_PH_COUNT; ++i) stats->phase_ms[i] = e->phase_ms[i];
     stats->phase_ms[GS_PH_D2H] = d2h;
+    if (e->kev_on) e->kev_class_ms(stats->phase_ms + GS_PH_K_PREP);
     stats->phase_ms[GS_PH_CLASSIFY] -= d2h;
     stats->phase_ms[GS_PH_H2D] = e->last_h2d_ms;
     stats->phase_ms[GS_PH_BUILD] = e->last_build_ms;

@@ -715,11 +715,7 @@ int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,
     st->phase_ms[GS_PH_CLEANUP] = tm.ms(1, 2);
     st->phase_ms[GS_PH_CLUSTER] = tm.ms(2, 3);
     st->phase_ms[GS_PH_CLASSIFY] = tm.ms(4, 5) - st->phase_ms[GS_PH_D2H];
-    for (int c = 0; c < kKernelClasses; ++c) {
-      float t = 0;
-      if (e->g.m > 0 && e->kev[c] && e->kev[c + 1]) cudaEventElapsedTime(&t, e->kev[c], e->kev[c + 1]);
-      st->phase_ms[GS_PH_K_PREP + c] = t;
-    }
+    e->kev_class_ms(st->phase_ms + GS_PH_K_PREP);
   }
   e->kev_on = false;
   return GS_OK;

@@ -188,12 +188,14 @@ struct gs_engine {
   // host-side pinned staging for counters
   unsigned long long* h_ctr = nullptr;
   std::vector<cudaEvent_t> ev;
-  // identify-pass kernel-class timing: kev[0] before the preparation, kev[1 + c]
-  // after class c (prep, huge, large, medium, small, tiny); recorded when
-  // kev_on, read by run_scan into gs_stats.phase_ms[GS_PH_K_PREP ..]
-  cudaEvent_t kev[gs::kKernelClasses + 1] = {};
+  // identify-pass kernel-class timing: kev[0] / kev[1] around the preparation,
+  // kev[2] at the start of the sweep, kev[2 + c] after class c (huge, large,
+  // medium, small, tiny); recorded when kev_on, read into
+  // gs_stats.phase_ms[GS_PH_K_PREP ..] (kev_class_ms)
+  cudaEvent_t kev[gs::kKernelClasses + 2] = {};
   bool kev_on = false;
   void kev_mark(int i);
+  void kev_class_ms(double* out);  // [kKernelClasses], synchronises the events
 
   int alloc(void** p, size_t bytes);
   void release(void* p);

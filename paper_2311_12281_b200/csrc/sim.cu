@@ -899,6 +899,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.shard_world = e->shard_world;
   const bool ident = mode == MODE_IDENTIFY;
   auto slot = [&](int c) { P.bslot = ident ? c : CTR_B_OTHER; };
+  if (ident) e->kev_mark(2);
   {
     const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
     P.hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
@@ -928,19 +929,19 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, g.dmax,
                                      e->stream)));
   }
-  if (ident) e->kev_mark(2);
+  if (ident) e->kev_mark(3);
   // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB) + cuckoo table
   // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
   // per candidate of a chunk); the small class runs warp-per-b
   slot(CTR_B_LARGE);
   GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
-  if (ident) e->kev_mark(3);
+  if (ident) e->kev_mark(4);
   slot(CTR_B_MED);
   GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024, dcls[1], e->stream)));
-  if (ident) e->kev_mark(4);
+  if (ident) e->kev_mark(5);
   slot(CTR_B_SMALL);
   GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
-  if (ident) e->kev_mark(5);
+  if (ident) e->kev_mark(6);
   slot(CTR_B_TINY);
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
@@ -949,7 +950,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     e->launches++;
     GS_CUDA(cudaGetLastError());
   }
-  if (ident) e->kev_mark(6);
+  if (ident) e->kev_mark(7);
   if (P.gtab) {
     GS_CUDA(cudaStreamSynchronize(e->stream));
     e->release(P.gtab);

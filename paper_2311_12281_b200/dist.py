@@ -78,6 +78,13 @@ def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
     dist.all_reduce(ph, op=dist.ReduceOp.MAX, group=group)
     for k, v in zip(ints, t.tolist()):
         setattr(st, k, int(v))
+    kb = torch.tensor(list(st.kernel_bytes) + [st.wsim_bytes, st.pcie_bytes], dtype=torch.int64,
+                      device=dev)
+    dist.all_reduce(kb, op=dist.ReduceOp.SUM, group=group)
+    kbl = kb.tolist()
+    for i in range(6):
+        st.kernel_bytes[i] = int(kbl[i])
+    st.wsim_bytes, st.pcie_bytes = int(kbl[6]), int(kbl[7])
     for i, v in enumerate(ph.tolist()):
         st.phase_ms[i] = v
     return st
