@@ -173,3 +173,56 @@ class ShardedScan:
         _lib.check(lib.gs_engine_phase_finish(h, labels_ptr, role_out, cluster_out,
                                               out_on_device, ctypes.byref(st)))
         return reduce_stats(st, g)
+
+
+def init_from_env() -> tuple[int, int, int]:
+    """Join the process group torchrun set up (RANK / WORLD_SIZE / LOCAL_RANK),
+    one GPU per rank over NCCL (GS_DIST_BACKEND=gloo: ranks may share a GPU, a
+    functional check).  Returns (rank, world, local device)."""
+    import os
+
+    backend = os.environ.get("GS_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    if ndev == 0:
+        raise RuntimeError("the sharded scan needs CUDA devices; none is visible")
+    if backend == "nccl" and local >= ndev:
+        raise RuntimeError(f"rank {local} has no GPU of its own ({ndev} visible)")
+    local %= ndev
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist.get_rank(), dist.get_world_size(), local
+
+
+def scan_sharded(g, mu: int, epsilon, *, workers: int = 1, group=None):
+    """scan_in_memory (scan.py:965-982) over the ranks of an initialised
+    process group: every rank passes the same graph and gets the same
+    (ClusteringResult, StatsReport); the edges are split b % world, the build
+    by rank-space rows, and the four exchanges run over NCCL."""
+    import numpy as np
+
+    from .graph import as_array, graph_arrays
+    from .scan import ClusteringResult, _validate, stats_from_native
+
+    f = _validate(mu, workers, epsilon)
+    n, m, off, adj = graph_arrays(g)
+    orig = as_array(g.orig_ids, np.uint32) if n else np.empty(0, np.uint32)
+    roles = np.empty(n, dtype=np.uint8)
+    cids = np.empty(n, dtype=np.int32)
+    st = _lib.GsStats()
+    if n:
+        eng = _lib.Engine(device=torch.cuda.current_device())
+        try:
+            shard = ShardedScan(eng, n, group)
+            shard.load_csr(m, off.ctypes.data, adj.ctypes.data, 0)
+            eps2 = _lib.eps2_struct(f, int(np.diff(off).max()))
+            shard.run(int(mu), eps2, roles.ctypes.data, cids.ctypes.data, 0, st)
+        finally:
+            eng.close()
+    stats = stats_from_native(st, n, m, workers)
+    stats.extra["devices"] = dist.get_world_size(group)
+    return ClusteringResult(n, roles, cids, orig), stats
