@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   __shared__ uint32_t s_stash[kStash];
   __shared__ unsigned long long s_ctr[LC_N];
   const int tid = threadIdx.x, lane = tid & 31;
-  SharedCtr lc{s_ctr};
+  HotCtr lc;
   shared_ctr_init(s_ctr);
   Cuckoo C;
   C.tab = GTAB ? (P.gtab + (int64_t)blockIdx.x * P.gtab_stride) : tab_s;
@@ -455,8 +455,12 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
         if (!sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
             2 * sk_words(db, P.sk_lk) <= skw) {  // b's sketch and its folds, once per b
           const int64_t wb = sk_words(db, P.sk_lk);
-          sk_stage_levels(sk_row(P, b, db, wb), wb, sk_lev, tid, NT, [] { __syncthreads(); });
-          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)wb);
+          // the levels are precomputed (sketch.cu): one coalesced copy, one barrier
+          const uint4* src = reinterpret_cast<const uint4*>(sk_row(P, b, db, wb));
+          uint4* dst = reinterpret_cast<uint4*>(sk_lev);
+          for (int64_t i = tid; i < (2 * wb - 4) / 4; i += NT) dst[i] = __ldg(src + i);
+          __syncthreads();
+          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)(2 * wb - 4));
           sk_staged = true;
         }
         if (tpass) {
@@ -553,14 +557,12 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           // long rows are left to the warp (thread-pass imbalance)
           if ((!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
-            skbytes = 4ull * (unsigned long long)(lev ? wa : wa + wb);
+            skbytes = 4ull * (unsigned long long)(lev ? wa : 2 * wa);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
-            if (lev)
-              skd = sk_rejects_lev(A, sk_lev + 2 * (wb - wa), wa, ad.y, jc.y, lane);
-            else if (GTAB)  // huge b beyond the staged levels: wide loads from global
-              skd = sk_rejects_fold4(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
-            else
-              skd = sk_rejects_fold(A, sk_row(P, b, db, wb), wa, wb, ad.y, jc.y, lane);
+            // b's level at a's resolution: staged in shared memory, or read from
+            // its precomputed slot in global memory (huge b beyond the staged room)
+            skd = sk_rejects_lev(A, lev ? sk_lev + 2 * (wb - wa) : sk_row(P, b, db, wb) + 2 * (wb - wa),
+                                 wa, ad.y, jc.y, lane);
           }
           const bool res = !skd && scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo,
                                                        rmax, C, nstash, nb, nlo, lane, scanned,
@@ -587,8 +589,10 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     if (built) {  // clear the bitmap words this b set (O(deg b), not O(R))
       for (int64_t i = s_nlo + tid; i < db; i += NT) bm[((uint32_t)nb[i] - hub_lo) >> 5] = 0u;
     }
+    hot_flush_warp(lc, s_ctr);
     __syncthreads();  // bitmap clean and s_item read by all before the next b
   }
+  hot_flush_warp(lc, s_ctr);
   shared_ctr_flush(P, s_ctr);
 }
 
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
   C.stash = tab + 4 * kWarpBuckets;
   C.nstash = reinterpret_cast<int*>(C.stash + kStash);
   __shared__ unsigned long long s_ctr[LC_N];
-  SharedCtr lc{s_ctr};
+  HotCtr lc;
   shared_ctr_init(s_ctr);
   for (;;) {
     int item = 0;
@@ -653,8 +657,9 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
             if (P.sk_thread && P.sk != nullptr && db >= P.sk_dmin && sk_try(P, da, db, cmin)) {
               const int64_t wa = sk_words(da, P.sk_lk), wbb = sk_words(db, P.sk_lk);
               unsigned long long words = 0;
-              const bool rej = sk_thread_rejects(sk_row(P, a, da, wa), sk_row(P, b, db, wbb), wa,
-                                                 wbb, da, cmin, true, words);
+              const bool rej = sk_thread_rejects(sk_row(P, a, da, wa),
+                                                 sk_row(P, b, db, wbb) + 2 * (wbb - wa), wa, wa,
+                                                 da, cmin, true, words);
               ctr_add(lc, LC_BYTES, 4ull * words + (rej ? kBytesRec : 0u));
               if (rej) {
                 st = 4;
@@ -711,10 +716,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
         unsigned long long skbytes = 0;
         if (!P.sk_thread && sk_try(P, sda, db, scm)) {
           const int64_t wa = sk_words(sda, P.sk_lk);
-          skbytes = 4ull * (unsigned long long)(wa + wb);
-          // S_b (<= 128 words at k <= 8) folded from global: L1-resident
-          skd = sk_rejects_fold(sk_row(P, sa, sda, wa), sk_row(P, b, db, wb), wa, wb, sda, scm,
-                                lane);
+          skbytes = 4ull * (unsigned long long)(2 * wa);
+          // S_b's level at a's resolution, from its precomputed slot
+          skd = sk_rejects_lev(sk_row(P, sa, sda, wa), sk_row(P, b, db, wb) + 2 * (wb - wa), wa,
+                               sda, scm, lane);
         }
         const bool res = !skd && scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu,
                                                       0, C, nstash, nb, db, lane, scanned, first);
@@ -733,8 +738,10 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
       apply_bounds(P.bounds, P.role, b, bsim, bdis, P.mu);
       ctr_add(lc, LC_BYTES, 16);
     }
+    hot_flush_warp(lc, s_ctr);
     __syncwarp();
   }
+  hot_flush_warp(lc, s_ctr);
   shared_ctr_flush(P, s_ctr);
 }
 

@@ -94,8 +94,16 @@ struct LocalCtr {
                      sketch = 0, wsim = 0;
 };
 
-struct SharedCtr {
-  unsigned long long* v;  // [LC_N], shared memory
+// Counters of the persistent CTA / warp kernels: a few registers per thread
+// (bytes 64-bit, the rest 32-bit), folded into a CTA-wide shared array once per
+// high endpoint b (warp reduction + one shared atomic per warp and counter):
+// per-event shared atomics on one address serialise the whole CTA, and eight
+// 64-bit register counters per thread cost spills at the 64-register limit.
+// evals = sketch-decided + intersected here (the O(1)-decided edges these
+// kernels re-meet in union / attach are not counted, see record_edge).
+struct HotCtr {
+  unsigned long long bytes = 0;
+  uint32_t sketch = 0, inters = 0, probes = 0, wsim_d = 0;  // wsim in units of 4 bytes
 };
 
 __device__ __forceinline__ void ctr_add(LocalCtr& c, int i, unsigned long long x) {
@@ -111,8 +119,38 @@ __device__ __forceinline__ void ctr_add(LocalCtr& c, int i, unsigned long long x
   }
 }
 
-__device__ __forceinline__ void ctr_add(const SharedCtr& c, int i, unsigned long long x) {
-  if (x) atomicAdd(c.v + i, x);
+__device__ __forceinline__ void ctr_add(HotCtr& c, int i, unsigned long long x) {
+  switch (i) {
+    case LC_BYTES: c.bytes += x; break;
+    case LC_SKETCH: c.sketch += (uint32_t)x; break;
+    case LC_INTERS: c.inters += (uint32_t)x; break;
+    case LC_PROBES: c.probes += (uint32_t)x; break;
+    case LC_WSIM: c.wsim_d += (uint32_t)(x >> 2); break;
+    default: break;  // LC_EVALS (derived), LC_BOUND (out of core only), LC_RETRIES (record_edge)
+  }
+}
+
+// fold a warp's HotCtr into the CTA's shared array (all 32 lanes call it)
+__device__ __forceinline__ void hot_flush_warp(HotCtr& c, unsigned long long* v) {
+  const unsigned sk = __reduce_add_sync(0xffffffffu, c.sketch);
+  const unsigned in = __reduce_add_sync(0xffffffffu, c.inters);
+  const unsigned pr = __reduce_add_sync(0xffffffffu, c.probes);
+  unsigned long long ws = c.wsim_d, by = c.bytes;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    by += __shfl_xor_sync(0xffffffffu, by, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (sk | in) atomicAdd(v + LC_EVALS, (unsigned long long)sk + in);
+    if (sk) atomicAdd(v + LC_SKETCH, (unsigned long long)sk);
+    if (in) atomicAdd(v + LC_INTERS, (unsigned long long)in);
+    if (pr) atomicAdd(v + LC_PROBES, (unsigned long long)pr);
+    if (ws) atomicAdd(v + LC_WSIM, 4ull * ws);
+    if (by) atomicAdd(v + LC_BYTES, by);
+  }
+  c.bytes = 0;
+  c.sketch = c.inters = c.probes = c.wsim_d = 0;
 }
 
 // global counter of each LC_* index (bytes go to the launch's class slot)
@@ -160,7 +198,7 @@ __device__ __forceinline__ void record_edge(const SimParams& P, int64_t e, int32
   } else if (P.mode == MODE_UNION && similar) {
     unsigned long long r = 0;
     uf_union(P.parent, a, b, r);
-    ctr_add(lc, LC_RETRIES, r);
+    if (r) atomicAdd(&P.ctr[CTR_UNION_RETRIES], r);  // failed CAS hooks: rare
   }
 }
 
@@ -409,9 +447,30 @@ __device__ __forceinline__ bool sk_try(const SimParams& P, int64_t da, int64_t d
   return ef < P.sk_gate * (float)cmin;
 }
 
+// v's sketch slot (2w words: S_v, then its levels; sketch.cu)
 __device__ __forceinline__ const uint32_t* sk_row(const SimParams& P, int64_t v, int64_t d,
                                                   int64_t w) {
-  return P.sk + P.skbase[d] + (v - P.rdeg[d]) * w;
+  return P.sk + P.skbase[d] + (v - P.rdeg[d]) * 2 * w;
+}
+
+// the levels of a row of w words held in `t` (2w words of room): level L
+// (w >> L words) at 2 (w - (w >> L)); threads [i0, i0 + nt) of a warp
+__device__ __forceinline__ void sk_fold_levels(uint32_t* t, int64_t w, int i0, int nt) {
+  for (int64_t lo = 0, x = w; x > 4; lo += x, x >>= 1) {
+    const int64_t h = x >> 1;
+    for (int64_t i = i0; i < h; i += nt) t[lo + x + i] = t[lo + i] | t[lo + h + i];
+    __syncwarp();
+  }
+}
+
+// ... by a CTA (sync = __syncthreads)
+template <class Sync>
+__device__ __forceinline__ void sk_fold_levels(uint32_t* t, int64_t w, int i0, int nt, Sync sync) {
+  for (int64_t lo = 0, x = w; x > 4; lo += x, x >>= 1) {
+    const int64_t h = x >> 1;
+    for (int64_t i = i0; i < h; i += nt) t[lo + x + i] = t[lo + i] | t[lo + h + i];
+    sync();
+  }
 }
 
 // B is S_b already folded to a's wa words (a shared-memory level, sim.cu)

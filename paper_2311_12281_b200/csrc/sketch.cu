@@ -20,6 +20,11 @@
 // -- and it reads k*d_a/8 bytes of a's sketch in one coalesced burst instead
 // of a dependent chain of adjacency steps.  The similar side is never decided
 // by the sketch (no lower bound), so results are unchanged bit for bit.
+//
+// Layout: every row carries its folds ("levels"): S_v (w words), S_v folded to
+// w/2, w/4, ... 4 words, back to back in a 2w-word slot -- level L (w >> L
+// words) at word 2 (w - (w >> L)).  So S_b at a's resolution (w_a words) is a
+// plain read of w_a words at 2 (w_b - w_a), by any kernel, without folding.
 #include <algorithm>
 
 #include <cub/cub.cuh>
@@ -33,7 +38,7 @@ __global__ void k_sk_sizes(int64_t dmax, int64_t dmin, int lk, const int32_t* __
                            int64_t* __restrict__ sizes) {
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d <= dmax + 1;
        d += (int64_t)gridDim.x * blockDim.x)
-    sizes[d] = (d >= dmin && d <= dmax) ? (int64_t)(rdeg[d + 1] - rdeg[d]) * sk_words(d, lk) : 0;
+    sizes[d] = (d >= dmin && d <= dmax) ? (int64_t)(rdeg[d + 1] - rdeg[d]) * 2 * sk_words(d, lk) : 0;
 }
 
 // warp per vertex, sketch of <= WMAX words built in shared memory
@@ -43,7 +48,7 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
                                                 int64_t r1, const int32_t* __restrict__ rdeg,
                                                 const int64_t* __restrict__ skbase, int lk,
                                                 uint32_t* __restrict__ sk) {
-  __shared__ uint32_t sm[NT / 32][WMAX];
+  __shared__ uint32_t sm[NT / 32][2 * WMAX];
   const int lane = threadIdx.x & 31;
   uint32_t* s = sm[threadIdx.x >> 5];
   const int64_t nw = ((int64_t)gridDim.x * NT) >> 5;
@@ -59,7 +64,7 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
       const int64_t o = off[v], d = off[v + 1] - o;
       const int64_t W = sk_words(d, lk);
       const uint32_t mask = (uint32_t)(W * 32 - 1);
-      uint32_t* t = s + hf * (WMAX / 2);
+      uint32_t* t = s + hf * WMAX;
       for (int64_t j = hl; j < W; j += 16) t[j] = 0u;
       __syncwarp();
       for (int64_t i = hl; i < d; i += 16) {
@@ -67,8 +72,9 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
         atomicOr(&t[h >> 5], 1u << (h & 31));
       }
       __syncwarp();
-      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
-      for (int64_t j = hl; j < W; j += 16) out[j] = t[j];
+      sk_fold_levels(t, W, hl, 16);
+      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
+      for (int64_t j = hl; j < 2 * W - 4; j += 16) out[j] = t[j];
       __syncwarp();
       continue;
     }
@@ -83,8 +89,9 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
         atomicOr(&s[h >> 5], 1u << (h & 31));
       }
       __syncwarp();
-      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
-      for (int64_t j = lane; j < W; j += 32) out[j] = s[j];
+      sk_fold_levels(s, W, lane, 32);
+      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
+      for (int64_t j = lane; j < 2 * W - 4; j += 32) out[j] = s[j];
       __syncwarp();
     }
   }
@@ -96,12 +103,12 @@ __global__ void __launch_bounds__(512) k_sk_cta(const int64_t* __restrict__ off,
                                                 int64_t r1, const int32_t* __restrict__ rdeg,
                                                 const int64_t* __restrict__ skbase, int lk,
                                                 uint32_t* __restrict__ sk, int64_t smem_words) {
-  extern __shared__ uint32_t s[];
+  extern __shared__ uint32_t s[];  // [2 * smem_words]
   for (int64_t v = r0 + blockIdx.x; v < r1; v += gridDim.x) {
     const int64_t o = off[v], d = off[v + 1] - o;
     const int64_t W = sk_words(d, lk);
     const uint32_t mask = (uint32_t)(W * 32 - 1);
-    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * W;
+    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
     const bool in_smem = W <= smem_words;
     uint32_t* t = in_smem ? s : out;
     for (int64_t j = threadIdx.x; j < W; j += blockDim.x) t[j] = 0u;
@@ -111,8 +118,17 @@ __global__ void __launch_bounds__(512) k_sk_cta(const int64_t* __restrict__ off,
       atomicOr(&t[h >> 5], 1u << (h & 31));
     }
     __syncthreads();
-    if (in_smem)
-      for (int64_t j = threadIdx.x; j < W; j += blockDim.x) out[j] = s[j];
+    if (in_smem) {
+      sk_fold_levels(s, W, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+      for (int64_t j = threadIdx.x; j < 2 * W - 4; j += blockDim.x) out[j] = s[j];
+    } else {  // level 0 was built with global atomics (at L2): fold through L2
+      for (int64_t lo = 0, w = W; w > 4; lo += w, w >>= 1) {
+        const int64_t h = w >> 1;
+        for (int64_t i = threadIdx.x; i < h; i += blockDim.x)
+          out[lo + w + i] = __ldcg(out + lo + i) | __ldcg(out + lo + h + i);
+        __syncthreads();
+      }
+    }
     __syncthreads();
   }
 }
@@ -123,6 +139,7 @@ __global__ void k_sk_bytes(const int64_t* __restrict__ off, int64_t n, int64_t r
                            const int64_t* __restrict__ skbase, int64_t dmax,
                            unsigned long long* __restrict__ ctr) {
   const int64_t arcs = off[n] - off[r0];
+  // skbase[dmax + 1] counts the 2w-word slots; the levels fill 2w - 4 of each
   atomicAdd(&ctr[CTR_B_PREP], (unsigned long long)(4 * arcs + 4 * skbase[dmax + 1] + 16 * (n - r0)));
 }
 
@@ -186,20 +203,20 @@ int build_sketch(gs_engine* e, int lk, int64_t dmin) {
     e->launches++;
   }
   if (r2 > r1) {
-    const int64_t smem_words = 2048;  // 8 KB: many CTAs per SM
+    const int64_t smem_words = 2048;  // 16 KB with the levels: many CTAs per SM
     const int64_t grid = std::min<int64_t>(r2 - r1, (int64_t)e->sms * 8);
-    k_sk_cta<<<(unsigned)grid, 256, smem_words * 4, st>>>(g.off, g.adj, r1, r2, s.rdeg, g.skbase,
+    k_sk_cta<<<(unsigned)grid, 256, smem_words * 8, st>>>(g.off, g.adj, r1, r2, s.rdeg, g.skbase,
                                                           lk, g.sk, smem_words);
     e->launches++;
   }
   if (n > r2) {
     const int64_t smem_words =
-        std::min<int64_t>(32768, sk_words(g.dmax, lk));  // <= 128 KB, global atomics beyond
+        std::min<int64_t>(16384, sk_words(g.dmax, lk));  // <= 128 KB with the levels
     auto kern = k_sk_cta;
     GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(smem_words * 4)));
+                                 (int)(smem_words * 8)));
     const int64_t grid = std::min<int64_t>(n - r2, (int64_t)e->sms * 2);
-    kern<<<(unsigned)grid, 512, smem_words * 4, st>>>(g.off, g.adj, r2, n, s.rdeg, g.skbase, lk,
+    kern<<<(unsigned)grid, 512, smem_words * 8, st>>>(g.off, g.adj, r2, n, s.rdeg, g.skbase, lk,
                                                       g.sk, smem_words);
     e->launches++;
   }

@@ -29,11 +29,12 @@ PREP = ("k_thresholds", "k_degree_tables", "k_hubsplit", "k_sk_sizes", "k_sk_war
 
 
 def kernel_class(name: str):
-    if "k_sim_hash<1024, true>" in name:
+    # ncu prints template flags as 0 / 1
+    if "k_sim_hash<1024, 1>" in name or "k_sim_hash<1024, true>" in name:
         return 1
-    if "k_sim_hash<1024, false>" in name:
+    if "k_sim_hash<1024, 0>" in name or "k_sim_hash<1024, false>" in name:
         return 2
-    if "k_sim_hash<512, false>" in name:
+    if "k_sim_hash<512, 0>" in name or "k_sim_hash<512, false>" in name:
         return 3
     if "k_sim_warp" in name:
         return 4
