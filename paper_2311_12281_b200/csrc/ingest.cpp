@@ -15,6 +15,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <new>
 #include <thread>
 #include <vector>
 
@@ -84,9 +85,8 @@ void parse_chunk(Chunk& c) {
 
 }  // namespace
 
-extern "C" int gs_parse_edge_text(const char* buf, int64_t len, int threads, uint32_t* u_out,
-                                  uint32_t* v_out, int64_t cap, int64_t* count,
-                                  int64_t* err_line) {
+static int parse_edge_text(const char* buf, int64_t len, int threads, uint32_t* u_out,
+                           uint32_t* v_out, int64_t cap, int64_t* count, int64_t* err_line) {
   *count = 0;
   *err_line = -1;
   if (len <= 0) return GS_OK;
@@ -183,9 +183,9 @@ inline char letter(uint8_t r) {
 
 }  // namespace
 
-extern "C" int gs_format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
-                                const uint32_t* orig, int threads, char* out, int64_t cap,
-                                int64_t* len) {
+static int format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
+                         const uint32_t* orig, int threads, char* out, int64_t cap,
+                         int64_t* len) {
   *len = 0;
   if (n <= 0) return GS_OK;
   if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
@@ -253,5 +253,30 @@ void gs_parallel_copy(void* dst, const void* src, size_t bytes) {
     const int t = omp_get_thread_num();
     const size_t lo = bytes * t / nt, hi = bytes * (t + 1) / nt;
     memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  }
+}
+
+// C-ABI: no C++ exception (thread creation, vector growth) crosses the boundary.
+extern "C" int gs_parse_edge_text(const char* buf, int64_t len, int threads, uint32_t* u_out,
+                                  uint32_t* v_out, int64_t cap, int64_t* count,
+                                  int64_t* err_line) {
+  try {
+    return parse_edge_text(buf, len, threads, u_out, v_out, cap, count, err_line);
+  } catch (const std::bad_alloc&) {
+    return GS_ENOMEM;
+  } catch (...) {
+    return GS_EINTERNAL;
+  }
+}
+
+extern "C" int gs_format_result(int64_t n, const uint8_t* role, const int32_t* cluster,
+                                const uint32_t* orig, int threads, char* out, int64_t cap,
+                                int64_t* len) {
+  try {
+    return format_result(n, role, cluster, orig, threads, out, cap, len);
+  } catch (const std::bad_alloc&) {
+    return GS_ENOMEM;
+  } catch (...) {
+    return GS_EINTERNAL;
   }
 }

@@ -60,8 +60,8 @@ def parse_edge_list(source: Union[bytes, str, BinaryIO]) -> EdgeList:
     duplicates merged, sparse ids remapped order-preservingly.
 
     Native ingest: libgscan's multi-threaded parser (gs_parse_edge_text) reads
-    the text, the device remaps and deduplicates (gs_normalize_sparse; host
-    numpy when no CUDA device is visible).  Input outside the parser's ASCII
+    the text, the device remaps and deduplicates (gs_normalize_sparse; no
+    host path).  Input outside the parser's ASCII
     grammar -- malformed lines included -- goes through the reference-exact
     Python parser below, so errors (ParseError with the line number) and
     exotic-but-valid inputs behave exactly as in the reference."""
@@ -90,30 +90,27 @@ def _parse_native(data: bytes):
 
 
 def _normalize(u: np.ndarray, v: np.ndarray) -> EdgeList:
+    """Remap sparse ids order-preservingly, drop self-loops, merge duplicates
+    (graph.py:98-118) on the device (gs_normalize_sparse).  There is no host
+    path: without a CUDA device this raises."""
+    u = np.ascontiguousarray(u, dtype=np.uint32)
+    v = np.ascontiguousarray(v, dtype=np.uint32)
     count = int(len(u))
+    if count == 0:
+        return EdgeList(n_hint=0, edges=np.empty((0, 2), dtype=np.int32),
+                        orig_ids=np.empty(0, dtype=np.uint32))
     lib = _lib.load()
-    if count and lib.gs_device_count() > 0:
-        ids = np.empty(2 * count, dtype=np.uint32)
-        edges = np.empty((count, 2), dtype=np.int32)
-        n = ctypes.c_int64(0)
-        m = ctypes.c_int64(0)
-        _lib.check(lib.gs_normalize_sparse(count, u.ctypes.data, v.ctypes.data, ids.ctypes.data,
-                                           ctypes.byref(n), edges.ctypes.data, ctypes.byref(m)))
-        return EdgeList(n_hint=n.value, edges=edges[: m.value].copy(),
-                        orig_ids=ids[: n.value].copy())
-    return _normalize_host(u.astype(np.int64), v.astype(np.int64))
-
-
-def _normalize_host(u: np.ndarray, v: np.ndarray) -> EdgeList:
-    ids = np.unique(np.concatenate([u, v]))
-    du = np.searchsorted(ids, u)
-    dv = np.searchsorted(ids, v)
-    keep = du != dv
-    lo = np.minimum(du, dv)[keep]
-    hi = np.maximum(du, dv)[keep]
-    key = np.unique(lo * (len(ids) + 1) + hi)
-    edges = np.stack([key // (len(ids) + 1), key % (len(ids) + 1)], axis=1).astype(np.int32)
-    return EdgeList(n_hint=len(ids), edges=edges, orig_ids=ids.astype(np.uint32))
+    if lib.gs_device_count() <= 0:
+        raise RuntimeError("parse_edge_list: normalising the edge list needs a CUDA device "
+                           "(libgscan has no CPU path)")
+    ids = np.empty(2 * count, dtype=np.uint32)
+    edges = np.empty((count, 2), dtype=np.int32)
+    n = ctypes.c_int64(0)
+    m = ctypes.c_int64(0)
+    _lib.check(lib.gs_normalize_sparse(count, u.ctypes.data, v.ctypes.data, ids.ctypes.data,
+                                       ctypes.byref(n), edges.ctypes.data, ctypes.byref(m)))
+    return EdgeList(n_hint=n.value, edges=edges[: m.value].copy(),
+                    orig_ids=ids[: n.value].copy())
 
 
 def _parse_exact(data: bytes) -> EdgeList:
@@ -142,7 +139,7 @@ def _parse_exact(data: bytes) -> EdgeList:
             raise ParseError(f"vertex id exceeds 4-byte unsigned range in {line!r}", lineno)
         us.append(u)
         vs.append(v)
-    return _normalize_host(np.asarray(us, dtype=np.int64), np.asarray(vs, dtype=np.int64))
+    return _normalize(np.asarray(us, dtype=np.uint32), np.asarray(vs, dtype=np.uint32))
 
 
 @dataclass

@@ -74,6 +74,32 @@ def make_graph(n, edges):
                  edge_ids=c.edge_ids, edge_list=c.edge_list, orig_ids=c.orig_ids)
 
 
+def normalise_on_host(u, v):
+    """graph.py:98-118's normalisation (sorted unique ids, self-loops dropped,
+    duplicates merged) in numpy -- the CPU tier's checker for the parser, in
+    place of the device normaliser the product calls (gs_normalize_sparse)."""
+    from paper_2311_12281_b200.graph import EdgeList
+
+    u = np.asarray(u, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    ids = np.unique(np.concatenate([u, v]))
+    du, dv = np.searchsorted(ids, u), np.searchsorted(ids, v)
+    keep = du != dv
+    lo, hi = np.minimum(du, dv)[keep], np.maximum(du, dv)[keep]
+    key = np.unique(lo * (len(ids) + 1) + hi)
+    edges = np.stack([key // (len(ids) + 1), key % (len(ids) + 1)], axis=1).astype(np.int32)
+    return EdgeList(n_hint=len(ids), edges=edges, orig_ids=ids.astype(np.uint32))
+
+
+@pytest.fixture
+def host_normaliser(monkeypatch):
+    """CPU tier: parse_edge_list's normalisation step served by the numpy
+    checker above (the product raises without a device)."""
+    import paper_2311_12281_b200.graph as graph
+
+    monkeypatch.setattr(graph, "_normalize", normalise_on_host)
+
+
 def cuda_ok() -> bool:
     try:
         import torch

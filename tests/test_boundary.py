@@ -143,7 +143,7 @@ def test_empty_graph_needs_no_device():
     assert result.n == 0 and result.to_text() == "" and stats.sim_evals == 0
 
 
-def test_parse_edge_list_rules():
+def test_parse_edge_list_rules(host_normaliser):
     from paper_2311_12281_b200 import ParseError, parse_edge_list
 
     el = parse_edge_list("# header\n\n0\t1\n  2 3\n\n  # c\n")

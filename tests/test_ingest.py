@@ -2,8 +2,8 @@
 libgscan parser, and the GSCG binary cache (graph.py:279-359), against golden
 outputs of the Python reference (tests/golden/make_parse_golden.py).
 
-CPU tier: the native parser + host normalisation; `-m gpu`: the same inputs
-through the device normaliser (gs_normalize_sparse)."""
+CPU tier: the native parser, normalised by the test's numpy checker; `-m gpu`:
+the same inputs through the product's device normaliser (gs_normalize_sparse)."""
 
 import base64
 import json
@@ -38,7 +38,7 @@ def _check_all():
         assert np.asarray(el.orig_ids).tolist() == exp["orig_ids"]
 
 
-def test_parse_matches_reference_cpu():
+def test_parse_matches_reference_cpu(host_normaliser):
     _check_all()
 
 
@@ -59,7 +59,7 @@ def test_native_parser_grammar():
     assert err.value == 3
 
 
-def test_parse_large_multichunk_matches_exact():
+def test_parse_large_multichunk_matches_exact(host_normaliser):
     rng = np.random.default_rng(5)
     ids = rng.integers(0, 2**32, 5000, dtype=np.uint64)
     u = ids[rng.integers(0, 5000, 300_000)]
@@ -71,6 +71,17 @@ def test_parse_large_multichunk_matches_exact():
     assert a.n_hint == b.n_hint
     np.testing.assert_array_equal(np.asarray(a.edges), np.asarray(b.edges))
     np.testing.assert_array_equal(np.asarray(a.orig_ids), np.asarray(b.orig_ids))
+
+
+def test_normaliser_has_no_host_path(monkeypatch):
+    """Without a device the product's normalisation raises (no CPU fallback)."""
+    lib = _lib.load()
+    if lib.gs_device_count() > 0:
+        pytest.skip("a CUDA device is visible")
+    with pytest.raises(RuntimeError, match="needs a CUDA device"):
+        gs.parse_edge_list("0 1\n1 2\n")
+    with pytest.raises(gs.ParseError):  # parse errors still come first
+        gs.parse_edge_list("0 1\nx\n")
 
 
 def test_gscg_cache_byte_compatible(tmp_path):
