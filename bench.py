@@ -433,7 +433,8 @@ def run_ours(args):
     for _ in range(args.warmup):
         step_device()
     sim_ms, ident_ms, launches, phase = [], [], 0, {}
-    cls_ms = [[] for _ in range(6)]
+    NK = len(_lib.KERNEL_CLASSES)
+    cls_ms = [[] for _ in range(NK)]
     barrier()
     with ClockSampler(local) as clk:
         e0 = torch.cuda.Event(enable_timing=True)
@@ -442,7 +443,7 @@ def run_ours(args):
         for _ in range(args.steps):
             step_device()
             ident_ms.append(st.phase_ms[_lib.GS_PH_IDENTIFY])
-            for c in range(6):
+            for c in range(NK):
                 cls_ms[c].append(st.phase_ms[_lib.GS_PH_K_PREP + c])
             launches += int(st.kernel_launches)
         e1.record(stream)
@@ -458,13 +459,13 @@ def run_ours(args):
     peak, peak_src = peaks()
     t_sim = statistics.median(ident_ms) / 1000.0
     kernels = []
-    for c in range(6):
+    for c in range(NK):
         t = statistics.median(cls_ms[c]) / 1000.0
         b = int(st.kernel_bytes[c])
         kernels.append({"kernel": _lib.KERNEL_CLASSES[c], "ms": round(t * 1000, 3), "bytes": b,
                         "achieved_gbs": b / t / 1e9 if t > 0 else None,
                         "frac": b / t / 1e9 / peak if t > 0 else None})
-    dom = max(range(6), key=lambda c: kernels[c]["ms"])
+    dom = max(range(NK), key=lambda c: kernels[c]["ms"])
     pass_bytes = sum(k["bytes"] for k in kernels)
     traffic, traffic_note = None, "no ncu record for these sources (tools/ncu_traffic.py)"
     tf = os.path.join(ROOT, "profiles", "sim_traffic.json")
@@ -481,7 +482,7 @@ def run_ours(args):
             traffic = tk.get("dram_bytes") if tk else None
             traffic_note = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of the {dom}-th "
                             f"class's launches, {td.get('when')}, sources {td.get('source_hash')}")
-            for c in range(6):
+            for c in range(NK):
                 tc = td.get("classes", {}).get(str(c))
                 if tc:
                     kernels[c]["dram_bytes_ncu"] = tc.get("dram_bytes")

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define GS_ABI_VERSION 2
+#define GS_ABI_VERSION 3
 
 #define GS_OK 0
 #define GS_EINVAL 1
@@ -85,6 +85,7 @@ enum {
   GS_PH_K_MEDIUM = 12, /* k_sim_hash<512>             (512 <= deg b < 4096) */
   GS_PH_K_SMALL = 13,  /* k_sim_warp                  (64 <= deg b < 512) */
   GS_PH_K_TINY = 14,   /* k_sim_tiny                  (deg b < 64) */
+  GS_PH_K_SKETCH = 15, /* k_sk_filter: sketch bound, thread per surviving edge (deg b >= 64) */
   GS_PH_COUNT = 16
 };
 
@@ -105,11 +106,11 @@ typedef struct gs_stats {
   int64_t sim_decided_by_sketch;  /* decided dissimilar by the sketch bound (no scan) */
   double phase_ms[GS_PH_COUNT];
   /* (ABI 2) algorithmic bytes of the identify pass per kernel class, in the
-   * order of GS_PH_K_PREP .. GS_PH_K_TINY: every global element of graph,
+   * order of GS_PH_K_PREP .. GS_PH_K_SKETCH (ABI 3: + the sketch filter): every global element of graph,
    * sketch and state data the kernels read or write, at its size (early
    * exits counted where they stop; scratch tables excluded).  Divided by the
    * class's phase_ms this is the roofline's achieved bandwidth. */
-  int64_t kernel_bytes[6];
+  int64_t kernel_bytes[7];
   int64_t wsim_bytes;    /* SURVEY 8(d) W_sim: 4 min(d) per edge left by the O(1)
                           * bounds + 4 d_b per staged b (the accounting of
                           * round 1, reported for comparison only) */

@@ -26,15 +26,17 @@ GS_EPARSE = 6
 GS_PH_H2D, GS_PH_BUILD, GS_PH_IDENTIFY, GS_PH_CLEANUP = 0, 1, 2, 3
 GS_PH_CLUSTER, GS_PH_CLASSIFY, GS_PH_D2H, GS_PH_TOTAL = 4, 5, 6, 7
 GS_PH_SIM_KERNELS = 8
-ABI_VERSION = 2  # GS_ABI_VERSION of include/gscan.h
+ABI_VERSION = 3  # GS_ABI_VERSION of include/gscan.h
 # identify pass by kernel class (gs_stats.phase_ms / kernel_bytes order)
-GS_PH_K_PREP, GS_PH_K_HUGE, GS_PH_K_LARGE, GS_PH_K_MEDIUM, GS_PH_K_SMALL, GS_PH_K_TINY = range(9, 15)
+(GS_PH_K_PREP, GS_PH_K_HUGE, GS_PH_K_LARGE, GS_PH_K_MEDIUM, GS_PH_K_SMALL, GS_PH_K_TINY,
+ GS_PH_K_SKETCH) = range(9, 16)
 KERNEL_CLASSES = ("prep: thresholds + degree tables + hub split + sketch build + Lemma-1 pre-pass",
                   "k_sim_hash<1024,L2 table> (deg b >= 28672)",
                   "k_sim_hash<1024> (4096 <= deg b < 28672)",
                   "k_sim_hash<512> (512 <= deg b < 4096)",
                   "k_sim_warp (64 <= deg b < 512)",
-                  "k_sim_tiny (deg b < 64)")
+                  "k_sim_tiny (deg b < 64)",
+                  "k_sk_filter (sketch bound, thread per surviving edge, deg b >= 64)")
 GS_PH_COUNT = 16
 
 
@@ -68,7 +70,7 @@ class GsStats(ctypes.Structure):
         ("peak_device_bytes", ctypes.c_int64),
         ("sim_decided_by_sketch", ctypes.c_int64),
         ("phase_ms", ctypes.c_double * GS_PH_COUNT),
-        ("kernel_bytes", ctypes.c_int64 * 6),
+        ("kernel_bytes", ctypes.c_int64 * 7),
         ("wsim_bytes", ctypes.c_int64),
         ("pcie_bytes", ctypes.c_int64),
     ]

@@ -141,8 +141,11 @@ void gs_engine::kev_mark(int i) {
 }
 
 void gs_engine::kev_class_ms(double* out) {
+  // class c runs between events from[c] and to[c] (the sketch filter first)
+  static const int from[kKernelClasses] = {0, 3, 4, 5, 6, 7, 2};
+  static const int to[kKernelClasses] = {1, 4, 5, 6, 7, 8, 3};
   for (int c = 0; c < kKernelClasses; ++c) {
-    const int a = c == 0 ? 0 : c + 1, b = c == 0 ? 1 : c + 2;
+    const int a = from[c], b = to[c];
     float t = 0;
     if (g.m > 0 && kev[a] && kev[b] && cudaEventSynchronize(kev[b]) == cudaSuccess &&
         cudaEventElapsedTime(&t, kev[a], kev[b]) != cudaSuccess) {

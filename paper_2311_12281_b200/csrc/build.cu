@@ -1077,9 +1077,74 @@ __device__ __forceinline__ void segmented_runs(uint32_t runs, int lane, int64_t 
   }
 }
 
+// Warp-wide bitonic sort of 32 K keys held K per lane, "blocked" (lane l holds
+// positions lK .. lK + K - 1), ascending.  Partner distances j < K are register
+// compare-swaps, j >= K shuffles; the direction bit (i & k) is a compile-time
+// constant for k < K and a function of the lane alone for k >= K.  (The
+// shared-memory network it replaces issued ~2x the instructions: two loads,
+// two stores and the index arithmetic per compare, plus a __syncwarp per stage.)
+template <int K>
+__device__ __forceinline__ void warp_bitonic_sort(int32_t (&x)[K], int lane) {
+  constexpr int P = 32 * K;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < K) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool up = k < K ? (r & k) == 0 : (lane & (k / K)) == 0;
+            const int32_t lo = min(x[r], x[p]), hi = max(x[r], x[p]);
+            x[r] = up ? lo : hi;
+            x[p] = up ? hi : lo;
+          }
+        }
+      } else {
+        const int lj = j / K;
+        const bool keep_lo = ((lane & lj) == 0) == ((lane & (k / K)) == 0);
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int32_t y = __shfl_xor_sync(0xffffffffu, x[r], lj);
+          x[r] = keep_lo ? min(x[r], y) : max(x[r], y);
+        }
+      }
+    }
+  }
+}
+
+// one caller run of d in (32 (K / 2), 32 K] neighbours: coalesced gather into
+// registers (any order: the network sorts it), warp sort, then a padded
+// shared-memory transpose (lane stride K + 1: no bank conflicts) so the
+// rank-space run is written coalesced
+template <int K>
+__device__ __forceinline__ void fused_run_regs(const int32_t* __restrict__ adj,
+                                               const int32_t* __restrict__ rank, int64_t ou,
+                                               int d, int64_t n, int64_t u, int32_t* o,
+                                               int32_t* sbuf, int lane, bool& b3, bool& b4,
+                                               bool& b5) {
+  int32_t x[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = lane + 32 * r;
+    x[r] = i < d ? rank[fused_check(adj, ou + i, ou, n, u, b3, b4)] : kPad;
+  }
+  warp_bitonic_sort<K>(x, lane);
+#pragma unroll
+  for (int r = 0; r < K; ++r) sbuf[lane * (K + 1) + r] = x[r];
+  __syncwarp();
+  for (int i = lane; i < d; i += 32) {
+    const int32_t v = sbuf[(i / K) * (K + 1) + i % K];
+    o[i] = v;
+    if (i + 1 < d) b5 |= sbuf[((i + 1) / K) * (K + 1) + (i + 1) % K] == v;
+  }
+  __syncwarp();
+}
+
 // warp per caller vertex with d <= 32 (lane i holds element i): register
-// bitonic network; d in (32, 511]: warp per vertex, bitonic in a 2 KB
-// shared-memory slice.  Longer runs are skipped (CTA kernels below).
+// bitonic network; d in (32, 511]: warp per vertex, K = 2..16 keys per lane
+// (warp_bitonic_sort).  Longer runs are skipped (CTA kernels below).
 __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ off, int64_t n,
                                                     const int32_t* __restrict__ adj,
                                                     const int32_t* __restrict__ rank,
@@ -1087,7 +1152,7 @@ __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ 
                                                     int32_t* __restrict__ out,
                                                     int* __restrict__ bad, int64_t row_lo,
                                                     int64_t row_hi) {
-  constexpr int CAP = 512;
+  constexpr int CAP = 32 * 17;  // the K = 16 transpose
   __shared__ int32_t buf[8 * CAP];
   const int lane = threadIdx.x & 31;
   int32_t* sbuf = buf + (threadIdx.x >> 5) * CAP;
@@ -1138,18 +1203,14 @@ __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ 
         o[lane] = x;
         b5 |= lane + 1 < d && nx == x;
       }
+    } else if (d <= 64) {
+      fused_run_regs<2>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
+    } else if (d <= 128) {
+      fused_run_regs<4>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
+    } else if (d <= 256) {
+      fused_run_regs<8>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
     } else {
-      int P = 64;
-      while (P < d) P <<= 1;
-      for (int i = lane; i < P; i += 32)
-        sbuf[i] = i < d ? rank[fused_check(adj, ou + i, ou, n, u, b3, b4)] : kPad;
-      __syncwarp();
-      bitonic_smem<false>(sbuf, P, lane, 32);
-      for (int i = lane; i < d; i += 32) {
-        o[i] = sbuf[i];
-        b5 |= i + 1 < d && sbuf[i + 1] == sbuf[i];
-      }
-      __syncwarp();
+      fused_run_regs<16>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
     }
     }
   }

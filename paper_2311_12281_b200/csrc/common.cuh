@@ -31,7 +31,9 @@ std::string cuda_msg(cudaError_t e, const char* what, const char* file, int line
 
 // ---------------------------------------------------------------------------
 // per-edge similarity status (scan.py:38-40) and role codes (scan.py:43-52)
-enum : uint8_t { SIM_UNKNOWN = 0, SIM_SIMILAR = 1, SIM_DISSIMILAR = 2 };
+// SIM_PENDING: identify stage 1 could not decide the edge; stage 2 decides it
+// (or resets it to SIM_UNKNOWN when pruning skips it), so it never outlives identify
+enum : uint8_t { SIM_UNKNOWN = 0, SIM_SIMILAR = 1, SIM_DISSIMILAR = 2, SIM_PENDING = 3 };
 enum : uint8_t {
   ROLE_UNKNOWN = 0,
   ROLE_CORE = 1,

@@ -105,12 +105,13 @@ enum Ctr {
   CTR_B_MED,    // k_sim_hash<512, false>
   CTR_B_SMALL,  // k_sim_warp
   CTR_B_TINY,   // k_sim_tiny
+  CTR_B_SKETCH, // k_sk_filter (identify stage 1: the sketch bound, thread per surviving edge)
   CTR_B_OTHER,  // the same kernels in the cleanup / union / attach passes
   CTR_WSIM,     // SURVEY 8(d) W_sim terms counted on the device (4 min(d) per intersected edge)
   CTR_PCIE,     // out of core: bytes read zero-copy from mapped host memory
   CTR_COUNT
 };
-static constexpr int kKernelClasses = 6;  // CTR_B_PREP .. CTR_B_TINY
+static constexpr int kKernelClasses = 7;  // CTR_B_PREP .. CTR_B_SKETCH
 
 enum SimMode : int {
   MODE_IDENTIFY = 0,  // identifyCore (Alg. 2): skip if both roles decided
@@ -147,6 +148,11 @@ struct SimParams {
   int sk_thread;        // thread-per-survivor sketch pass before the warp scans
   int32_t sk_tmax;      //   for rows of at most this many words (longer: per warp)
   int bslot;            // counter slot of this launch's algorithmic bytes (CTR_B_*)
+  // identify stage 2: the sketch filter (k_sk_filter) ran first; only edges
+  // it marked SIM_PENDING are scanned, b's with p1_pend[b - p1_lo] == 0 skipped
+  const int32_t* p1_pend = nullptr;
+  const int32_t* p1_j0 = nullptr;  // survivor start of b's owned prefix
+  int64_t p1_lo = 0;
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;
@@ -189,10 +195,10 @@ struct gs_engine {
   unsigned long long* h_ctr = nullptr;
   std::vector<cudaEvent_t> ev;
   // identify-pass kernel-class timing: kev[0] / kev[1] around the preparation,
-  // kev[2] at the start of the sweep, kev[2 + c] after class c (huge, large,
-  // medium, small, tiny); recorded when kev_on, read into
+  // kev[2] at the start of the sweep, kev[3] after the sketch filter, kev[3 + c]
+  // after class c (huge, large, medium, small, tiny); recorded when kev_on, read into
   // gs_stats.phase_ms[GS_PH_K_PREP ..] (kev_class_ms)
-  cudaEvent_t kev[gs::kKernelClasses + 2] = {};
+  cudaEvent_t kev[gs::kKernelClasses + 2] = {};  // see kev_class_ms
   bool kev_on = false;
   void kev_mark(int i);
   void kev_class_ms(double* out);  // [kKernelClasses], synchronises the events

@@ -19,6 +19,8 @@
 
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "simcore.cuh"
 
 namespace gs {
@@ -400,12 +402,13 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   C.stash = s_stash;
   for (uint32_t i = tid; i < ((bm_words + 4 + 3) & ~3u); i += NT) bm[i] = 0u;
 
+  const bool p1 = P.p1_pend != nullptr;  // identify stage 2: SIM_PENDING edges only
   for (;;) {
     if (tid == 0) s_item = atomicAdd(&P.wq[qi], 1);
     __syncthreads();
     const int64_t b = shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
-    if (P.mode >= MODE_UNION && !b_needed(P, b)) {
+    if ((P.mode >= MODE_UNION && !b_needed(P, b)) || (p1 && P.p1_pend[b - P.p1_lo] == 0)) {
       __syncthreads();  // s_item read by all before the next claim
       continue;
     }
@@ -415,23 +418,28 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
     bool built = false, sk_staged = false, wsim_b = false;
-    unsigned long long sb = kBytesB;
-    const int64_t j0 = survivor_start_cta<NT>(P, nb, nlow, th, P.dmax, sb);
+    unsigned long long sb = kBytesB + (p1 ? 8 : 0);
+    const int64_t j0 = p1 ? P.p1_j0[b - P.p1_lo] : survivor_start_cta<NT>(P, nb, nlow, th, P.dmax, sb);
     if (tid == 0) ctr_add(lc, LC_BYTES, sb);
     for (int64_t base = j0; base < nlow; base += chunk) {
       if (tid == 0) { s_nsurv = 0; s_next = 0; s_bsim = 0; s_bdis = 0; }
       __syncthreads();
       const int64_t lim = base + chunk < nlow ? base + chunk : nlow;
-      if (tid == 0) ctr_add(lc, LC_BYTES, (unsigned long long)(lim - base) * kBytesCand);
+      if (tid == 0) ctr_add(lc, LC_BYTES, (unsigned long long)(lim - base) * (p1 ? 1u : kBytesCand));
       // filter + O(1) bounds, one candidate a per thread
       for (int64_t j = base + tid; j < lim; j += NT) {
         const int64_t e = e0 + j;
+        if (p1 && P.sim[e] != SIM_PENDING) continue;  // decided (or skipped) by stage 1
         const int32_t a = nb[j];
         const int64_t oa = P.off[a];
         const int64_t da = P.off[a + 1] - oa;
+        if (p1) ctr_add(lc, LC_BYTES, kBytesCand);
         const bool bdec = da + 1 < xmin || da <= simmax;
         if (bdec && P.mode <= MODE_CLEANUP) continue;  // folded in by the pre-pass
-        if (!edge_needed(P, e, a, (int32_t)b)) continue;
+        if (!edge_needed(P, e, a, (int32_t)b)) {
+          if (p1) P.sim[e] = SIM_UNKNOWN;  // pruned since stage 1: undecided, as in Alg. 2
+          continue;
+        }
         if (da + 1 < xmin) {  // only union / attach get here (identify: pre-pass)
           record_edge(P, e, a, (int32_t)b, false, false, lc, false);
         } else if (da <= simmax) {
@@ -450,9 +458,9 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
         if (tid == 0 && !wsim_b) ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)db);  // once
         wsim_b = true;
         int ns_scan = ns;
-        const bool tpass = P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
+        const bool tpass = !p1 && P.sk_thread && P.sk != nullptr && db >= P.sk_dmin &&
                            2 * sk_words(db, P.sk_lk) <= skw;
-        if (!sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
+        if (!p1 && !sk_staged && P.sk != nullptr && db >= P.sk_dmin &&
             2 * sk_words(db, P.sk_lk) <= skw) {  // b's sketch and its folds, once per b
           const int64_t wb = sk_words(db, P.sk_lk);
           // the levels are precomputed (sketch.cu): one coalesced copy, one barrier
@@ -555,7 +563,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           bool skd = false;
           unsigned long long skbytes = 0;
           // long rows are left to the warp (thread-pass imbalance)
-          if ((!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
+          if (!p1 && (!tpass || sk_words(ad.y, P.sk_lk) > P.sk_tmax) && sk_try(P, ad.y, db, jc.y)) {
             const int64_t wa = sk_words(ad.y, P.sk_lk);
             skbytes = 4ull * (unsigned long long)(lev ? wa : 2 * wa);
             const uint32_t* A = sk_row(P, ad.x, ad.y, wa);
@@ -571,12 +579,18 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
             ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
             ctr_add(lc, skd ? LC_SKETCH : LC_INTERS, 1);
             ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)scanned + kBytesRec + skbytes);
-            record_edge(P, e0 + jc.x, ad.x, (int32_t)b, res, false, lc);
+            surv_jc[s].y = res ? 1 : 0;  // recorded below, all survivors at once
             atomicAdd(res ? &s_bsim : &s_bdis, 1u);
           }
           s = s2;
           first = first2;
         }
+        // record the chunk's decisions thread-per-edge: the bound atomics of
+        // a (a returned value each) are all in flight together instead of one
+        // per survivor on the deciding warp's critical path
+        __syncthreads();
+        for (int i = tid; i < ns_scan; i += NT)
+          record_edge(P, e0 + surv_jc[i].x, surv_ad[i].x, (int32_t)b, surv_jc[i].y != 0, false, lc);
       }
       __syncthreads();
       if (tid == 0 && (s_bsim | s_bdis) &&
@@ -617,6 +631,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
   __shared__ unsigned long long s_ctr[LC_N];
   HotCtr lc;
   shared_ctr_init(s_ctr);
+  const bool p1 = P.p1_pend != nullptr;  // identify stage 2: SIM_PENDING edges only
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
@@ -624,6 +639,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     const int64_t b = shard_top(rlo, rhi, item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
     if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
+    if (p1 && P.p1_pend[b - P.p1_lo] == 0) continue;
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
     const int32_t* __restrict__ nb = P.adj + ob;
@@ -631,22 +647,25 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     bool built = false;
     uint32_t bsim = 0, bdis = 0;
     int64_t wb = 0;
-    unsigned long long sb = kBytesB;
-    const int64_t j0 = survivor_start_warp(P, nb, nlow, th, P.dmax, lane, sb);
+    unsigned long long sb = kBytesB + (p1 ? 8 : 0);
+    const int64_t j0 = p1 ? P.p1_j0[b - P.p1_lo] : survivor_start_warp(P, nb, nlow, th, P.dmax, lane, sb);
     if (lane == 0) ctr_add(lc, LC_BYTES, sb);
     for (int64_t base = j0; base < nlow; base += 32) {
       const int64_t j = base + lane;
       if (lane == 0)
-        ctr_add(lc, LC_BYTES, (unsigned long long)min((int64_t)32, nlow - base) * kBytesCand);
+        ctr_add(lc, LC_BYTES, (unsigned long long)min((int64_t)32, nlow - base) * (p1 ? 1u : kBytesCand));
       int st = 0;  // 0 none, 1 dissimilar by bound, 2 similar by bound, 3 survivor
       int32_t a = 0, da = 0, cmin = 0;
       int64_t oa = 0;
-      if (j < nlow) {
+      if (j < nlow && (!p1 || P.sim[e0 + j] == SIM_PENDING)) {
         a = nb[j];
         oa = P.off[a];
         da = (int32_t)(P.off[a + 1] - oa);
+        if (p1) ctr_add(lc, LC_BYTES, kBytesCand);
         const bool bdec = da + 1 < th.x || da <= th.y;
-        if (!(bdec && P.mode <= MODE_CLEANUP) && edge_needed(P, e0 + j, a, (int32_t)b)) {
+        const bool need = !(bdec && P.mode <= MODE_CLEANUP) && edge_needed(P, e0 + j, a, (int32_t)b);
+        if (p1 && !need) P.sim[e0 + j] = SIM_UNKNOWN;  // pruned since stage 1
+        if (need) {
           if (da + 1 < th.x) st = 1;
           else if (da <= th.y) st = 2;
           else {
@@ -654,7 +673,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
             cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
             ctr_add(lc, LC_WSIM, 4ull * (unsigned long long)da);  // SURVEY W_sim: 4 min(d)
             // thread-per-candidate sketch bound (S_b folded from global, L1-resident)
-            if (P.sk_thread && P.sk != nullptr && db >= P.sk_dmin && sk_try(P, da, db, cmin)) {
+            if (!p1 && P.sk_thread && P.sk != nullptr && db >= P.sk_dmin && sk_try(P, da, db, cmin)) {
               const int64_t wa = sk_words(da, P.sk_lk), wbb = sk_words(db, P.sk_lk);
               unsigned long long words = 0;
               const bool rej = sk_thread_rejects(sk_row(P, a, da, wa),
@@ -696,6 +715,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
       // survivors of this batch, software-pipelined like the CTA kernel
       int src = smask ? __ffs(smask) - 1 : 0;
       uint32_t first = kPast;
+      bool myres = false;
       if (smask) {
         const int32_t da0 = __shfl_sync(0xffffffffu, da, src);
         const int64_t oa0 = __shfl_sync(0xffffffffu, oa, src);
@@ -714,7 +734,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
         int32_t scanned = 0;
         bool skd = false;
         unsigned long long skbytes = 0;
-        if (!P.sk_thread && sk_try(P, sda, db, scm)) {
+        if (!p1 && !P.sk_thread && sk_try(P, sda, db, scm)) {
           const int64_t wa = sk_words(sda, P.sk_lk);
           skbytes = 4ull * (unsigned long long)(2 * wa);
           // S_b's level at a's resolution, from its precomputed slot
@@ -728,11 +748,14 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
           ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
           ctr_add(lc, skd ? LC_SKETCH : LC_INTERS, 1);
           ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)scanned + kBytesRec + skbytes);
-          record_edge(P, e0 + base + src, sa, (int32_t)b, res, false, lc);
         }
+        if (lane == src) myres = res;
         src = src2;
         first = first2;
       }
+      // the batch's decisions recorded by their own lanes at once (the bound
+      // atomics of the a's in flight together, off the survivor loop)
+      if (st == 3) record_edge(P, e0 + j, a, (int32_t)b, myres, false, lc);
     }
     if (lane == 0 && (bsim | bdis) && (P.mode == MODE_IDENTIFY || P.mode == MODE_CLEANUP)) {
       apply_bounds(P.bounds, P.role, b, bsim, bdis, P.mu);
@@ -740,6 +763,157 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     }
     hot_flush_warp(lc, s_ctr);
     __syncwarp();
+  }
+  hot_flush_warp(lc, s_ctr);
+  shared_ctr_flush(P, s_ctr);
+}
+
+// ---------------------------------------------------------------------------
+// Identify, stage 1 (k_sk_filter): the sketch bound for every surviving edge
+// of the classes deg b >= 64, one thread per edge, before any table of N(b) is
+// built.  The CTA-per-b kernels used to run this pass between two barriers
+// per chunk of b's survivors -- the CTA then waited for its longest row (30%
+// of the medium class's stall samples) at half occupancy.  Here warps are
+// independent: a warp takes a work item of up to kP1Chunk candidates of one b
+// (rank order, so neighbouring lanes have neighbouring degrees and rows of
+// similar length), reads S_a and S_b's level at a's resolution straight from
+// their sketch slots (b's level is shared by the warp, L1-resident), records
+// the edges it proves dissimilar and marks the rest SIM_PENDING for stage 2
+// (the class kernels, which then scan only pending edges and skip every b
+// without one).
+static constexpr int kP1Chunk = 256;  // candidates per work item
+
+// per b of [rlo, rhi): survivor start (the O(1) bounds' suffix) and work items
+__global__ void k_p1_items(SimParams P, int64_t rlo, int64_t rhi, int32_t* __restrict__ j0s,
+                           int32_t* __restrict__ nit) {
+  unsigned long long bytes = 0;
+  for (int64_t b = rlo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < rhi;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t j0 = 0, cnt = 0;
+    if (owns(b, P.shard_rank, P.shard_world)) {
+      const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
+      const int64_t nlow = P.eoff[b + 1] - P.eoff[b];
+      bytes += kBytesB + 8;
+      j0 = survivor_start(P, P.adj + ob, nlow, P.thr[db], P.dmax, bytes);
+      cnt = nlow - j0;
+    }
+    j0s[b - rlo] = (int32_t)j0;
+    nit[b - rlo] = (int32_t)((cnt + kP1Chunk - 1) / kP1Chunk);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(&P.ctr[CTR_B_SKETCH], bytes);
+}
+
+// item -> b (index from rlo); the item count lands in *total
+__global__ void k_p1_owner(int64_t nb, const int32_t* __restrict__ nit,
+                           const int32_t* __restrict__ ioff, int32_t* __restrict__ owner,
+                           int32_t* __restrict__ total) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t k = nit[i], o = ioff[i];
+    for (int32_t t = 0; t < k; ++t) owner[o + t] = (int32_t)i;
+    if (i == nb - 1) *total = o + k;
+  }
+}
+
+template <int NT, int MINB, int UNROLL>
+__global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo,
+                                                  const int32_t* __restrict__ j0s,
+                                                  const int32_t* __restrict__ ioff,
+                                                  const int32_t* __restrict__ owner,
+                                                  const int32_t* __restrict__ total,
+                                                  int32_t* __restrict__ pend) {
+  __shared__ unsigned long long s_ctr[LC_N];
+  const int lane = threadIdx.x & 31;
+  HotCtr lc;
+  shared_ctr_init(s_ctr);
+  const int32_t T = *total;
+  for (;;) {
+    int item = 0;
+    if (lane == 0) item = atomicAdd(&P.wq[5], 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= T) break;
+    const int32_t bi = owner[item];
+    const int64_t b = rlo + bi;
+    const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
+    const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
+    const int64_t jlo = (int64_t)j0s[bi] + (int64_t)(item - ioff[bi]) * kP1Chunk;
+    const int64_t jhi = min(nlow, jlo + kP1Chunk);
+    const int32_t* __restrict__ nb = P.adj + ob;
+    const bool skb = P.sk != nullptr && db >= P.sk_dmin;
+    const int64_t wb = skb ? sk_words(db, P.sk_lk) : 0;
+    const uint32_t* levb = skb ? sk_row(P, b, db, wb) : nullptr;
+    // owner, ioff, j0s, off / eoff pairs of b; b's sketch slot once per b (the
+    // warps re-read it from L1 / L2 per edge: not algorithmic traffic)
+    const bool first_item = item == ioff[bi];
+    if (lane == 0) ctr_add(lc, LC_BYTES, 44ull + (first_item && skb ? 4ull * (2 * wb - 4) : 0ull));
+    uint32_t ndis = 0, npend = 0;
+    // Software-pipelined over the item's batches of 32: batch i+1's degree and
+    // role and batch i+2's a are in flight while batch i walks its rows, and
+    // the role decision of a recorded edge (the bound atomic's returned value)
+    // is taken one batch later, so neither latency sits on the walk's path.
+    constexpr uint64_t kDis = 0ull - (1ull << 32);  // one dissimilar outcome: upper - 1
+    int32_t pa = -1;                               // deferred role decision: a, old bounds
+    uint64_t pold = 0;
+    int32_t a1 = jlo + lane < jhi ? nb[jlo + lane] : -1;
+    int32_t a2 = jlo + 32 + lane < jhi ? nb[jlo + 32 + lane] : -1;
+    int64_t o1a = 0, o1b = 0;
+    uint8_t r1 = 0;
+    if (a1 >= 0) { o1a = P.off[a1]; o1b = P.off[a1 + 1]; r1 = ld_role(P.role, a1); }
+    for (int64_t jb = jlo; jb < jhi; jb += 32) {
+      const int32_t a = a1;
+      const int64_t da = o1b - o1a;
+      const uint8_t ra = r1;
+      a1 = a2;
+      if (a1 >= 0) { o1a = P.off[a1]; o1b = P.off[a1 + 1]; r1 = ld_role(P.role, a1); }
+      a2 = jb + 64 + lane < jhi ? nb[jb + 64 + lane] : -1;
+      if (pa >= 0) {  // the previous batch's record: noncore once upper < mu
+        if ((int32_t)(uint32_t)((pold + kDis) >> 32) < P.mu) P.role[pa] = ROLE_NONCORE;
+        pa = -1;
+      }
+      const uint8_t rb = ld_role(P.role, b);
+      bool dis = false, pnd = false;
+      if (a >= 0) {
+        const int64_t e = e0 + jb + lane;
+        unsigned long long by = kBytesCand;
+        // every j >= j0 survives the O(1) bounds; identify skips an edge whose
+        // endpoints both have a role (Alg. 2 line 2)
+        if (ra == ROLE_UNKNOWN || rb == ROLE_UNKNOWN) {
+          const int32_t cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
+          if (skb && sk_try(P, da, db, cmin)) {
+            const int64_t wa = sk_words(da, P.sk_lk);
+            unsigned long long words = 0;
+            dis = sk_rejects256<UNROLL>(sk_row(P, a, da, wa), levb + 2 * (wb - wa), wa, da, cmin,
+                                        words);
+            by += 4ull * words;  // S_a's words read (b's level: per b, above)
+          }
+          if (dis) {  // record_edge(dissimilar), the role decision deferred
+            P.sim[e] = SIM_DISSIMILAR;
+            pold = atomicAdd(reinterpret_cast<unsigned long long*>(&P.bounds[a]),
+                             (unsigned long long)kDis);
+            pa = a;
+            ctr_add(lc, LC_SKETCH, 1);
+            by += kBytesRec;
+          } else {
+            P.sim[e] = SIM_PENDING;
+            pnd = true;
+            by += 1;
+          }
+        }
+        ctr_add(lc, LC_BYTES, by);
+      }
+      ndis += __popc(__ballot_sync(0xffffffffu, dis));
+      npend += __popc(__ballot_sync(0xffffffffu, pnd));
+    }
+    if (pa >= 0 && (int32_t)(uint32_t)((pold + kDis) >> 32) < P.mu) P.role[pa] = ROLE_NONCORE;
+    if (lane == 0) {
+      if (ndis) {
+        apply_bounds(P.bounds, P.role, b, 0u, ndis, P.mu);
+        ctr_add(lc, LC_BYTES, 16);
+      }
+      if (npend) atomicAdd(&pend[bi], (int32_t)npend);
+    }
   }
   hot_flush_warp(lc, s_ctr);
   shared_ctr_flush(P, s_ctr);
@@ -925,6 +1099,44 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     dcls[0] = o[1] - o[0];
     dcls[1] = o[3] - o[2];
   }
+  // identify stage 1: the sketch filter over every surviving edge of deg b >= 64
+  // (GS_P1=0: the class kernels run the sketch bound themselves, as before)
+  static const bool p1_on = !(getenv("GS_P1") && atoi(getenv("GS_P1")) == 0);
+  int32_t *p1_j0 = nullptr, *p1_nit = nullptr, *p1_ioff = nullptr, *p1_owner = nullptr,
+          *p1_pend = nullptr;
+  if (ident && p1_on && g.sk != nullptr && g.n > rc[1]) {
+    const int64_t lo = rc[1], nb = g.n - lo;
+    GS_TRY(e->alloc_n(&p1_j0, nb));
+    GS_TRY(e->alloc_n(&p1_nit, nb));
+    GS_TRY(e->alloc_n(&p1_ioff, nb + 1));  // [nb]: the item count
+    GS_TRY(e->alloc_n(&p1_pend, nb));
+    GS_TRY(e->alloc_n(&p1_owner, nb + g.m / kP1Chunk + 1));  // >= items
+    GS_CUDA(cudaMemsetAsync(p1_pend, 0, sizeof(int32_t) * (size_t)nb, e->stream));
+    P.bslot = CTR_B_SKETCH;
+    const unsigned gi = (unsigned)std::min<int64_t>(grid_for(nb, 256), (int64_t)e->sms * 16);
+    k_p1_items<<<gi, 256, 0, e->stream>>>(P, lo, g.n, p1_j0, p1_nit);
+    size_t tb = 0;
+    GS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, p1_nit, p1_ioff, nb, e->stream));
+    void* tmp = nullptr;
+    GS_TRY(e->alloc(&tmp, tb > 0 ? tb : 1));
+    GS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, p1_nit, p1_ioff, nb, e->stream));
+    e->release(tmp);
+    k_p1_owner<<<gi, 256, 0, e->stream>>>(nb, p1_nit, p1_ioff, p1_owner, p1_ioff + nb);
+    static const int p1v = getenv("GS_P1_VARIANT") ? atoi(getenv("GS_P1_VARIANT")) : 0;
+    auto kern = p1v == 1 ? k_sk_filter<256, 4, 2> : p1v == 2 ? k_sk_filter<256, 5, 1>
+              : p1v == 3 ? k_sk_filter<256, 6, 1> : k_sk_filter<256, 4, 1>;
+    int occ = 0;
+    GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
+    kern<<<(unsigned)(std::max(occ, 1) * e->sms), 256, 0, e->stream>>>(P, lo, p1_j0, p1_ioff,
+                                                                     p1_owner, p1_ioff + nb,
+                                                                     p1_pend);
+    e->launches += 4;
+    GS_CUDA(cudaGetLastError());
+    P.p1_pend = p1_pend;
+    P.p1_j0 = p1_j0;
+    P.p1_lo = lo;
+  }
+  if (ident) e->kev_mark(3);
   // huge b first (longest work items), with an L2-resident table per CTA
   const int64_t rhuge = rc[4];
   if (g.n > rhuge) {
@@ -936,20 +1148,22 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, g.dmax,
                                      e->stream)));
   }
-  if (ident) e->kev_mark(3);
+  if (ident) e->kev_mark(4);
   // shared memory per CTA: hub bitmap (top 2^18 ranks: 32 KB) + cuckoo table
   // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
   // per candidate of a chunk); the small class runs warp-per-b
   slot(CTR_B_LARGE);
   GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
-  if (ident) e->kev_mark(4);
+  if (ident) e->kev_mark(5);
   slot(CTR_B_MED);
   GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024, dcls[1], e->stream)));
-  if (ident) e->kev_mark(5);
+  if (ident) e->kev_mark(6);
   slot(CTR_B_SMALL);
   GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
-  if (ident) e->kev_mark(6);
+  if (ident) e->kev_mark(7);
   slot(CTR_B_TINY);
+  P.p1_pend = nullptr;  // the tiny class (deg b < 64) is not in stage 1
+  P.p1_j0 = nullptr;
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
@@ -957,7 +1171,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     e->launches++;
     GS_CUDA(cudaGetLastError());
   }
-  if (ident) e->kev_mark(7);
+  if (ident) e->kev_mark(8);
+  for (int32_t* x : {p1_j0, p1_nit, p1_ioff, p1_owner, p1_pend}) e->release(x);
   if (P.gtab) {
     GS_CUDA(cudaStreamSynchronize(e->stream));
     e->release(P.gtab);

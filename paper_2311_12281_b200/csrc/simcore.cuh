@@ -586,6 +586,56 @@ __device__ __forceinline__ bool sk_thread_rejects(const uint32_t* __restrict__ A
   return false;
 }
 
+// 256-bit global load (sm_100: LDG.E.256): one whole 32-byte sector per thread
+__device__ __forceinline__ void ldg256(const uint32_t* p, uint32_t (&r)[8]) {
+  asm("ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "l"(p));
+}
+
+// Thread-per-edge sketch bound with 32-byte loads: the row walk of
+// sk_thread_rejects, but every load fetches one whole sector, so an L1
+// wavefront carries 32 useful bytes instead of 16 (a warp's lanes walk 32
+// different rows: with 16-byte loads the L1 was the limiter, 86% busy).  A (S_a)
+// and B (b's level at a's resolution) are global, 32-byte aligned (sketch
+// slots are multiples of 8 words; wa >= 4).  `words` += the words of A read.
+template <int UNROLL>
+__device__ __forceinline__ bool sk_rejects256(const uint32_t* __restrict__ A,
+                                              const uint32_t* __restrict__ B, int64_t wa,
+                                              int64_t da, int32_t cmin,
+                                              unsigned long long& words) {
+  int64_t u = da;
+  if (wa < 8) {  // a 4-word row: one 16-byte step
+    const uint4 x = __ldg(reinterpret_cast<const uint4*>(A));
+    const uint4 y = __ldg(reinterpret_cast<const uint4*>(B));
+    words += 4;
+    u -= __popc(x.x & ~y.x) + __popc(x.y & ~y.y) + __popc(x.z & ~y.z) + __popc(x.w & ~y.w);
+    return u < cmin;
+  }
+  const int64_t q = wa >> 3;
+  for (int64_t j = 0; j < q; j += UNROLL) {
+    uint32_t x[UNROLL][8], y[UNROLL][8];
+#pragma unroll
+    for (int t = 0; t < UNROLL; ++t) {
+      if (j + t < q) {
+        ldg256(A + 8 * (j + t), x[t]);
+        ldg256(B + 8 * (j + t), y[t]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[t][k] = y[t][k] = 0u;
+      }
+    }
+    words += 8ull * (unsigned long long)min((int64_t)UNROLL, q - j);
+#pragma unroll
+    for (int t = 0; t < UNROLL; ++t)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) u -= __popc(x[t][k] & ~y[t][k]);
+    if (u < cmin) return true;
+  }
+  return false;
+}
+
 // Stage S_b (wb words) and its folds into `lev`: level L (wb >> L words)
 // starts at word 2 (wb - (wb >> L)), so a's level (wa words) is at
 // lev + 2 (wb - wa).  Threads [t0, t0 + nt) cooperate; sync() orders the

@@ -82,9 +82,10 @@ def reduce_stats(st: _lib.GsStats, group=None) -> _lib.GsStats:
                       device=dev)
     dist.all_reduce(kb, op=dist.ReduceOp.SUM, group=group)
     kbl = kb.tolist()
-    for i in range(6):
+    nk = len(st.kernel_bytes)
+    for i in range(nk):
         st.kernel_bytes[i] = int(kbl[i])
-    st.wsim_bytes, st.pcie_bytes = int(kbl[6]), int(kbl[7])
+    st.wsim_bytes, st.pcie_bytes = int(kbl[nk]), int(kbl[nk + 1])
     for i, v in enumerate(ph.tolist()):
         st.phase_ms[i] = v
     return st

@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     bound = {s[0] for s in _lib.SIGNATURES}
     assert bound == set(declared_functions())
-    assert lib.gs_version() == 2  # ABI 2: gs_stats grew kernel_bytes, wsim_bytes, pcie_bytes
+    assert lib.gs_version() == 3  # ABI 3: kernel_bytes[7] (+ the sketch filter class)
     assert isinstance(lib.gs_last_error(), bytes)
 
 

@@ -9,7 +9,8 @@ record taken on other sources: `roofline.traffic` is then null).
 
 Classes (gs_stats.kernel_bytes order): 0 prep (thresholds, degree tables,
 hub split, sketch build, Lemma-1 pre-pass), 1 k_sim_hash<1024,true>,
-2 k_sim_hash<1024,false>, 3 k_sim_hash<512,false>, 4 k_sim_warp, 5 k_sim_tiny.
+2 k_sim_hash<1024,false>, 3 k_sim_hash<512,false>, 4 k_sim_warp, 5 k_sim_tiny,
+6 identify stage 1 (k_p1_items, k_p1_owner, k_sk_filter).
 """
 
 from __future__ import annotations
@@ -40,6 +41,8 @@ def kernel_class(name: str):
         return 4
     if "k_sim_tiny" in name:
         return 5
+    if any(k in name for k in ("k_sk_filter", "k_p1_items", "k_p1_owner")):
+        return 6
     if any(k in name for k in PREP):
         return 0
     return None

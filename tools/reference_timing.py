@@ -85,7 +85,7 @@ def main():
         res, st = gs.scan_in_memory(g, args.mu, args.eps)
         rec["engine_scan_in_memory_wall_s"] = round(time.perf_counter() - t0, 4)
         ref_view = graphscan.ClusteringResult(
-            n=res.n, roles=[graphscan.Role(int(r.value)) for r in res.roles],
+            n=res.n, roles=[graphscan.Role(r.value) for r in res.roles],
             cluster_id=list(res.cluster_id), orig_ids=list(res.orig_ids))
         rep = results_equivalent(ref_view, oracle_res)
         rec["engine_equivalent_to_serial_scan"] = bool(rep)
