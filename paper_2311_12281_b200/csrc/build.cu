@@ -1145,7 +1145,8 @@ __device__ __forceinline__ void fused_run_regs(const int32_t* __restrict__ adj,
 // warp per caller vertex with d <= 32 (lane i holds element i): register
 // bitonic network; d in (32, 511]: warp per vertex, K = 2..16 keys per lane
 // (warp_bitonic_sort).  Longer runs are skipped (CTA kernels below).
-__global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ off, int64_t n,
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused_warp(const int64_t* __restrict__ off, int64_t n,
                                                     const int32_t* __restrict__ adj,
                                                     const int32_t* __restrict__ rank,
                                                     const int64_t* __restrict__ noff,
@@ -1172,6 +1173,11 @@ __global__ void __launch_bounds__(256) k_fused_warp(const int64_t* __restrict__ 
       myr = rank[myu];
       if (myr < row_lo || myr >= row_hi) myd = 0;
     }
+    // the group's runs are then read one after another: pull their first
+    // 512 bytes into L2 now, so each run's reads wait for L2, not DRAM
+    if (myd > 0 && myd < kHeavyScatter)
+      for (int t = 0; t < myd && t < 128; t += 32)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(adj + myo + t));
     uint32_t rest = __ballot_sync(0xffffffffu, myd > 16 && myd < kHeavyScatter);
     // runs of <= 8: four per round (8 lanes each), of 9..16: two per round
     segmented_runs<8>(__ballot_sync(0xffffffffu, myd > 0 && myd <= 8), lane, g0, myo, myd, myr,
@@ -1280,7 +1286,9 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   e->release(d_cls);
   e->launches++;
   const int endbit = std::min(32, bits_for(n - 1) + 1);
-  k_fused_warp<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
+  static const int fminb = getenv("GS_FUSED_MINB") ? atoi(getenv("GS_FUSED_MINB")) : 4;
+  auto fk = fminb >= 6 ? k_fused_warp<6> : fminb == 5 ? k_fused_warp<5> : k_fused_warp<4>;
+  fk<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
                  0, st>>>(off, n, adj, g.rank, g.off, arcs, d_bad, row_lo, row_hi);
   e->launches++;
   auto clip = [&](int64_t x) { return std::min(std::max(x, row_lo), row_hi); };
