@@ -588,6 +588,100 @@ __global__ void k_run_dups(const int64_t* __restrict__ off, int64_t rlo, int64_t
   if (dup) atomicExch(bad, 5);
 }
 
+// The long runs (ranks [rbig, row_hi), >= 4096 neighbours, already
+// scattered into `arcs`) sorted on stream `st`: as segments over the neighbour
+// bits (cub segmented radix sort), then the duplicate check.  With `defer`
+// the scratch blocks are handed back to the caller, who releases them once
+// `st` has joined the engine stream (the engine's block cache is ordered by
+// the engine stream only).
+static int sort_hub_tail(gs_engine* e, cudaStream_t st, int64_t n, int32_t* arcs, int* d_bad,
+                         int64_t rbig, int64_t row_hi, std::vector<void*>* defer) {
+  DevGraph& g = e->g;
+  if (row_hi <= rbig) return GS_OK;
+  int64_t hbig = 0, hend = 0;
+  GS_CUDA(cudaMemcpyAsync(&hbig, g.off + rbig, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaMemcpyAsync(&hend, g.off + row_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  const int64_t cnt = hend - hbig;
+  const bool seg_tail = !(getenv("GS_SEG_TAIL") && atoi(getenv("GS_SEG_TAIL")) == 0);
+  auto drop = [&](void* p) {
+    if (defer) defer->push_back(p); else e->release(p);
+  };
+  if (cnt > 0 && seg_tail) {
+    // the long runs sorted as segments over the neighbour bits only (int32
+    // keys, B bits) instead of one radix sort of 64-bit (run, neighbour) keys
+    // (batches of runs holding < 2^30 slots: the segmented sort counts items in int)
+    const int B = bits_for(n - 1);
+    const int64_t nseg = row_hi - rbig;
+    std::vector<int64_t> hoff(nseg + 1);
+    GS_CUDA(cudaMemcpyAsync(hoff.data(), g.off + rbig, sizeof(int64_t) * (size_t)(nseg + 1),
+                            cudaMemcpyDeviceToHost, st));
+    GS_CUDA(cudaStreamSynchronize(st));
+    int64_t kBatch = (int64_t)1 << 30;
+    if (const char* v = getenv("GS_SEG_BATCH")) kBatch = std::max<int64_t>(1, atoll(v));  // tests
+    std::vector<int64_t> cut{0};  // batch boundaries (run indices); a batch holds >= 1 run
+    int64_t most = 0;
+    for (int64_t a = 0; a < nseg;) {
+      int64_t z = a + 1;
+      while (z < nseg && hoff[z + 1] - hoff[a] <= kBatch) ++z;
+      most = std::max(most, hoff[z] - hoff[a]);
+      cut.push_back(z);
+      a = z;
+    }
+    int64_t* segoff = nullptr;
+    int32_t* tmp = nullptr;
+    GS_TRY(e->alloc_n(&segoff, nseg + 1));
+    GS_TRY(e->alloc_n(&tmp, most));
+    for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
+      const int64_t a = cut[bi], z = cut[bi + 1];  // runs [a, z)
+      const int64_t base = hoff[a], items = hoff[z] - base;
+      k_rebase<<<grid_for(z - a + 1, 256), 256, 0, st>>>(g.off + rbig + a, z - a + 1, base,
+                                                          segoff);
+      cub::DoubleBuffer<int32_t> db(arcs + base, tmp);
+      size_t tb = 0;
+      GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tb, db, (int)items, (int)(z - a),
+                                                      segoff, segoff + 1, 0, B, st));
+      void* t = nullptr;
+      GS_TRY(e->alloc(&t, tb > 0 ? tb : 1));
+      GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(t, tb, db, (int)items, (int)(z - a), segoff,
+                                                      segoff + 1, 0, B, st));
+      if (db.Current() != arcs + base)
+        GS_CUDA(cudaMemcpyAsync(arcs + base, db.Current(), sizeof(int32_t) * (size_t)items,
+                                cudaMemcpyDeviceToDevice, st));
+      GS_CUDA(cudaStreamSynchronize(st));  // segoff / tmp reuse across batches
+      drop(t);
+      e->launches += 2;
+    }
+    k_run_dups<<<(unsigned)std::min<int64_t>(grid_for(cnt, 256), (int64_t)e->sms * 16), 256, 0,
+                 st>>>(g.off, rbig, row_hi, hbig, hend, arcs, d_bad);
+    e->launches++;
+    drop(segoff);
+    drop(tmp);
+  } else if (cnt > 0) {
+    const int B = bits_for(n - 1);
+    const int R = bits_for(row_hi - 1 - rbig);
+    uint64_t *k1 = nullptr, *k2 = nullptr;
+    GS_TRY(e->alloc_n(&k1, cnt));
+    GS_TRY(e->alloc_n(&k2, cnt));
+    const int64_t nv = row_hi - rbig;
+    k_tail_keys<<<(unsigned)(nv < 65535 * 4 ? nv : 65535 * 4), 256, 0, st>>>(g.off, rbig, row_hi,
+                                                                            arcs, B, k1);
+    cub::DoubleBuffer<uint64_t> db(k1, k2);
+    size_t tb = 0;
+    GS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, cnt, 0, B + R, st));
+    void* t = nullptr;
+    GS_TRY(e->alloc(&t, tb > 0 ? tb : 1));
+    GS_CUDA(cub::DeviceRadixSort::SortKeys(t, tb, db, cnt, 0, B + R, st));
+    k_tail_extract<<<e->sms * 16, 256, 0, st>>>(db.Current(), cnt, B, arcs + hbig, d_bad);
+    e->launches += 3;
+    drop(t);
+    drop(k1);
+    drop(k2);
+  }
+  GS_CUDA(cudaGetLastError());
+  return GS_OK;
+}
+
 // Sort every run of `arcs` (offsets g.off) in place.
 static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int* d_bad,
                      int64_t row_lo, int64_t row_hi, bool classes_done = false) {
@@ -597,7 +691,7 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
   int64_t* d_cls = nullptr;
   GS_TRY(e->alloc_n(&d_cls, 7));
   k_sort_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
-  int64_t r[7], hbig = 0;
+  int64_t r[7];
   GS_CUDA(cudaMemcpyAsync(r, d_cls, sizeof(r), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_cls);
@@ -646,79 +740,7 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
     e->launches++;
   }
   GS_CUDA(cudaGetLastError());
-  // long runs of this part: ranks [rbig, row_hi)
-  int64_t hend = 0;
-  GS_CUDA(cudaMemcpyAsync(&hbig, g.off + rbig, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GS_CUDA(cudaMemcpyAsync(&hend, g.off + row_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  GS_CUDA(cudaStreamSynchronize(st));
-  const int64_t cnt = hend - hbig;
-  (void)slots;
-  const bool seg_tail = !(getenv("GS_SEG_TAIL") && atoi(getenv("GS_SEG_TAIL")) == 0);
-  if (cnt > 0 && seg_tail) {
-    // the long runs sorted as segments over the neighbour bits only (int32
-    // keys, B bits) instead of one radix sort of 64-bit (run, neighbour) keys
-    // (batches of runs holding < 2^30 slots: the segmented sort counts items in int)
-    const int B = bits_for(n - 1);
-    const int64_t nseg = row_hi - rbig;
-    std::vector<int64_t> hoff(nseg + 1);
-    GS_CUDA(cudaMemcpyAsync(hoff.data(), g.off + rbig, sizeof(int64_t) * (size_t)(nseg + 1),
-                            cudaMemcpyDeviceToHost, st));
-    GS_CUDA(cudaStreamSynchronize(st));
-    int64_t kBatch = (int64_t)1 << 30;
-    if (const char* v = getenv("GS_SEG_BATCH")) kBatch = std::max<int64_t>(1, atoll(v));  // tests
-    std::vector<int64_t> cut{0};  // batch boundaries (run indices); a batch holds >= 1 run
-    int64_t most = 0;
-    for (int64_t a = 0; a < nseg;) {
-      int64_t z = a + 1;
-      while (z < nseg && hoff[z + 1] - hoff[a] <= kBatch) ++z;
-      most = std::max(most, hoff[z] - hoff[a]);
-      cut.push_back(z);
-      a = z;
-    }
-    int64_t* segoff = nullptr;
-    int32_t* tmp = nullptr;
-    GS_TRY(e->alloc_n(&segoff, nseg + 1));
-    GS_TRY(e->alloc_n(&tmp, most));
-    for (size_t bi = 0; bi + 1 < cut.size(); ++bi) {
-      const int64_t a = cut[bi], z = cut[bi + 1];  // runs [a, z)
-      const int64_t base = hoff[a], items = hoff[z] - base;
-      k_rebase<<<grid_for(z - a + 1, 256), 256, 0, st>>>(g.off + rbig + a, z - a + 1, base,
-                                                          segoff);
-      cub::DoubleBuffer<int32_t> db(arcs + base, tmp);
-      GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-        return cub::DeviceSegmentedRadixSort::SortKeys(t, b, db, (int)items, (int)(z - a), segoff,
-                                                       segoff + 1, 0, B, st);
-      }));
-      if (db.Current() != arcs + base)
-        GS_CUDA(cudaMemcpyAsync(arcs + base, db.Current(), sizeof(int32_t) * (size_t)items,
-                                cudaMemcpyDeviceToDevice, st));
-      e->launches += 2;
-    }
-    k_run_dups<<<(unsigned)std::min<int64_t>(grid_for(cnt, 256), (int64_t)e->sms * 16), 256, 0,
-                 st>>>(g.off, rbig, row_hi, hbig, hend, arcs, d_bad);
-    e->launches++;
-    GS_CUDA(cudaStreamSynchronize(st));  // hoff / segoff reuse across batches is stream-ordered
-    e->release(segoff);
-    e->release(tmp);
-  } else if (cnt > 0) {
-    const int B = bits_for(n - 1);
-    const int R = bits_for(row_hi - 1 - rbig);
-    uint64_t *k1 = nullptr, *k2 = nullptr;
-    GS_TRY(e->alloc_n(&k1, cnt));
-    GS_TRY(e->alloc_n(&k2, cnt));
-    const int64_t nv = row_hi - rbig;
-    k_tail_keys<<<(unsigned)(nv < 65535 * 4 ? nv : 65535 * 4), 256, 0, st>>>(g.off, rbig, row_hi,
-                                                                            arcs, B, k1);
-    cub::DoubleBuffer<uint64_t> db(k1, k2);
-    GS_TRY(cub_call(e, [&](void* t, size_t& b) {
-      return cub::DeviceRadixSort::SortKeys(t, b, db, cnt, 0, B + R, st);
-    }));
-    k_tail_extract<<<e->sms * 16, 256, 0, st>>>(db.Current(), cnt, B, arcs + hbig, d_bad);
-    e->launches += 3;
-    e->release(k1);
-    e->release(k2);
-  }
-  return GS_OK;
+  return sort_hub_tail(e, st, n, arcs, d_bad, rbig, row_hi, nullptr);
 }
 
 // shared tail: arcs scattered into their runs (`arcs`, 2m) -> sorted CSR
@@ -891,8 +913,8 @@ static int arcs_buffer(gs_engine* e, int64_t slots, int32_t* adj_out, int32_t** 
 // after the scatter: sort this part's runs, then finish now or on finish_build
 static int finish_part(gs_engine* e, int64_t n, int64_t m, int32_t* arcs, const int64_t* h_cls,
                        int* d_bad, int64_t row_lo, int64_t row_hi, bool defer,
-                       bool classes_done = false) {
-  GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, row_lo, row_hi, classes_done));
+                       bool classes_done = false, bool all_sorted = false) {
+  if (!all_sorted) GS_TRY(sort_runs(e, n, 2 * m, arcs, d_bad, row_lo, row_hi, classes_done));
   e->g.adj = arcs;
   if (!defer) return finish_rest(e, n, m, h_cls, d_bad);
   GS_CUDA(cudaStreamSynchronize(e->stream));  // the part is complete for the exchange
@@ -940,7 +962,7 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const
   const bool fused = m > 0 && !(getenv("GS_FUSED_BUILD") && atoi(getenv("GS_FUSED_BUILD")) == 0);
   if (fused) {
     GS_TRY(fused_scatter_sort(e, n, m, off, adj, arcs, d_bad, row_lo, row_hi, h_cls[2]));
-    return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, true);
+    return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, true, true);
   }
   if (m > 0) {
     k_scatter_csr<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
@@ -1270,32 +1292,105 @@ __global__ void __launch_bounds__(NT) k_fused_block(const int64_t* __restrict__ 
   if (b5) atomicExch(bad, 5);
 }
 
-// the device-CSR build's relabel + per-run sorts, fused (runs >= 4096 are
-// only scattered here; sort_runs sorts them afterwards)
+// ... for runs of up to 16384 neighbours: one 1024-thread CTA per run, the
+// block radix sort's scratch in dynamic shared memory (beyond the 48 KB static
+// limit); replaces scatter + segmented radix sort for these hub runs
+template <int NT, int ITEMS>
+__global__ void __launch_bounds__(NT, 1) k_fused_block_dyn(const int64_t* __restrict__ off,
+                                                           int64_t n, int64_t rlo, int64_t rhi,
+                                                           const int32_t* __restrict__ orig,
+                                                           const int32_t* __restrict__ adj,
+                                                           const int32_t* __restrict__ rank,
+                                                           const int64_t* __restrict__ noff,
+                                                           int endbit, int32_t* __restrict__ out,
+                                                           int* __restrict__ bad) {
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(dsm);
+  const int t = threadIdx.x;
+  bool b3 = false, b4 = false, b5 = false;
+  for (int64_t r = rlo + blockIdx.x; r < rhi; r += gridDim.x) {
+    const int64_t u = orig[r];
+    const int64_t ou = off[u];
+    const int d = (int)(off[u + 1] - ou);
+    uint32_t k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      k[i] = idx < d ? (uint32_t)rank[fused_check(adj, ou + idx, ou, n, u, b3, b4)] : 0xFFFFFFFFu;
+    }
+    Sort(tmp).SortBlockedToStriped(k, 0, endbit);
+    int32_t* o = out + noff[r];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx < d) o[idx] = (int32_t)k[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx + 1 < d) b5 |= o[idx] == o[idx + 1];
+    }
+    __syncthreads();
+  }
+  if (b3) atomicExch(bad, 3);
+  if (b4) atomicExch(bad, 4);
+  if (b5) atomicExch(bad, 5);
+}
+
+__global__ void k_fused_classes(const int64_t* __restrict__ off, int64_t n,
+                                int64_t* __restrict__ out) {
+  const int64_t th[5] = {1025, 2049, 4096, 16385, 0};
+  const int c = threadIdx.x;
+  if (c < 4) out[c] = rank_of_degree(off, n, th[c]);
+}
+
+// the device-CSR build's relabel + per-run sorts, fused.  Runs of > 16384
+// neighbours are scattered and sorted as segments on the copy stream (idle in
+// this build) while the engine stream sorts everything shorter; the engine
+// stream joins it before the CSR is finished.
 static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t* off,
                               const int32_t* adj, int32_t* arcs, int* d_bad, int64_t row_lo,
                               int64_t row_hi, int64_t r512) {
   DevGraph& g = e->g;
-  cudaStream_t st = e->stream;
+  cudaStream_t st = e->stream, cs = e->cstream;
   int64_t* d_cls = nullptr;
-  GS_TRY(e->alloc_n(&d_cls, 8));
-  k_sort_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
-  int64_t r[7];
-  GS_CUDA(cudaMemcpyAsync(r, d_cls, 7 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GS_TRY(e->alloc_n(&d_cls, 4));
+  k_fused_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
+  int64_t r[4];
+  GS_CUDA(cudaMemcpyAsync(r, d_cls, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_cls);
   e->launches++;
   const int endbit = std::min(32, bits_for(n - 1) + 1);
-  static const int fminb = getenv("GS_FUSED_MINB") ? atoi(getenv("GS_FUSED_MINB")) : 4;
+  auto clip = [&](int64_t x) { return std::min(std::max(x, row_lo), row_hi); };
+  // rank ranges by degree (ranks ascend with the degree): [512, 1024], [1025, 2048],
+  // [2049, 4095], [4096, 16384], > 16384 (r512 = first rank of degree >= 512, h_cls[2])
+  const int64_t h512 = clip(r512), h1025 = clip(r[0]), h2049 = clip(r[1]), h4096 = clip(r[2]),
+                h16k = clip(r[3]);
+  static const bool two_streams = !(getenv("GS_BUILD_STREAMS") && atoi(getenv("GS_BUILD_STREAMS")) == 1);
+  // the longest runs first, on the copy stream: scatter, then the segmented sort
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<void*> deferred;
+  cudaStream_t hs = two_streams ? cs : st;
+  if (row_hi > h16k && two_streams) {
+    GS_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    GS_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+    GS_CUDA(cudaEventRecord(ev0, st));
+    GS_CUDA(cudaStreamWaitEvent(cs, ev0, 0));
+  }
+  if (row_hi > h16k) {
+    k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(row_hi - h16k, (int64_t)e->sms * 16), 256,
+                          0, hs>>>(off, n, h16k, row_hi, g.orig, adj, 0, 2 * m, 0, g.rank,
+                                   g.off, arcs, d_bad);
+    e->launches++;
+  }
+  static const int fminb = getenv("GS_FUSED_MINB") ? atoi(getenv("GS_FUSED_MINB")) : 6;
   auto fk = fminb >= 6 ? k_fused_warp<6> : fminb == 5 ? k_fused_warp<5> : k_fused_warp<4>;
   fk<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
                  0, st>>>(off, n, adj, g.rank, g.off, arcs, d_bad, row_lo, row_hi);
   e->launches++;
-  auto clip = [&](int64_t x) { return std::min(std::max(x, row_lo), row_hi); };
-  // rank ranges by degree (ranks ascend with the degree): [512, 1024], [1025, 2048],
-  // [2049, 4095], >= 4096 (r512 = first rank of degree >= 512, h_cls[2])
-  const int64_t h512 = clip(r512), h1025 = clip(r[4]), h2049 = clip(r[5]),
-                h4096 = clip(r[6]);
   auto blocks = [&](int64_t runs) {
     return (unsigned)std::min<int64_t>(std::max<int64_t>(runs, 1), (int64_t)e->sms * 16);
   };
@@ -1308,12 +1403,25 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   if (h4096 > h2049)
     k_fused_block<256, 16><<<blocks(h4096 - h2049), 256, 0, st>>>(
         off, n, h2049, h4096, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
-  if (row_hi > h4096)  // longest runs: scattered, sorted by sort_runs' radix tail
-    k_scatter_csr_heavy<<<(unsigned)std::min<int64_t>(row_hi - h4096, (int64_t)e->sms * 16), 256,
-                          0, st>>>(off, n, h4096, row_hi, g.orig, adj, 0, 2 * m, 0, g.rank,
-                                   g.off, arcs, d_bad);
+  if (h16k > h4096) {
+    auto kb = k_fused_block_dyn<1024, 16>;
+    const int sm = (int)sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16>::TempStorage);
+    GS_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    kb<<<(unsigned)std::min<int64_t>(h16k - h4096, (int64_t)e->sms), 1024, sm, st>>>(
+        off, n, h4096, h16k, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+  }
   e->launches += 4;
   GS_CUDA(cudaGetLastError());
+  if (row_hi > h16k) {  // host syncs on the copy stream only: the engine stream keeps running
+    GS_TRY(sort_hub_tail(e, hs, n, arcs, d_bad, h16k, row_hi, two_streams ? &deferred : nullptr));
+    if (two_streams) {
+      GS_CUDA(cudaEventRecord(ev1, cs));
+      GS_CUDA(cudaStreamWaitEvent(st, ev1, 0));
+    }
+  }
+  for (void* p : deferred) e->release(p);  // stream-ordered after the join
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
   return GS_OK;
 }
 
