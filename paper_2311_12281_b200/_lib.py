@@ -143,9 +143,19 @@ _lib = None
 _lock = threading.Lock()
 
 
+_warm_thread: Optional[threading.Thread] = None
+
+
 def load() -> ctypes.CDLL:
-    """Load libgscan.so (once).  Raises ImportError if it was never built."""
+    """Load libgscan.so (once).  Raises ImportError if it was never built.
+
+    A caller other than the warm-up thread first waits for it: two threads
+    loading kernels lazily at once serialise on the driver and took 3-5 s
+    together where either alone takes ~1 s."""
     global _lib
+    w = _warm_thread
+    if w is not None and w is not threading.current_thread() and w.is_alive():
+        w.join(timeout=30)
     with _lock:
         if _lib is not None:
             return _lib
@@ -266,6 +276,8 @@ def warm_up_async() -> Optional[threading.Thread]:
         except Exception:  # no library / no device: the first real call reports it
             pass
 
+    global _warm_thread
     t = threading.Thread(target=run, name="gscan-warmup", daemon=True)
+    _warm_thread = t
     t.start()
     return t
