@@ -373,11 +373,40 @@ __global__ void k_hubsplit(const int64_t* __restrict__ off, const int32_t* __res
   if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(&ctr[CTR_B_PREP], bytes);
 }
 
-template <int NT, bool GTAB>
+// Claim the next b with a pending edge and start the bulk copy of N(b) into
+// `buf` (16-byte aligned source: the list starts *pre words in).  Not inlined:
+// its registers stay out of the kernel's scan loop (inlined: 142 B of spills).
+__device__ __noinline__ int pf_claim_copy(int32_t* wq, const int32_t* pend, int64_t p1_lo,
+                                          const int64_t* off, const int32_t* adj, int64_t rlo,
+                                          int64_t rhi, int rank, int world, uint32_t* buf,
+                                          int* pre_out, uint64_t* bar) {
+  for (;;) {
+    const int it = atomicAdd(wq, 1);
+    const int64_t bb = shard_top(rlo, rhi, it, rank, world);
+    if (bb < rlo) return it;
+    if (pend[bb - p1_lo] == 0) continue;
+    const int64_t o = off[bb], d = off[bb + 1] - o;
+    const uintptr_t src = reinterpret_cast<uintptr_t>(adj + o);
+    const uintptr_t s0 = src & ~uintptr_t(15);
+    const uint32_t pre = (uint32_t)((src - s0) >> 2);
+    const uint32_t bytes = (uint32_t)(((pre + d) * 4 + 15) & ~int64_t(15));
+    *pre_out = (int)pre;
+    fence_proxy_async_smem();  // the buffer's last reads (generic proxy) come first
+    bulk_copy_g2s(buf, reinterpret_cast<const void*>(s0), bytes, bar);
+    return it;
+  }
+}
+
+// PF (identify stage 2, medium class): N(b) of the NEXT claimed b is copied
+// into one of two shared-memory buffers by the bulk-copy engine (TMA,
+// cp.async.bulk, completion on an mbarrier) while the CTA works on the current
+// b, whose list is then read from shared memory by the survivor filter, the
+// table build and the bitmap clean-up (`nbuf_words` words per buffer).
+template <int NT, bool GTAB, bool PF = false>
 __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_hash(SimParams P, int64_t rlo, int64_t rhi,
                                                  uint32_t tcap, int qi, int chunk,
                                                  uint32_t hub_lo, uint32_t bm_words,
-                                                 int64_t skw) {
+                                                 int64_t skw, uint32_t nbuf_words) {
   extern __shared__ __align__(16) uint32_t smem[];
   uint32_t* bm = smem;  // [bm_words] + zero guard words (kept 16-byte aligned)
   // bitmap + >= 4 zero guard words, padded so the 16-byte buckets stay aligned
@@ -403,8 +432,33 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   for (uint32_t i = tid; i < ((bm_words + 4 + 3) & ~3u); i += NT) bm[i] = 0u;
 
   const bool p1 = P.p1_pend != nullptr;  // identify stage 2: SIM_PENDING edges only
+  // PF: the prefetched claim, its buffer's mbarrier phase and its list offset
+  __shared__ int s_pitem;
+  __shared__ int s_pref[2];
+  __shared__ __align__(8) uint64_t s_mbar[2];
+  uint32_t* nbuf = sk_lev + ((skw + 3) & ~int64_t(3));
+  const bool pf = PF && p1;
+  int cur = 0;
+  uint32_t phase = 0;  // bit k: parity of buffer k's next completion
+  auto pf_claim = [&](int k) -> int {
+    return pf_claim_copy(P.wq + qi, P.p1_pend, P.p1_lo, P.off, P.adj, rlo, rhi, P.shard_rank,
+                         P.shard_world, nbuf + (size_t)k * nbuf_words, &s_pref[k], &s_mbar[k]);
+  };
+  if (pf && tid == 0) {
+    mbar_init(&s_mbar[0], 1);
+    mbar_init(&s_mbar[1], 1);
+    mbar_init_fence();
+    s_pitem = pf_claim(0);
+  }
   for (;;) {
-    if (tid == 0) s_item = atomicAdd(&P.wq[qi], 1);
+    if (pf) {
+      if (tid == 0) {
+        s_item = s_pitem;
+        if (shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world) >= rlo) s_pitem = pf_claim(cur ^ 1);
+      }
+    } else if (tid == 0) {
+      s_item = atomicAdd(&P.wq[qi], 1);
+    }
     __syncthreads();
     const int64_t b = shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world);
     if (b < rlo) break;
@@ -415,6 +469,13 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
     const int64_t ob = P.off[b], db = P.off[b + 1] - ob;
     const int64_t e0 = P.eoff[b], nlow = P.eoff[b + 1] - e0;
     const int32_t* __restrict__ nb = P.adj + ob;
+    // N(b) as the CTA reads it: the landed shared-memory copy (PF) or global
+    const int32_t* nbl = nb;
+    if (pf) {
+      mbar_wait(&s_mbar[cur], (phase >> cur) & 1u);
+      phase ^= 1u << cur;
+      nbl = reinterpret_cast<const int32_t*>(nbuf + (size_t)cur * nbuf_words) + s_pref[cur];
+    }
     const int2 th = P.thr[db];
     const int64_t xmin = th.x, simmax = th.y;
     bool built = false, sk_staged = false, wsim_b = false;
@@ -430,7 +491,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       for (int64_t j = base + tid; j < lim; j += NT) {
         const int64_t e = e0 + j;
         if (p1 && P.sim[e] != SIM_PENDING) continue;  // decided (or skipped) by stage 1
-        const int32_t a = nb[j];
+        const int32_t a = nbl[j];
         const int64_t oa = P.off[a];
         const int64_t da = P.off[a + 1] - oa;
         if (p1) ctr_add(lc, LC_BYTES, kBytesCand);
@@ -528,7 +589,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
               reinterpret_cast<uint4*>(C.tab)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
           __syncthreads();
           for (int64_t i = tid; i < db; i += NT) {
-            const uint32_t w = (uint32_t)nb[i];
+            const uint32_t w = (uint32_t)nbl[i];
             if (i >= nlo) {
               const uint32_t r = w - hub_lo;
               atomicOr(&bm[r >> 5], 1u << (r & 31));
@@ -601,10 +662,11 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       __syncthreads();
     }
     if (built) {  // clear the bitmap words this b set (O(deg b), not O(R))
-      for (int64_t i = s_nlo + tid; i < db; i += NT) bm[((uint32_t)nb[i] - hub_lo) >> 5] = 0u;
+      for (int64_t i = s_nlo + tid; i < db; i += NT) bm[((uint32_t)nbl[i] - hub_lo) >> 5] = 0u;
     }
     hot_flush_warp(lc, s_ctr);
     __syncthreads();  // bitmap clean and s_item read by all before the next b
+    cur ^= 1;
   }
   hot_flush_warp(lc, s_ctr);
   shared_ctr_flush(P, s_ctr);
@@ -922,15 +984,17 @@ __global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo
 // ---------------------------------------------------------------------------
 // host driver
 
-template <int NT, bool GTAB>
+template <int NT, bool GTAB, bool PF = false>
 static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rhi,
                        uint32_t tcap, int qi, int chunk, int64_t dcls, cudaStream_t st) {
   if (rhi <= rlo) return GS_OK;
   size_t smem =
       (size_t)((P.bm_words + 4 + 3) & ~3u) * 4 + (GTAB ? 0 : (size_t)tcap * 16) + (size_t)chunk * 24;
-  // b's sketch levels in shared memory when they fit (else folded from global)
+  // b's sketch levels in shared memory when they fit (else folded from global);
+  // identify stage 2 needs none (stage 1 applied the sketch bound)
   int64_t skw = 0;
-  if (P.sk != nullptr) {
+  const bool p1 = P.p1_pend != nullptr;
+  if (P.sk != nullptr && !p1) {
     // dcls bounds the class's degrees (no device read, no host sync)
     const int64_t want = 2 * sk_words(dcls, P.sk_lk);
     const int64_t room = ((int64_t)e->smem_optin - 1024 - (int64_t)smem) / 4;  // static smem
@@ -941,7 +1005,24 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
     }
     smem += (size_t)skw * 4;
   }
-  auto kern = k_sim_hash<NT, GTAB>;
+  // PF: two N(b) buffers for the bulk-copy prefetch -- measured and off by
+  // default (GS_TMA=1 enables): the prefetch state costs 118 B of spills at the
+  // 64-register cap and the buffers halve the survivor chunk; s24 eps 0.2 medium
+  // class 12.8 -> 14.9 ms (eps 0.5: 0.31 -> 0.27 ms), DESIGN 3c
+  static const bool tma_on = getenv("GS_TMA") && atoi(getenv("GS_TMA")) == 1;
+  const bool pf = PF && p1 && tma_on;
+  uint32_t nbuf_words = 0;
+  if (pf) {
+    nbuf_words = (uint32_t)((dcls + 8 + 3) & ~int64_t(3));
+    smem += 2ull * nbuf_words * 4;
+    // keep two CTAs per SM: halve the survivor chunk if the buffers do not fit
+    static const bool keep_chunk = getenv("GS_TMA_KEEPCHUNK") != nullptr;  // experiments
+    if (!keep_chunk && 2 * (smem + 1024) > 228 * 1024 && chunk > 256) {
+      smem -= (size_t)chunk * 12;
+      chunk /= 2;
+    }
+  }
+  auto kern = pf ? k_sim_hash<NT, GTAB, PF> : k_sim_hash<NT, GTAB, false>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -950,7 +1031,7 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   if (grid > rhi - rlo) grid = rhi - rlo;
   if (GTAB && grid > e->sms * 2) grid = e->sms * 2;
   kern<<<(unsigned)grid, NT, smem, st>>>(P, rlo, rhi, tcap, qi, chunk, P.hub_lo, P.bm_words,
-                                         skw);
+                                         skw, nbuf_words);
   e->launches++;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
@@ -1156,7 +1237,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
   if (ident) e->kev_mark(5);
   slot(CTR_B_MED);
-  GS_TRY((launch_hash<512, false>(e, P, rc[2], rc[3], 2048, 2, 1024, dcls[1], e->stream)));
+  static const int med_chunk = getenv("GS_MED_CHUNK") ? atoi(getenv("GS_MED_CHUNK")) : 1024;
+  GS_TRY((launch_hash<512, false, true>(e, P, rc[2], rc[3], 2048, 2, med_chunk, dcls[1], e->stream)));
   if (ident) e->kev_mark(6);
   slot(CTR_B_SMALL);
   GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
