@@ -423,6 +423,90 @@ __global__ void k_sort_classes(const int64_t* __restrict__ off, int64_t n,
   if (c < 7) out[c] = rank_of_degree(off, n, th[c]);
 }
 
+// Warp-wide bitonic sort of 32 K keys held K per lane, "blocked" (lane l holds
+// positions lK .. lK + K - 1), ascending.  Partner distances j < K are register
+// compare-swaps, j >= K shuffles; the direction bit (i & k) is a compile-time
+// constant for k < K and a function of the lane alone for k >= K.  (The
+// shared-memory network it replaces issued ~2x the instructions: two loads,
+// two stores and the index arithmetic per compare, plus a __syncwarp per stage.)
+template <int K>
+__device__ __forceinline__ void warp_bitonic_sort(int32_t (&x)[K], int lane) {
+  constexpr int P = 32 * K;
+#pragma unroll
+  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < K) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int p = r ^ j;
+          if (p > r) {
+            const bool up = k < K ? (r & k) == 0 : (lane & (k / K)) == 0;
+            const int32_t lo = min(x[r], x[p]), hi = max(x[r], x[p]);
+            x[r] = up ? lo : hi;
+            x[p] = up ? hi : lo;
+          }
+        }
+      } else {
+        const int lj = j / K;
+        const bool keep_lo = ((lane & lj) == 0) == ((lane & (k / K)) == 0);
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const int32_t y = __shfl_xor_sync(0xffffffffu, x[r], lj);
+          x[r] = keep_lo ? min(x[r], y) : max(x[r], y);
+        }
+      }
+    }
+  }
+}
+
+// one run of d in (32 (K / 2), 32 K] slots of `o`, sorted in place by the warp
+// (registers; a padded shared-memory transpose for the coalesced write-back)
+template <int K>
+__device__ __forceinline__ void sort_run_inplace(int32_t* o, int d, int32_t* sbuf, int lane,
+                                                 bool& dup) {
+  int32_t x[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int i = lane + 32 * r;
+    x[r] = i < d ? o[i] : kPad;
+  }
+  warp_bitonic_sort<K>(x, lane);
+#pragma unroll
+  for (int r = 0; r < K; ++r) sbuf[lane * (K + 1) + r] = x[r];
+  __syncwarp();
+  for (int i = lane; i < d; i += 32) {
+    const int32_t v = sbuf[(i / K) * (K + 1) + i % K];
+    o[i] = v;
+    if (i + 1 < d) dup |= sbuf[((i + 1) / K) * (K + 1) + (i + 1) % K] == v;
+  }
+  __syncwarp();
+}
+
+// runs of 33..512 slots: one warp per run, K = 2..16 keys per lane (replaces a
+// shared-memory bitonic network for 33..256 and a 128-thread block radix sort
+// for 257..512)
+__global__ void __launch_bounds__(256) k_sort_runs_wreg(const int64_t* __restrict__ off,
+                                                        RunSet R, int32_t* __restrict__ arcs,
+                                                        int* __restrict__ bad) {
+  __shared__ int32_t buf[8 * 32 * 17];
+  const int lane = threadIdx.x & 31;
+  int32_t* sbuf = buf + (threadIdx.x >> 5) * (32 * 17);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nr = rs_size(R);
+  bool dup = false;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < nr; it += nw) {
+    const int64_t v = rs_at(R, it);
+    const int64_t o = off[v];
+    const int d = (int)(off[v + 1] - o);
+    if (d <= 64) sort_run_inplace<2>(arcs + o, d, sbuf, lane, dup);
+    else if (d <= 128) sort_run_inplace<4>(arcs + o, d, sbuf, lane, dup);
+    else if (d <= 256) sort_run_inplace<8>(arcs + o, d, sbuf, lane, dup);
+    else sort_run_inplace<16>(arcs + o, d, sbuf, lane, dup);
+  }
+  if (dup) atomicExch(bad, 5);
+}
+
 __global__ void __launch_bounds__(256) k_sort_runs_reg(const int64_t* __restrict__ off,
                                                        RunSet R, int32_t* __restrict__ arcs,
                                                        int* __restrict__ bad) {
@@ -713,15 +797,15 @@ static int sort_runs(gs_engine* e, int64_t n, int64_t slots, int32_t* arcs, int*
     e->launches++;
   }
   if (!classes_done && r257 > r33) {
-    k_sort_runs_smem<false, 256><<<warps_grid(r257 - r33), 256, 0, st>>>(g.off, RunSet{r33, r257, nullptr, nullptr}, arcs,
+    k_sort_runs_wreg<<<warps_grid(r257 - r33), 256, 0, st>>>(g.off, RunSet{r33, r257, nullptr, nullptr}, arcs,
                                                                         d_bad);
     e->launches++;
   }
   // CTA classes sized to the run: (256,512] 128x4, (512,1024] 128x8, (1024,2048] 256x8,
   // (2048,4096) 256x16 slots
   if (!classes_done && r[3] > r[2]) {
-    k_sort_runs_block<128, 4><<<blocks_grid(r[3] - r[2]), 128, 0, st>>>(g.off, RunSet{r[2], r[3], nullptr, nullptr}, endbit,
-                                                                        arcs, d_bad);
+    k_sort_runs_wreg<<<warps_grid(r[3] - r[2]), 256, 0, st>>>(g.off, RunSet{r[2], r[3], nullptr, nullptr},
+                                                               arcs, d_bad);
     e->launches++;
   }
   if (!classes_done && r[4] > r[3]) {
@@ -1026,8 +1110,8 @@ static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64
   const unsigned wg = (unsigned)std::min<int64_t>((ub - ua + 7) / 8, (int64_t)e->sms * 16);
   const unsigned bg = (unsigned)std::min<int64_t>(ub - ua, (int64_t)e->sms * 8);
   k_sort_runs_reg<<<wg, 256, 0, st>>>(g.off, L(0), arcs, d_bad);
-  k_sort_runs_smem<false, 256><<<wg, 256, 0, st>>>(g.off, L(1), arcs, d_bad);
-  k_sort_runs_block<128, 4><<<bg, 128, 0, st>>>(g.off, L(2), endbit, arcs, d_bad);
+  k_sort_runs_wreg<<<wg, 256, 0, st>>>(g.off, L(1), arcs, d_bad);
+  k_sort_runs_wreg<<<wg, 256, 0, st>>>(g.off, L(2), arcs, d_bad);
   k_sort_runs_block<128, 8><<<bg, 128, 0, st>>>(g.off, L(3), endbit, arcs, d_bad);
   k_sort_runs_block<256, 8><<<bg, 256, 0, st>>>(g.off, L(4), endbit, arcs, d_bad);
   k_sort_runs_block<256, 16><<<bg, 256, 0, st>>>(g.off, L(5), endbit, arcs, d_bad);
@@ -1095,43 +1179,6 @@ __device__ __forceinline__ void segmented_runs(uint32_t runs, int lane, int64_t 
     if (sl < d) {
       out[noff[ru] + sl] = x;
       b5 |= sl + 1 < d && nx == x;
-    }
-  }
-}
-
-// Warp-wide bitonic sort of 32 K keys held K per lane, "blocked" (lane l holds
-// positions lK .. lK + K - 1), ascending.  Partner distances j < K are register
-// compare-swaps, j >= K shuffles; the direction bit (i & k) is a compile-time
-// constant for k < K and a function of the lane alone for k >= K.  (The
-// shared-memory network it replaces issued ~2x the instructions: two loads,
-// two stores and the index arithmetic per compare, plus a __syncwarp per stage.)
-template <int K>
-__device__ __forceinline__ void warp_bitonic_sort(int32_t (&x)[K], int lane) {
-  constexpr int P = 32 * K;
-#pragma unroll
-  for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < K) {
-#pragma unroll
-        for (int r = 0; r < K; ++r) {
-          const int p = r ^ j;
-          if (p > r) {
-            const bool up = k < K ? (r & k) == 0 : (lane & (k / K)) == 0;
-            const int32_t lo = min(x[r], x[p]), hi = max(x[r], x[p]);
-            x[r] = up ? lo : hi;
-            x[p] = up ? hi : lo;
-          }
-        }
-      } else {
-        const int lj = j / K;
-        const bool keep_lo = ((lane & lj) == 0) == ((lane & (k / K)) == 0);
-#pragma unroll
-        for (int r = 0; r < K; ++r) {
-          const int32_t y = __shfl_xor_sync(0xffffffffu, x[r], lj);
-          x[r] = keep_lo ? min(x[r], y) : max(x[r], y);
-        }
-      }
     }
   }
 }
