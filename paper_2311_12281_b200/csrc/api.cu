@@ -203,6 +203,8 @@ void gs_engine::free_state() {
   release(s.ctr);
   release(s.wq);
   release(s.coreadj);
+  release(s.clist);
+  release(s.lcnt);
   release(s.thr);
   release(s.rdeg);
   release(s.dxs);

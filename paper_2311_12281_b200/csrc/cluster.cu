@@ -11,7 +11,7 @@
 // exact information classify_vertex_from_neighbors needs (scan.py:794-808).
 #include <algorithm>
 
-#include "engine.cuh"
+#include "simcore.cuh"
 
 namespace gs {
 
@@ -414,11 +414,347 @@ int phase_resolve(gs_engine* e, bool allow_cleanup) {
   return GS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Core-centric cluster phases.  When the cores' adjacency is a small part of
+// the graph (R-MAT s24: <= 500 cores for every eps >= 0.2), union and attach
+// only concern edges incident to a core, so they walk the cores' own lists
+// instead of sweeping every oriented edge and every high endpoint b of the
+// graph (elo / ehi endpoint arrays, neighbour flags, five class launches of
+// the similarity kernels), and classification starts from the clustered
+// vertices.  Decisions are exact and recorded as in the dense passes
+// (sim[e], counters), so the canonical output is identical.
+
+// position of w in the sorted slots [lo, hi) (w present: its index)
+__device__ __forceinline__ int64_t run_find(const int32_t* __restrict__ adj, int64_t lo,
+                                            int64_t hi, int32_t w) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (adj[mid] < w) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// sigma(a, b) >= eps?  a < b in rank (deg a <= deg b), one warp.  The O(1)
+// degree bounds first (such an edge is not counted again: the identify
+// pre-pass counted it), then N(a) from its high end, each lane locating its
+// element in N(b) by binary search in a window that only shrinks (its next
+// element is smaller), with the scan's exact early exits.
+__device__ bool warp_decide(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                            const int2* __restrict__ thr, const Eps2& eps, int32_t a, int32_t b,
+                            int lane, bool& counted, unsigned long long& probes) {
+  const int64_t oa = off[a], da = off[a + 1] - oa, ob = off[b], db = off[b + 1] - ob;
+  const int2 t = thr[db];
+  counted = false;
+  if (da + 1 < t.x) return false;
+  if (da <= t.y) return true;
+  counted = true;
+  const int64_t cmin = c_min_exact(da, db, da - 1, eps);
+  int64_t hi = db;  // this lane's window in N(b): positions [0, hi]
+  int64_t c = 0;
+  for (int64_t s = 0; s < da; s += 32) {
+    const int64_t j = s + lane;
+    bool hit = false;
+    if (j < da) {
+      const int32_t x = adj[oa + da - 1 - j];
+      const int64_t pos = run_find(adj, ob, ob + hi, x) - ob;
+      hit = pos < db && adj[ob + pos] == x;
+      hi = pos;
+    }
+    c += __popc(__ballot_sync(0xffffffffu, hit));
+    const int64_t scanned = min(da, s + 32);
+    probes += (unsigned long long)(scanned - s);
+    if (c >= cmin) return true;
+    if (c + (da - scanned) < cmin) return false;
+  }
+  return c >= cmin;
+}
+
+// the cores as a list, and the sum of their degrees (the sparse paths' work)
+// (deg_sum[0] += degrees, deg_sum[1] = max degree)
+__global__ void k_core_list(int64_t n, const uint8_t* __restrict__ role,
+                            const int64_t* __restrict__ off, int32_t* __restrict__ list,
+                            int* __restrict__ cnt, unsigned long long* __restrict__ deg_sum) {
+  unsigned long long ds = 0, dm = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (role[v] != ROLE_CORE) continue;
+    list[atomicAdd(cnt, 1)] = (int32_t)v;
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    ds += d;
+    dm = d > dm ? d : dm;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, dm, o);
+    dm = x > dm ? x : dm;
+  }
+  if ((threadIdx.x & 31) == 0 && ds) {
+    atomicAdd(deg_sum, ds);
+    atomicMax(deg_sum + 1, dm);
+  }
+}
+
+// union over the core-core edges: warp per core c, the cores w < c of its run
+// (c is their high endpoint: e = eoff[c] + i); known-similar edges union, an
+// unknown one is decided unless both ends already share a root (scan.py:601-660)
+__global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
+                               const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                               const int64_t* __restrict__ eoff, const int2* __restrict__ thr,
+                               Eps2 eps, uint8_t* __restrict__ sim,
+                               const uint8_t* __restrict__ role, int32_t* parent,
+                               unsigned long long* __restrict__ ctr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nc = *ncores;
+  unsigned long long evals = 0, probes = 0, retries = 0;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
+    const int32_t c = clist[k];
+    const int64_t oc = off[c], e0 = eoff[c], nlow = eoff[c + 1] - e0;
+    for (int64_t base = 0; base < nlow; base += 32) {
+      const int64_t i = base + lane;
+      int32_t w = -1;
+      uint8_t st = SIM_DISSIMILAR;
+      if (i < nlow) {
+        w = adj[oc + i];
+        if (role[w] == ROLE_CORE) st = sim[e0 + i];
+      }
+      if (st == SIM_SIMILAR) uf_union(parent, w, c, retries);
+      uint32_t mask = __ballot_sync(0xffffffffu, st == SIM_UNKNOWN);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int32_t ww = __shfl_sync(0xffffffffu, w, src);
+        int same = 0;
+        if (lane == 0) same = uf_find(parent, ww) == uf_find(parent, c);
+        if (__shfl_sync(0xffffffffu, same, 0)) continue;
+        bool counted = false;
+        unsigned long long pr = 0;
+        const bool similar = warp_decide(off, adj, thr, eps, ww, c, lane, counted, pr);
+        if (lane == 0) {
+          sim[e0 + base + src] = similar ? SIM_SIMILAR : SIM_DISSIMILAR;
+          evals += counted;
+          probes += pr;
+          if (similar) uf_union(parent, ww, c, retries);
+        }
+      }
+    }
+  }
+  if (lane == 0 && evals) {
+    atomicAdd(&ctr[CTR_SIM_EVALS], evals);
+    atomicAdd(&ctr[CTR_INTERSECTIONS], evals);
+  }
+  if (lane == 0 && probes) atomicAdd(&ctr[CTR_PROBES], probes);
+  if (retries) atomicAdd(&ctr[CTR_UNION_RETRIES], retries);
+}
+
+// attach over the core / non-core edges: warp per core c, every non-core
+// neighbour w (e = eoff[high] + position of low in high's run); similar ->
+// w's member labels take c's canonical label (scan.py:662-698)
+__global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
+                                const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                                const int64_t* __restrict__ eoff, const int2* __restrict__ thr,
+                                Eps2 eps, uint8_t* __restrict__ sim,
+                                const uint8_t* __restrict__ role, int32_t* __restrict__ lmin,
+                                int32_t* __restrict__ lmax, unsigned long long* __restrict__ ctr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nc = *ncores;
+  unsigned long long evals = 0, probes = 0;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
+    const int32_t c = clist[k];
+    const int32_t L = lmin[c];
+    const int64_t oc = off[c], dc = off[c + 1] - oc, nlow = eoff[c + 1] - eoff[c];
+    for (int64_t base = 0; base < dc; base += 32) {
+      const int64_t i = base + lane;
+      int32_t w = -1;
+      int64_t e = -1;
+      uint8_t st = SIM_DISSIMILAR;
+      if (i < dc) {
+        w = adj[oc + i];
+        if (role[w] != ROLE_CORE) {
+          e = i < nlow ? eoff[c] + i
+                       : eoff[w] + (run_find(adj, off[w], off[w] + (eoff[w + 1] - eoff[w]), c) -
+                                    off[w]);
+          st = sim[e];
+        }
+      }
+      if (st == SIM_SIMILAR) {
+        atomicMin(&lmin[w], L);
+        atomicMax(&lmax[w], L);
+      }
+      uint32_t mask = __ballot_sync(0xffffffffu, st == SIM_UNKNOWN);
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int32_t ww = __shfl_sync(0xffffffffu, w, src);
+        const int64_t ee = __shfl_sync(0xffffffffu, e, src);
+        bool counted = false;
+        unsigned long long pr = 0;
+        const bool similar = ww < c ? warp_decide(off, adj, thr, eps, ww, c, lane, counted, pr)
+                                    : warp_decide(off, adj, thr, eps, c, ww, lane, counted, pr);
+        if (lane == 0) {
+          sim[ee] = similar ? SIM_SIMILAR : SIM_DISSIMILAR;
+          evals += counted;
+          probes += pr;
+          if (similar) {
+            atomicMin(&lmin[ww], L);
+            atomicMax(&lmax[ww], L);
+          }
+        }
+      }
+    }
+  }
+  if (lane == 0 && evals) {
+    atomicAdd(&ctr[CTR_SIM_EVALS], evals);
+    atomicAdd(&ctr[CTR_INTERSECTIONS], evals);
+  }
+  if (lane == 0 && probes) atomicAdd(&ctr[CTR_PROBES], probes);
+}
+
+// classification from the clustered side: the clustered vertices (lmax >= 0)
+// as a list, ...
+__global__ void k_clustered_list(int64_t n, const int32_t* __restrict__ lmax,
+                                 int32_t* __restrict__ list, int* __restrict__ cnt,
+                                 unsigned long long* __restrict__ deg_sum,
+                                 const int64_t* __restrict__ off) {
+  unsigned long long ds = 0, dm = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (lmax[v] < 0) continue;
+    list[atomicAdd(cnt, 1)] = (int32_t)v;
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    ds += d;
+    dm = d > dm ? d : dm;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+    const unsigned long long x = __shfl_xor_sync(0xffffffffu, dm, o);
+    dm = x > dm ? x : dm;
+  }
+  if ((threadIdx.x & 31) == 0 && ds) {
+    atomicAdd(deg_sum, ds);
+    atomicMax(deg_sum + 1, dm);
+  }
+}
+
+// ... whose final roles are set here, and whose unclustered neighbours (the
+// only hub candidates) are listed once each (first setter of their mark byte)
+__global__ void k_near_list(const int* __restrict__ nclu, const int32_t* __restrict__ clu,
+                            const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
+                            const int32_t* __restrict__ lmax, const uint8_t* __restrict__ role,
+                            uint8_t* __restrict__ mark, int32_t* __restrict__ near,
+                            int* __restrict__ nnear, uint8_t* __restrict__ fin) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nc = *nclu;
+  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
+    const int32_t u = clu[k];
+    if (lane == 0) fin[u] = role[u] == ROLE_CORE ? ROLE_CORE : ROLE_MEMBER;
+    for (int64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
+      const int32_t w = adj[i];
+      if (lmax[w] >= 0) continue;
+      const unsigned bit = 1u << (8 * (w & 3));
+      const unsigned old = atomicOr(reinterpret_cast<unsigned*>(mark) + (w >> 2), bit);
+      if (!(old & bit)) near[atomicAdd(nnear, 1)] = w;
+    }
+  }
+}
+
+// hub or outlier for each listed candidate (scan.py:779-829), CTA per vertex
+// (a candidate can be a hub of the whole graph: its list is split 256 ways)
+__global__ void __launch_bounds__(256) k_classify_list(const int* __restrict__ nnear,
+                                                       const int32_t* __restrict__ near,
+                                                       const int64_t* __restrict__ off,
+                                                       const int32_t* __restrict__ adj,
+                                                       const int32_t* __restrict__ lmin,
+                                                       const int32_t* __restrict__ lmax,
+                                                       uint8_t* __restrict__ fin) {
+  __shared__ int s_cnt[8];
+  __shared__ int32_t s_min[8], s_max[8];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t nn = *nnear;
+  for (int64_t k = blockIdx.x; k < nn; k += gridDim.x) {
+    const int32_t v = near[k];
+    int cnt = 0;
+    int32_t umin = 0x7fffffff, umax = -1;
+    for (int64_t i = off[v] + threadIdx.x; i < off[v + 1]; i += blockDim.x) {
+      const int32_t x = adj[i];
+      const int32_t hx = lmax[x];
+      if (hx < 0) continue;
+      ++cnt;
+      const int32_t lx = lmin[x];
+      umin = lx < umin ? lx : umin;
+      umax = hx > umax ? hx : umax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+      umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+    }
+    if (lane == 0) {
+      s_cnt[wid] = cnt;
+      s_min[wid] = umin;
+      s_max[wid] = umax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        cnt += s_cnt[w];
+        umin = min(umin, s_min[w]);
+        umax = max(umax, s_max[w]);
+      }
+      fin[v] = (cnt >= 2 && umin != umax) ? ROLE_HUB : ROLE_OUTLIER;
+    }
+    __syncthreads();
+  }
+}
+
 // unions over this shard's similar core-core edges (Alg. 3 lines 1-18)
+// Sparse (core-centric) union / attach iff the cores' arcs are at most this
+// fraction of all arcs (GS_SPARSE_CLUSTER=0 / 1 forces the dense / sparse path)
+static constexpr int64_t kSparseDiv = 16;
+static constexpr int64_t kSparseMaxDeg = 4096;  // ... and no core / clustered vertex above this degree
+
+static int sparse_mode() {
+  static const int v = getenv("GS_SPARSE_CLUSTER") ? atoi(getenv("GS_SPARSE_CLUSTER")) : -1;
+  return v;
+}
+
 int phase_union(gs_engine* e) {
   if (e->ncores == 0) return GS_OK;  // no core, no cluster
   DevGraph& g = e->g;
   DevState& s = e->s;
+  s.sparse = false;
+  if (e->shard_world == 1 && g.m > 0 && sparse_mode() != 0) {
+    // the cores as a list and their degree sum: the sparse passes' work
+    GS_TRY(e->alloc_n(&s.clist, (int64_t)e->ncores));
+    GS_TRY(e->alloc_n(&s.lcnt, 4));
+    unsigned long long* dsum = nullptr;
+    GS_TRY(e->alloc_n(&dsum, 2));
+    GS_CUDA(cudaMemsetAsync(s.lcnt, 0, 4 * sizeof(int), e->stream));
+    GS_CUDA(cudaMemsetAsync(dsum, 0, 2 * sizeof(unsigned long long), e->stream));
+    k_core_list<<<gridv(e, g.n), 256, 0, e->stream>>>(g.n, s.role, g.off, s.clist, s.lcnt, dsum);
+    unsigned long long h[2] = {0, 0};
+    GS_CUDA(cudaMemcpyAsync(h, dsum, sizeof(h), cudaMemcpyDeviceToHost, e->stream));
+    GS_CUDA(cudaStreamSynchronize(e->stream));
+    e->release(dsum);
+    e->launches++;
+    // a core's edges are decided one by one by its warp: no hub cores
+    s.sparse = sparse_mode() == 1 ||
+               ((int64_t)h[0] <= 2 * g.m / kSparseDiv && (int64_t)h[1] <= kSparseMaxDeg);
+  }
+  if (s.sparse) {
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)(e->ncores + 7) / 8, (int64_t)e->sms * 16);
+    k_union_sparse<<<grid, 256, 0, e->stream>>>(s.lcnt, s.clist, g.off, g.adj, g.eoff, s.thr, e->eps,
+                                               s.sim, s.role, s.parent, s.ctr);
+    e->launches++;
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+  }
   if (g.m > 0) {
     GS_TRY(ensure_endpoints(e));
     k_union_known<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.parent,
@@ -529,7 +865,15 @@ int phase_attach(gs_engine* e) {
   if (e->ncores == 0) return GS_OK;
   DevGraph& g = e->g;
   DevState& s = e->s;
-  if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, g.n));
+  if (s.sparse) {
+    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)(e->ncores + 7) / 8, (int64_t)e->sms * 16);
+    k_attach_sparse<<<grid, 256, 0, e->stream>>>(s.lcnt, s.clist, g.off, g.adj, g.eoff, s.thr,
+                                                e->eps, s.sim, s.role, s.lmin, s.lmax, s.ctr);
+    e->launches++;
+    GS_CUDA(cudaGetLastError());
+    return GS_OK;
+  }
+  if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, (g.n + 3) & ~int64_t(3)));
   GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)(g.n > 0 ? g.n : 1), e->stream));
   if (g.n > 0) flag_neighbours<true>(e, s.coreadj);
   GS_TRY(run_similarity(e, MODE_ATTACH, e->eps, e->mu));
@@ -577,11 +921,51 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     if (cluster_out) GS_TRY(e->alloc_n(&d_cluster_out, n));
   }
   const int64_t rsplit = e->ncores > 0 ? g.rclass[1] : 0;
+  // From the clustered side when its arcs are few: the clustered vertices are
+  // listed (their roles set), their unclustered neighbours listed once each
+  // and only those scanned for a hub; everyone else is an outlier.
+  bool listed = false;
+  if (e->ncores > 0 && n > 0 && sparse_mode() != 0) {
+    int32_t* clu = nullptr;
+    unsigned long long* dsum = nullptr;
+    int* cnt = nullptr;
+    GS_TRY(e->alloc_n(&clu, n));
+    GS_TRY(e->alloc_n(&dsum, 2));
+    GS_TRY(e->alloc_n(&cnt, 2));
+    GS_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), str));
+    GS_CUDA(cudaMemsetAsync(dsum, 0, 2 * sizeof(unsigned long long), str));
+    k_clustered_list<<<gridv(e, n), 256, 0, str>>>(n, s.lmax, clu, cnt, dsum, g.off);
+    unsigned long long h[2] = {0, 0};
+    GS_CUDA(cudaMemcpyAsync(h, dsum, sizeof(h), cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaStreamSynchronize(str));
+    e->launches++;
+    listed = sparse_mode() == 1 ||
+             ((int64_t)h[0] <= 2 * m / kSparseDiv && (int64_t)h[1] <= kSparseMaxDeg);
+    if (listed) {
+      int32_t* nearl = nullptr;
+      GS_TRY(e->alloc_n(&nearl, n));
+      if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, (n + 3) & ~int64_t(3)));
+      GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)((n + 3) & ~int64_t(3)), str));
+      GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
+      const unsigned gw = (unsigned)std::min<int64_t>(grid_for((int64_t)n * 32, 256), (int64_t)e->sms * 16);
+      k_near_list<<<gw, 256, 0, str>>>(cnt, clu, g.off, g.adj, s.lmax, s.role, s.coreadj, nearl,
+                                       cnt + 1, fin);
+      k_classify_list<<<(unsigned)e->sms * 8, 256, 0, str>>>(cnt + 1, nearl, g.off, g.adj, s.lmin,
+                                                             s.lmax, fin);
+      e->launches += 2;
+      GS_CUDA(cudaGetLastError());
+      GS_CUDA(cudaStreamSynchronize(str));  // the lists are released below
+      e->release(nearl);
+    }
+    e->release(clu);
+    e->release(dsum);
+    e->release(cnt);
+  }
   // near[v]: v has a clustered neighbour (only those can be hubs).  Flagging
   // costs the clustered vertices' degrees, the hub scan it saves the rest's:
   // flag only when the clustered side is the smaller one.
   bool use_near = false;
-  if (e->ncores > 0 && n > 0) {
+  if (!listed && e->ncores > 0 && n > 0) {
     unsigned long long* d_sum = nullptr;
     GS_TRY(e->alloc_n(&d_sum, 1));
     GS_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(unsigned long long), str));
@@ -593,7 +977,7 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     e->launches++;
     use_near = (int64_t)h_sum < g.m;  // < half of the 2m arcs
     if (use_near) {
-      if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, n));
+      if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, (n + 3) & ~int64_t(3)));
       GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)n, str));
       flag_neighbours<false>(e, s.coreadj);
     }
@@ -601,12 +985,12 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
   const uint8_t* near = use_near ? s.coreadj : nullptr;
   if (e->ncores == 0 && n > 0)  // nothing is clustered: every vertex is an outlier
     GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
-  if (rsplit > 0) {
+  if (rsplit > 0 && !listed) {
     k_classify_thread<<<gridv(e, rsplit), 256, 0, str>>>(0, rsplit, g.off, g.adj, s.role, s.lmin,
                                                         s.lmax, near, fin);
     e->launches++;
   }
-  if (e->ncores > 0 && n > rsplit) {
+  if (e->ncores > 0 && n > rsplit && !listed) {
     k_classify_warp<<<gridv(e, (n - rsplit) * 32), 256, 0, str>>>(rsplit, n, g.off, g.adj, s.role,
                                                                  s.lmin, s.lmax, near, fin);
     e->launches++;

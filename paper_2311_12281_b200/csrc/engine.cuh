@@ -79,6 +79,9 @@ struct DevState {
   int32_t* nlo = nullptr;       // [n] hub split of each adjacency run
   int32_t* wq = nullptr;        // work-queue heads for persistent kernels
   uint8_t* coreadj = nullptr;   // [n] has a core neighbour (set before attach)
+  int32_t* clist = nullptr;     // [ncores] the cores (core-centric cluster phases)
+  int* lcnt = nullptr;          // [4] list sizes (cores, clustered, near) + spare
+  bool sparse = false;          // this scan's union / attach run core-centric
 };
 
 enum Ctr {
