@@ -208,7 +208,6 @@ void gs_engine::free_state() {
   release(s.thr);
   release(s.rdeg);
   release(s.dxs);
-  release(s.nlo);
   s = DevState();
 }
 

@@ -76,7 +76,6 @@ struct DevState {
   int2* thr = nullptr;          // [dmax+1] per-degree O(1) thresholds for this epsilon
   int32_t* rdeg = nullptr;      // [dmax+3] first rank with degree >= d (degrees ascend with rank)
   int2* dxs = nullptr;          // [dmax+1] per low degree d: {dx, ds} (see sim.cu)
-  int32_t* nlo = nullptr;       // [n] hub split of each adjacency run
   int32_t* wq = nullptr;        // work-queue heads for persistent kernels
   uint8_t* coreadj = nullptr;   // [n] has a core neighbour (set before attach)
   int32_t* clist = nullptr;     // [ncores] the cores (core-centric cluster phases)
@@ -139,7 +138,6 @@ struct SimParams {
   const int2* thr;      // per degree d of b: {xmin, simmax} O(1) bounds (see sim.cu)
   const int32_t* rdeg;  // [dmax+3] first rank with degree >= d
   int64_t dmax;
-  const int32_t* nlo;   // per vertex: neighbours below hub_lo (the non-hub prefix)
   uint32_t hub_lo;      // first rank of the hub bitmap range
   uint32_t bm_words;    // hub bitmap words (range [hub_lo, n))
   const uint32_t* sk;   // neighbourhood sketches (nullptr: none), see DevGraph

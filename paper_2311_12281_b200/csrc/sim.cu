@@ -74,6 +74,23 @@ __device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const 
   return lo;
 }
 
+// first index of the sorted run a[0, n) holding a value >= key, by a whole CTA
+// (the same two-round sampled search)
+template <int NT>
+__device__ __forceinline__ int64_t cta_lower_bound(const int32_t* a, int64_t n, uint32_t key) {
+  int64_t lo = 0, hi = n;
+  while (hi > lo) {
+    const int64_t step = (hi - lo + NT - 1) / NT;
+    const int64_t idx = lo + (int64_t)threadIdx.x * step;
+    const int cnt = __syncthreads_count(idx < hi && (uint32_t)a[idx] < key);
+    const int64_t nlo = cnt == 0 ? lo : lo + (int64_t)(cnt - 1) * step + 1;
+    const int64_t nhi = min(hi, lo + (int64_t)cnt * step);
+    lo = nlo;
+    hi = nhi;
+  }
+  return lo;
+}
+
 // ... and by one warp
 __device__ __forceinline__ int64_t survivor_start_warp(const SimParams& P, const int32_t* nb,
                                                        int64_t nlow, int2 th, int64_t dmax,
@@ -351,27 +368,6 @@ __global__ void k_degrees(const int64_t* __restrict__ off, int64_t n, uint32_t* 
     deg[v] = (uint32_t)(off[v + 1] - off[v]);
 }
 
-// per-vertex split of the adjacency run at hub_lo (runs are sorted)
-__global__ void k_hubsplit(const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
-                           int64_t n, uint32_t hub_lo, int32_t* __restrict__ nlo,
-                           unsigned long long* __restrict__ ctr) {
-  unsigned long long bytes = 0;
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t l = off[v], h = off[v + 1];
-    const int64_t lo0 = l;
-    bytes += 16 + 4 + 4ull * (64 - __clzll((unsigned long long)(h - l)));
-    while (l < h) {
-      const int64_t mid = (l + h) >> 1;
-      if ((uint32_t)adj[mid] < hub_lo) l = mid + 1; else h = mid;
-    }
-    nlo[v] = (int32_t)(l - lo0);
-  }
-  if (ctr == nullptr) return;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
-  if ((threadIdx.x & 31) == 0 && bytes) atomicAdd(&ctr[CTR_B_PREP], bytes);
-}
 
 // Claim the next b with a pending edge and start the bulk copy of N(b) into
 // `buf` (16-byte aligned source: the list starts *pre words in).  Not inlined:
@@ -576,12 +572,13 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           ns_scan = s_nkeep;
         }
         if (ns_scan > 0 && !built) {  // stage N(b) once per b: hub suffix -> bitmap, rest -> cuckoo
+          // hub split of N(b), found by the CTA (no per-vertex table to build)
+          const int64_t nlo = cta_lower_bound<NT>(nbl, db, hub_lo);
           if (tid == 0) {
-            s_nlo = P.nlo[b];
+            s_nlo = nlo;
             s_nstash = 0;
           }
           __syncthreads();
-          const int64_t nlo = s_nlo;
           uint32_t T = (uint32_t)((nlo * 5) / 12 + 1);  // <= 0.6 keys per slot
           if (T > tcap) T = tcap;
           C.T = T;
@@ -599,7 +596,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           }
           __syncthreads();
           built = true;
-          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull + 4ull * (unsigned long long)db);  // nlo[b], N(b)
+          if (tid == 0) ctr_add(lc, LC_BYTES, 4ull * (unsigned long long)db);  // N(b)
         }
         const int nstash = s_nstash;
         const int64_t nlo = s_nlo;
@@ -1093,7 +1090,6 @@ int prepare_similarity(gs_engine* e, const Eps2& eps) {
   DevGraph& g = e->g;
   DevState& s = e->s;
   GS_TRY(e->alloc_n(&s.thr, g.dmax + 1));
-  GS_TRY(e->alloc_n(&s.nlo, g.n));
   k_thresholds<<<grid_for(g.dmax + 1, 256), 256, 0, e->stream>>>(g.dmax, eps, s.thr);
   GS_TRY(e->alloc_n(&s.rdeg, g.dmax + 3));
   GS_TRY(e->alloc_n(&s.dxs, g.dmax + 1));
@@ -1109,13 +1105,6 @@ int prepare_similarity(gs_engine* e, const Eps2& eps) {
     }
     if (const char* v = getenv("GS_SKETCH_DMIN")) dmin = std::max(1, atoi(v));
     GS_TRY(build_sketch(e, lk, dmin));
-  }
-  const int64_t bits = std::min<int64_t>(kHubBits, ((g.n + 31) / 32) * 32);
-  const uint32_t hub_lo = (uint32_t)std::max<int64_t>(0, g.n - bits);
-  if (g.n > 0) {
-    k_hubsplit<<<grid_for(g.n, 256), 256, 0, e->stream>>>(g.off, g.adj, g.n, hub_lo, s.nlo,
-                                                          s.ctr);
-    e->launches += 2;
   }
   GS_CUDA(cudaGetLastError());
   return GS_OK;
@@ -1144,7 +1133,6 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.thr = s.thr;
   P.rdeg = s.rdeg;
   P.dmax = g.dmax;
-  P.nlo = s.nlo;
   P.sk = g.sk;
   P.skbase = g.skbase;
   P.sk_lk = g.sk_lk;
