@@ -876,7 +876,7 @@ __global__ void k_p1_owner(int64_t nb, const int32_t* __restrict__ nit,
   }
 }
 
-template <int NT, int MINB, int UNROLL>
+template <int NT, int MINB, int UNROLL, bool NA = true, bool NAB = false>
 __global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo,
                                                   const int32_t* __restrict__ j0s,
                                                   const int32_t* __restrict__ ioff,
@@ -943,8 +943,8 @@ __global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo
           if (skb && sk_try(P, da, db, cmin)) {
             const int64_t wa = sk_words(da, P.sk_lk);
             unsigned long long words = 0;
-            dis = sk_rejects256<UNROLL>(sk_row(P, a, da, wa), levb + 2 * (wb - wa), wa, da, cmin,
-                                        words);
+            dis = sk_rejects256<UNROLL, NA, NAB>(sk_row(P, a, da, wa), levb + 2 * (wb - wa), wa,
+                                                 da, cmin, words);
             by += 4ull * words;  // S_a's words read (b's level: per b, above)
           }
           if (dis) {  // record_edge(dissimilar), the role decision deferred
@@ -1192,8 +1192,10 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     e->release(tmp);
     k_p1_owner<<<gi, 256, 0, e->stream>>>(nb, p1_nit, p1_ioff, p1_owner, p1_ioff + nb);
     static const int p1v = getenv("GS_P1_VARIANT") ? atoi(getenv("GS_P1_VARIANT")) : 0;
-    auto kern = p1v == 1 ? k_sk_filter<256, 4, 2> : p1v == 2 ? k_sk_filter<256, 5, 1>
-              : p1v == 3 ? k_sk_filter<256, 6, 1> : k_sk_filter<256, 4, 1>;
+    // 0: S_a read without L1 allocation (best), 1: with, 2: S_a and b's level
+    // without, 3: two 32-byte steps per check
+    auto kern = p1v == 1 ? k_sk_filter<256, 4, 1, false> : p1v == 2 ? k_sk_filter<256, 4, 1, true, true>
+              : p1v == 3 ? k_sk_filter<256, 4, 2> : k_sk_filter<256, 4, 1>;
     int occ = 0;
     GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
     kern<<<(unsigned)(std::max(occ, 1) * e->sms), 256, 0, e->stream>>>(P, lo, p1_j0, p1_ioff,

@@ -594,13 +594,21 @@ __device__ __forceinline__ void ldg256(const uint32_t* p, uint32_t (&r)[8]) {
       : "l"(p));
 }
 
+// ... without allocating in L1 (a row of S_a is read once per edge; 7% L1 hits)
+__device__ __forceinline__ void ldg256_na(const uint32_t* p, uint32_t (&r)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "l"(p));
+}
+
 // Thread-per-edge sketch bound with 32-byte loads: the row walk of
 // sk_thread_rejects, but every load fetches one whole sector, so an L1
 // wavefront carries 32 useful bytes instead of 16 (a warp's lanes walk 32
 // different rows: with 16-byte loads the L1 was the limiter, 86% busy).  A (S_a)
 // and B (b's level at a's resolution) are global, 32-byte aligned (sketch
 // slots are multiples of 8 words; wa >= 4).  `words` += the words of A read.
-template <int UNROLL>
+template <int UNROLL, bool NA = false, bool NAB = false>
 __device__ __forceinline__ bool sk_rejects256(const uint32_t* __restrict__ A,
                                               const uint32_t* __restrict__ B, int64_t wa,
                                               int64_t da, int32_t cmin,
@@ -619,8 +627,8 @@ __device__ __forceinline__ bool sk_rejects256(const uint32_t* __restrict__ A,
 #pragma unroll
     for (int t = 0; t < UNROLL; ++t) {
       if (j + t < q) {
-        ldg256(A + 8 * (j + t), x[t]);
-        ldg256(B + 8 * (j + t), y[t]);
+        if (NA) ldg256_na(A + 8 * (j + t), x[t]); else ldg256(A + 8 * (j + t), x[t]);
+        if (NAB) ldg256_na(B + 8 * (j + t), y[t]); else ldg256(B + 8 * (j + t), y[t]);
       } else {
 #pragma unroll
         for (int k = 0; k < 8; ++k) x[t][k] = y[t][k] = 0u;
