@@ -343,11 +343,25 @@ __device__ __forceinline__ bool member(const uint32_t* bm, uint32_t hub_lo, cons
 // sentinel >= n that lands on an always-zero bitmap guard word.
 static constexpr uint32_t kPast = 0x7fffffffu;  // scan sentinel, >= n
 
+// an element of N(a) for the scan: read once per edge, so not allocated in L1
+#ifndef GS_SCAN_NA
+#define GS_SCAN_NA 1
+#endif
+__device__ __forceinline__ uint32_t ld_scan(const int32_t* p) {
+#if GS_SCAN_NA
+  uint32_t r;
+  asm("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+#else
+  return (uint32_t)__ldg(p);
+#endif
+}
+
 // The first step's element of this lane (the top 32 of N(a)); issued early so
 // the load of survivor s+1 overlaps the scan of survivor s.
 __device__ __forceinline__ uint32_t first_element(const int32_t* __restrict__ a_run, int32_t da,
                                                   int lane) {
-  return lane < da ? (uint32_t)__ldg(a_run + (da - 1 - lane)) : kPast;
+  return lane < da ? ld_scan(a_run + (da - 1 - lane)) : kPast;
 }
 
 template <bool GTAB>
@@ -374,7 +388,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
     const int32_t rem = da - lane;
 #pragma unroll
     for (int u = 1; u < 4; ++u)
-      if (u < cu && 32 * u < rem) cur[u] = (uint32_t)__ldg(top - 32 * u);
+      if (u < cu && 32 * u < rem) cur[u] = ld_scan(top - 32 * u);
   }
   int32_t c = 0;
   scanned = 0;
@@ -390,7 +404,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
       const int32_t rem = da - nbase - lane;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        nxt[u] = (u < nu && 32 * u < rem) ? (uint32_t)__ldg(q - 32 * u) : kPast;
+        nxt[u] = (u < nu && 32 * u < rem) ? ld_scan(q - 32 * u) : kPast;
     }
     const uint32_t lo4 = min(min(cur[0], cur[1]), min(cur[2], cur[3]));
     uint32_t hits = 0;
@@ -419,7 +433,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
       const int32_t rem = da - scanned - lane;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        cur[u] = (u < cu && 32 * u < rem) ? (uint32_t)__ldg(q - 32 * u) : kPast;
+        cur[u] = (u < cu && 32 * u < rem) ? ld_scan(q - 32 * u) : kPast;
     }
   }
 }
