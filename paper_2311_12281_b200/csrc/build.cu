@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(256, MINB) k_fused_warp(const int64_t* __restr
 
 // CTA per run of a rank range whose degrees lie in [kHeavyScatter, NT * ITEMS]:
 // block radix sort over the rank bits
-template <int NT, int ITEMS>
+template <int NT, int ITEMS, int RB = 4>
 __global__ void __launch_bounds__(NT) k_fused_block(const int64_t* __restrict__ off, int64_t n,
                                                     int64_t rlo, int64_t rhi,
                                                     const int32_t* __restrict__ orig,
@@ -1305,7 +1305,7 @@ __global__ void __launch_bounds__(NT) k_fused_block(const int64_t* __restrict__ 
                                                     const int64_t* __restrict__ noff, int endbit,
                                                     int32_t* __restrict__ out,
                                                     int* __restrict__ bad) {
-  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS, cub::NullType, RB>;
   __shared__ typename Sort::TempStorage tmp;
   const int t = threadIdx.x;
   bool b3 = false, b4 = false, b5 = false;
@@ -1342,7 +1342,7 @@ __global__ void __launch_bounds__(NT) k_fused_block(const int64_t* __restrict__ 
 // ... for runs of up to 16384 neighbours: one 1024-thread CTA per run, the
 // block radix sort's scratch in dynamic shared memory (beyond the 48 KB static
 // limit); replaces scatter + segmented radix sort for these hub runs
-template <int NT, int ITEMS>
+template <int NT, int ITEMS, int RB = 4>
 __global__ void __launch_bounds__(NT, 1) k_fused_block_dyn(const int64_t* __restrict__ off,
                                                            int64_t n, int64_t rlo, int64_t rhi,
                                                            const int32_t* __restrict__ orig,
@@ -1351,7 +1351,7 @@ __global__ void __launch_bounds__(NT, 1) k_fused_block_dyn(const int64_t* __rest
                                                            const int64_t* __restrict__ noff,
                                                            int endbit, int32_t* __restrict__ out,
                                                            int* __restrict__ bad) {
-  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS>;
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS, cub::NullType, RB>;
   extern __shared__ __align__(16) unsigned char dsm[];
   typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(dsm);
   const int t = threadIdx.x;
@@ -1444,15 +1444,22 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   if (h1025 > h512)
     k_fused_block<128, 8><<<blocks(h1025 - h512), 128, 0, st>>>(
         off, n, h512, h1025, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+  // radix bits per pass of the CTA sorts (25-bit keys at s24: 5 passes of 5 bits
+  // beat 7 of 4 -- 12.07 -> 11.57 ms -- and 5 of 6)
+  static const int rb = getenv("GS_SORT_RB") ? atoi(getenv("GS_SORT_RB")) : 5;
+  static const int rbd = getenv("GS_SORT_RBD") ? atoi(getenv("GS_SORT_RBD")) : 5;
+  auto kb8 = rb == 4 ? k_fused_block<256, 8, 4> : k_fused_block<256, 8, 5>;
+  auto kb16 = rb == 4 ? k_fused_block<256, 16, 4> : k_fused_block<256, 16, 5>;
   if (h2049 > h1025)
-    k_fused_block<256, 8><<<blocks(h2049 - h1025), 256, 0, st>>>(
+    kb8<<<blocks(h2049 - h1025), 256, 0, st>>>(
         off, n, h1025, h2049, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
   if (h4096 > h2049)
-    k_fused_block<256, 16><<<blocks(h4096 - h2049), 256, 0, st>>>(
+    kb16<<<blocks(h4096 - h2049), 256, 0, st>>>(
         off, n, h2049, h4096, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
   if (h16k > h4096) {
-    auto kb = k_fused_block_dyn<1024, 16>;
-    const int sm = (int)sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16>::TempStorage);
+    auto kb = rbd == 5 ? k_fused_block_dyn<1024, 16, 5> : k_fused_block_dyn<1024, 16, 4>;
+    const int sm = (int)std::max({sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 4>::TempStorage),
+                                  sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 5>::TempStorage)});
     GS_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     kb<<<(unsigned)std::min<int64_t>(h16k - h4096, (int64_t)e->sms), 1024, sm, st>>>(
         off, n, h4096, h16k, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
