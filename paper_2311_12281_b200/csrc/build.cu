@@ -1244,10 +1244,12 @@ __global__ void __launch_bounds__(256, MINB) k_fused_warp(const int64_t* __restr
     }
     // the group's runs are then read one after another: pull their first
     // 512 bytes into L2 now, so each run's reads wait for L2, not DRAM
-    if (myd > 0 && myd < kHeavyScatter)
+    if (myd > 0 && myd <= 256)
       for (int t = 0; t < myd && t < 128; t += 32)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(adj + myo + t));
-    uint32_t rest = __ballot_sync(0xffffffffu, myd > 16 && myd < kHeavyScatter);
+    // 257..511: k_fused_warp16 (its 16 keys per lane would set this kernel's
+    // register budget; at 32 registers it runs 64 warps per SM)
+    uint32_t rest = __ballot_sync(0xffffffffu, myd > 16 && myd <= 256);
     // runs of <= 8: four per round (8 lanes each), of 9..16: two per round
     segmented_runs<8>(__ballot_sync(0xffffffffu, myd > 0 && myd <= 8), lane, g0, myo, myd, myr,
                       adj, rank, noff, out, n, b3, b4, b5);
@@ -1282,12 +1284,38 @@ __global__ void __launch_bounds__(256, MINB) k_fused_warp(const int64_t* __restr
       fused_run_regs<2>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
     } else if (d <= 128) {
       fused_run_regs<4>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
-    } else if (d <= 256) {
-      fused_run_regs<8>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
     } else {
-      fused_run_regs<16>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
+      fused_run_regs<8>(adj, rank, ou, d, n, u, o, sbuf, lane, b3, b4, b5);
     }
     }
+  }
+  if (b3) atomicExch(bad, 3);
+  if (b4) atomicExch(bad, 4);
+  if (b5) atomicExch(bad, 5);
+}
+
+// runs of 257..511 neighbours (the rank range [rlo, rhi)): warp per run, 16 keys
+// per lane in registers (fused_run_regs<16>)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fused_warp16(const int64_t* __restrict__ off,
+                                                            int64_t n, int64_t rlo, int64_t rhi,
+                                                            const int32_t* __restrict__ orig,
+                                                            const int32_t* __restrict__ adj,
+                                                            const int32_t* __restrict__ rank,
+                                                            const int64_t* __restrict__ noff,
+                                                            int32_t* __restrict__ out,
+                                                            int* __restrict__ bad) {
+  __shared__ int32_t buf[8 * 32 * 17];
+  const int lane = threadIdx.x & 31;
+  int32_t* sbuf = buf + (threadIdx.x >> 5) * (32 * 17);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  bool b3 = false, b4 = false, b5 = false;
+  for (int64_t r = rlo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5); r < rhi;
+       r += nw) {
+    const int64_t u = orig[r];
+    const int64_t ou = off[u];
+    const int d = (int)(off[u + 1] - ou);
+    fused_run_regs<16>(adj, rank, ou, d, n, u, out + noff[r], sbuf, lane, b3, b4, b5);
   }
   if (b3) atomicExch(bad, 3);
   if (b4) atomicExch(bad, 4);
@@ -1388,9 +1416,9 @@ __global__ void __launch_bounds__(NT, 1) k_fused_block_dyn(const int64_t* __rest
 
 __global__ void k_fused_classes(const int64_t* __restrict__ off, int64_t n,
                                 int64_t* __restrict__ out) {
-  const int64_t th[5] = {1025, 2049, 4096, 16385, 0};
+  const int64_t th[5] = {1025, 2049, 4096, 16385, 257};
   const int c = threadIdx.x;
-  if (c < 4) out[c] = rank_of_degree(off, n, th[c]);
+  if (c < 5) out[c] = rank_of_degree(off, n, th[c]);
 }
 
 // the device-CSR build's relabel + per-run sorts, fused.  Runs of > 16384
@@ -1403,10 +1431,10 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   DevGraph& g = e->g;
   cudaStream_t st = e->stream, cs = e->cstream;
   int64_t* d_cls = nullptr;
-  GS_TRY(e->alloc_n(&d_cls, 4));
+  GS_TRY(e->alloc_n(&d_cls, 5));
   k_fused_classes<<<1, 32, 0, st>>>(g.off, n, d_cls);
-  int64_t r[4];
-  GS_CUDA(cudaMemcpyAsync(r, d_cls, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int64_t r[5];
+  GS_CUDA(cudaMemcpyAsync(r, d_cls, 5 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaStreamSynchronize(st));
   e->release(d_cls);
   e->launches++;
@@ -1415,7 +1443,7 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   // rank ranges by degree (ranks ascend with the degree): [512, 1024], [1025, 2048],
   // [2049, 4095], [4096, 16384], > 16384 (r512 = first rank of degree >= 512, h_cls[2])
   const int64_t h512 = clip(r512), h1025 = clip(r[0]), h2049 = clip(r[1]), h4096 = clip(r[2]),
-                h16k = clip(r[3]);
+                h16k = clip(r[3]), h257 = clip(r[4]);
   static const bool two_streams = !(getenv("GS_BUILD_STREAMS") && atoi(getenv("GS_BUILD_STREAMS")) == 1);
   // the longest runs first, on the copy stream: scatter, then the segmented sort
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1433,11 +1461,18 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
                                    g.off, arcs, d_bad);
     e->launches++;
   }
-  static const int fminb = getenv("GS_FUSED_MINB") ? atoi(getenv("GS_FUSED_MINB")) : 6;
-  auto fk = fminb >= 6 ? k_fused_warp<6> : fminb == 5 ? k_fused_warp<5> : k_fused_warp<4>;
+  static const int fminb = getenv("GS_FUSED_MINB") ? atoi(getenv("GS_FUSED_MINB")) : 8;
+  auto fk = fminb >= 8 ? k_fused_warp<8> : fminb == 7 ? k_fused_warp<7> : fminb == 6 ? k_fused_warp<6> : fminb == 5 ? k_fused_warp<5> : k_fused_warp<4>;
   fk<<<(unsigned)std::min<int64_t>(grid_for(n * 32, 256), (int64_t)e->sms * 64), 256,
                  0, st>>>(off, n, adj, g.rank, g.off, arcs, d_bad, row_lo, row_hi);
   e->launches++;
+  if (h512 > h257) {
+    static const int f16 = getenv("GS_FUSED16_MINB") ? atoi(getenv("GS_FUSED16_MINB")) : 4;
+    auto fk16 = f16 >= 6 ? k_fused_warp16<6> : f16 == 5 ? k_fused_warp16<5> : k_fused_warp16<4>;
+    fk16<<<(unsigned)std::min<int64_t>(grid_for((h512 - h257) * 32, 256), (int64_t)e->sms * 32),
+           256, 0, st>>>(off, n, h257, h512, g.orig, adj, g.rank, g.off, arcs, d_bad);
+    e->launches++;
+  }
   auto blocks = [&](int64_t runs) {
     return (unsigned)std::min<int64_t>(std::max<int64_t>(runs, 1), (int64_t)e->sms * 16);
   };
