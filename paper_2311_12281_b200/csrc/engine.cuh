@@ -154,6 +154,10 @@ struct SimParams {
   const int32_t* p1_pend = nullptr;
   const int32_t* p1_j0 = nullptr;  // survivor start of b's owned prefix
   int64_t p1_lo = 0;
+  // ... and the b's with a pending edge, ascending (p1_list), this launch's slice
+  // [p1_rng[0], p1_rng[1]) of it: the stage-2 launches visit only those
+  const int32_t* p1_list = nullptr;
+  const int* p1_rng = nullptr;
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;

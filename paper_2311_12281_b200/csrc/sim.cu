@@ -74,6 +74,17 @@ __device__ __forceinline__ int64_t survivor_start_cta(const SimParams& P, const 
   return lo;
 }
 
+// The item-th high endpoint of a launch (largest first): from the stage-1 list
+// of b's with a pending edge when the launch has one, else this shard's range.
+__device__ __forceinline__ int64_t stage_b(const SimParams& P, int64_t rlo, int64_t rhi,
+                                           int64_t item) {
+  if (P.p1_list) {
+    const int lo = P.p1_rng[0], hi = P.p1_rng[1];
+    return item < hi - lo ? (int64_t)P.p1_list[hi - 1 - item] : rlo - 1;
+  }
+  return shard_top(rlo, rhi, item, P.shard_rank, P.shard_world);
+}
+
 // first index of the sorted run a[0, n) holding a value >= key, by a whole CTA
 // (the same two-round sampled search)
 template <int NT>
@@ -456,7 +467,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
       s_item = atomicAdd(&P.wq[qi], 1);
     }
     __syncthreads();
-    const int64_t b = shard_top(rlo, rhi, s_item, P.shard_rank, P.shard_world);
+    const int64_t b = stage_b(P, rlo, rhi, s_item);
     if (b < rlo) break;
     if ((P.mode >= MODE_UNION && !b_needed(P, b)) || (p1 && P.p1_pend[b - P.p1_lo] == 0)) {
       __syncthreads();  // s_item read by all before the next claim
@@ -695,7 +706,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
     int item = 0;
     if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
     item = __shfl_sync(0xffffffffu, item, 0);
-    const int64_t b = shard_top(rlo, rhi, item, P.shard_rank, P.shard_world);
+    const int64_t b = stage_b(P, rlo, rhi, item);
     if (b < rlo) break;
     if (P.mode >= MODE_UNION && !b_needed(P, b)) continue;
     if (p1 && P.p1_pend[b - P.p1_lo] == 0) continue;
@@ -875,6 +886,30 @@ __global__ void k_p1_owner(int64_t nb, const int32_t* __restrict__ nit,
     if (i == nb - 1) *total = o + k;
   }
 }
+
+// the stage-2 classes' slices of the list of b's with a pending edge:
+// cls[k] = first list index with b >= bound[k] (k < 4), cls[4] = list size
+__global__ void k_p1_bounds(const int32_t* __restrict__ list, const int* __restrict__ nsel,
+                            int64_t b1, int64_t b2, int64_t b3, int64_t b4, int* __restrict__ cls) {
+  const int t = threadIdx.x;
+  const int64_t key = t == 0 ? b1 : t == 1 ? b2 : t == 2 ? b3 : b4;
+  const int cnt = *nsel;
+  if (t < 4) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)list[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    cls[t] = lo;
+  }
+  if (t == 4) cls[4] = cnt;
+}
+
+struct HasPending {
+  const int32_t* pend;
+  int64_t lo;
+  __device__ bool operator()(int32_t b) const { return pend[b - lo] > 0; }
+};
 
 template <int NT, int MINB, int UNROLL, bool NA = true, bool NAB = false>
 __global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo,
@@ -1172,7 +1207,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   // (GS_P1=0: the class kernels run the sketch bound themselves, as before)
   static const bool p1_on = !(getenv("GS_P1") && atoi(getenv("GS_P1")) == 0);
   int32_t *p1_j0 = nullptr, *p1_nit = nullptr, *p1_ioff = nullptr, *p1_owner = nullptr,
-          *p1_pend = nullptr;
+          *p1_pend = nullptr, *p1_list = nullptr;
+  int* p1_cls = nullptr;
   if (ident && p1_on && g.sk != nullptr && g.n > rc[1]) {
     const int64_t lo = rc[1], nb = g.n - lo;
     GS_TRY(e->alloc_n(&p1_j0, nb));
@@ -1206,6 +1242,26 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     P.p1_pend = p1_pend;
     P.p1_j0 = p1_j0;
     P.p1_lo = lo;
+    // the b's with a pending edge, ascending, and each class's slice of them
+    // (GS_P1_LIST=0: the stage-2 launches claim every b of their class)
+    // (the TMA prefetch variant claims from the class range itself)
+    static const bool use_list = !(getenv("GS_P1_LIST") && atoi(getenv("GS_P1_LIST")) == 0) &&
+                                 !(getenv("GS_TMA") && atoi(getenv("GS_TMA")) == 1);
+    if (use_list) {
+      GS_TRY(e->alloc_n(&p1_list, nb));
+      GS_TRY(e->alloc_n(&p1_cls, 8));
+      size_t tb2 = 0;
+      cub::CountingInputIterator<int32_t> it((int32_t)lo);
+      const HasPending pred{p1_pend, lo};
+      GS_CUDA(cub::DeviceSelect::If(nullptr, tb2, it, p1_list, p1_cls + 5, (int)nb, pred, e->stream));
+      void* t2 = nullptr;
+      GS_TRY(e->alloc(&t2, tb2 > 0 ? tb2 : 1));
+      GS_CUDA(cub::DeviceSelect::If(t2, tb2, it, p1_list, p1_cls + 5, (int)nb, pred, e->stream));
+      e->release(t2);
+      k_p1_bounds<<<1, 32, 0, e->stream>>>(p1_list, p1_cls + 5, rc[1], rc[2], rc[3], rc[4], p1_cls);
+      e->launches += 2;
+      P.p1_list = p1_list;
+    }
   }
   if (ident) e->kev_mark(3);
   // huge b first (longest work items), with an L2-resident table per CTA
@@ -1216,6 +1272,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     GS_TRY(e->alloc_n(&P.gtab, 4 * tcap_g * nblk));
     P.gtab_stride = 4 * tcap_g;
     slot(CTR_B_HUGE);
+    if (P.p1_list) P.p1_rng = p1_cls + 3;
     GS_TRY((launch_hash<1024, true>(e, P, rhuge, g.n, (uint32_t)tcap_g, 4, 1024, g.dmax,
                                      e->stream)));
   }
@@ -1224,18 +1281,22 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   // for the non-hub part of N(b) (16-byte buckets) + survivor lists (24 B
   // per candidate of a chunk); the small class runs warp-per-b
   slot(CTR_B_LARGE);
+  if (P.p1_list) P.p1_rng = p1_cls + 2;
   GS_TRY((launch_hash<1024, false>(e, P, rc[3], rc[4], 8192, 3, 1024, dcls[0], e->stream)));
   if (ident) e->kev_mark(5);
   slot(CTR_B_MED);
+  if (P.p1_list) P.p1_rng = p1_cls + 1;
   static const int med_chunk = getenv("GS_MED_CHUNK") ? atoi(getenv("GS_MED_CHUNK")) : 1024;
   GS_TRY((launch_hash<512, false, true>(e, P, rc[2], rc[3], 2048, 2, med_chunk, dcls[1], e->stream)));
   if (ident) e->kev_mark(6);
   slot(CTR_B_SMALL);
+  if (P.p1_list) P.p1_rng = p1_cls + 0;
   GS_TRY(launch_warp(e, P, rc[1], rc[2], 1, e->stream));
   if (ident) e->kev_mark(7);
   slot(CTR_B_TINY);
   P.p1_pend = nullptr;  // the tiny class (deg b < 64) is not in stage 1
   P.p1_j0 = nullptr;
+  P.p1_list = nullptr;
   if (rc[1] > rc[0]) {
     int64_t grid = (rc[1] - rc[0] + 255) / 256;
     if (grid > e->sms * 16) grid = e->sms * 16;
@@ -1244,7 +1305,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     GS_CUDA(cudaGetLastError());
   }
   if (ident) e->kev_mark(8);
-  for (int32_t* x : {p1_j0, p1_nit, p1_ioff, p1_owner, p1_pend}) e->release(x);
+  for (int32_t* x : {p1_j0, p1_nit, p1_ioff, p1_owner, p1_pend, p1_list}) e->release(x);
+  e->release(p1_cls);
   if (P.gtab) {
     GS_CUDA(cudaStreamSynchronize(e->stream));
     e->release(P.gtab);
