@@ -1231,7 +1231,8 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
     // 0: S_a read without L1 allocation (best), 1: with, 2: S_a and b's level
     // without, 3: two 32-byte steps per check
     auto kern = p1v == 1 ? k_sk_filter<256, 4, 1, false> : p1v == 2 ? k_sk_filter<256, 4, 1, true, true>
-              : p1v == 3 ? k_sk_filter<256, 4, 2> : k_sk_filter<256, 4, 1>;
+              : p1v == 3 ? k_sk_filter<256, 4, 2> : p1v == 5 ? k_sk_filter<256, 5, 1>
+              : p1v == 6 ? k_sk_filter<256, 6, 1> : k_sk_filter<256, 4, 1>;
     int occ = 0;
     GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0));
     kern<<<(unsigned)(std::max(occ, 1) * e->sms), 256, 0, e->stream>>>(P, lo, p1_j0, p1_ioff,
