@@ -317,6 +317,107 @@ __global__ void k_scatter_edges(const int32_t* __restrict__ uv, int64_t m, int64
   }
 }
 
+// Edge input, bucketed: the direct scatter above issues one random 8-byte
+// cursor atomic and one random 4-byte write per arc over the whole 2m-slot
+// array (ncu at s24: 14.7 ms, 17 GB read + 8 GB written for 4.2 GB of arcs, 95%
+// of cycles with no eligible warp).  Instead (1) each tile of edges sorts its
+// 2 x 2048 arcs into B rank-range buckets of ~equal arc counts (bucket b = the
+// slots of runs [bstart[b], bstart[b+1]), so the (run, neighbour) pairs land
+// in the bucket's own slot range, one global reservation per bucket per tile),
+// then (2) one grid-stride pass over that bucket-ordered array places each
+// arc in its run: at any moment the whole grid works inside one or two
+// buckets, whose cursors and output slots stay in L2.
+static constexpr int kEdgeTile = 8;    // edges per thread per tile
+static constexpr int kMaxBuckets = 1024;
+
+__global__ void __launch_bounds__(256) k_bucket_arcs(const int32_t* __restrict__ uv, int64_t m,
+                                                     int64_t n, const int32_t* __restrict__ rank,
+                                                     const int32_t* __restrict__ bstart, int nbk,
+                                                     unsigned long long* __restrict__ bcur,
+                                                     int2* __restrict__ arcs2,
+                                                     int* __restrict__ bad) {
+  __shared__ int s_cnt[kMaxBuckets], s_pos[kMaxBuckets];
+  __shared__ unsigned long long s_base[kMaxBuckets];
+  __shared__ int32_t s_bst[kMaxBuckets + 1];
+  for (int i = threadIdx.x; i <= nbk; i += blockDim.x) s_bst[i] = bstart[i];
+  const int64_t tile = (int64_t)blockDim.x * kEdgeTile;
+  bool b3 = false;
+  auto bucket_of = [&](int32_t r) {
+    int lo = 0, hi = nbk;  // last b with bstart[b] <= r
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_bst[mid] <= r) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  for (int64_t t0 = (int64_t)blockIdx.x * tile; t0 < m; t0 += (int64_t)gridDim.x * tile) {
+    for (int i = threadIdx.x; i < nbk; i += blockDim.x) { s_cnt[i] = 0; s_pos[i] = 0; }
+    __syncthreads();
+    int32_t ru[kEdgeTile], rv[kEdgeTile];
+    int bu[kEdgeTile], bv[kEdgeTile];
+#pragma unroll
+    for (int k = 0; k < kEdgeTile; ++k) {
+      const int64_t e = t0 + (int64_t)k * blockDim.x + threadIdx.x;
+      ru[k] = rv[k] = -1;
+      if (e < m) {
+        const int2 p = reinterpret_cast<const int2*>(uv)[e];
+        if (p.x < 0 || p.y < 0 || p.x >= n || p.y >= n || p.x == p.y) { b3 = true; continue; }
+        ru[k] = rank[p.x];
+        rv[k] = rank[p.y];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kEdgeTile; ++k) {
+      if (ru[k] < 0) continue;
+      bu[k] = bucket_of(ru[k]);
+      bv[k] = bucket_of(rv[k]);
+      atomicAdd(&s_cnt[bu[k]], 1);
+      atomicAdd(&s_cnt[bv[k]], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbk; i += blockDim.x)
+      if (s_cnt[i]) s_base[i] = atomicAdd(&bcur[i], (unsigned long long)s_cnt[i]);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kEdgeTile; ++k) {
+      if (ru[k] < 0) continue;
+      arcs2[s_base[bu[k]] + atomicAdd(&s_pos[bu[k]], 1)] = make_int2(ru[k], rv[k]);
+      arcs2[s_base[bv[k]] + atomicAdd(&s_pos[bv[k]], 1)] = make_int2(rv[k], ru[k]);
+    }
+    __syncthreads();
+  }
+  if (b3) atomicExch(bad, 1);
+}
+
+__global__ void k_bucket_starts(const int64_t* __restrict__ rows, int nbk,
+                                const int64_t* __restrict__ off, int32_t* __restrict__ bst,
+                                unsigned long long* __restrict__ bcur) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > nbk) return;
+  bst[k] = (int32_t)rows[k];
+  if (k < nbk) bcur[k] = (unsigned long long)off[rows[k]];
+}
+
+// (arcs of one hub run arrive together in its bucket: lanes holding the same
+// run share one cursor atomic, or a hub's cursor serialises the bucket)
+__global__ void k_place_arcs(const int2* __restrict__ arcs2, int64_t slots,
+                             unsigned long long* __restrict__ cur, int32_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int64_t ss = (slots + 31) / 32 * 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ss;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool in = i < slots;
+    const int2 a = in ? arcs2[i] : make_int2(-1 - lane, 0);
+    const unsigned grp = __match_any_sync(0xffffffffu, a.x);
+    const int lead = __ffs(grp) - 1;
+    unsigned long long base = 0;
+    if (in && lane == lead) base = atomicAdd(&cur[a.x], (unsigned long long)__popc(grp));
+    base = __shfl_sync(0xffffffffu, base, lead);
+    if (in) out[base + __popc(grp & below)] = a.y;
+  }
+}
+
 // CSR input: slot i of caller vertex u lands at the same position of u's
 // rank-space run (no atomics); validates ids and the strictly increasing runs.
 static constexpr int64_t kHeavyScatter = 512;  // == deg_class(2): rclass[2] starts them
@@ -905,6 +1006,9 @@ static int rank_and_offsets(gs_engine* e, int64_t n, uint32_t* deg, int64_t* h_c
   return GS_OK;
 }
 
+__global__ void k_row_split(const int64_t* __restrict__ off, int64_t n, int64_t slots, int world,
+                            int64_t* __restrict__ rows);
+
 int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
   cudaStream_t st = e->stream;
   DevGraph& g = e->g;
@@ -928,7 +1032,68 @@ int build_from_edges(gs_engine* e, int64_t n, int64_t m, const int32_t* uv) {
     GS_CUDA(cudaMemcpyAsync(cur, g.off, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToDevice, st));
   int32_t* arcs = nullptr;
   GS_TRY(e->alloc_n(&arcs, 2 * m));
-  if (m > 0) {
+  // bucketed placement (GS_EDGE_BUCKETS=1, when its 8-byte arc buffer fits):
+  // measured 25.2 -> 20.9 ms at R-MAT s24 but 181 -> 209 ms on the skewed
+  // Chung-Lu graph (its hub runs' cursors serialise inside their buckets), so
+  // the direct scatter stays the default
+  static const bool buckets_on = getenv("GS_EDGE_BUCKETS") && atoi(getenv("GS_EDGE_BUCKETS")) == 1;
+  int2* arcs2 = nullptr;
+  if (m > 0 && buckets_on) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = 16 * (size_t)m;
+    if (need < fr / 2 && (!e->cap || e->reserved + need + (64ull << 20) < e->cap)) {
+      if (e->alloc_n(&arcs2, 2 * m) != GS_OK) { cudaGetLastError(); arcs2 = nullptr; }
+    }
+  }
+  if (m > 0 && arcs2) {
+    // ~32 M arcs per bucket (measured best of 2^19..2^25 at s24: 20.9 vs 25.2 ms direct)
+    static const int bshift = getenv("GS_EDGE_BSHIFT") ? atoi(getenv("GS_EDGE_BSHIFT")) : 25;
+    const int nbk = (int)std::min<int64_t>(kMaxBuckets, std::max<int64_t>(1, (2 * m) >> bshift));
+    int64_t* rows = nullptr;
+    int32_t* bst = nullptr;
+    unsigned long long* bcur = nullptr;
+    GS_TRY(e->alloc_n(&rows, nbk + 1));
+    GS_TRY(e->alloc_n(&bst, nbk + 1));
+    GS_TRY(e->alloc_n(&bcur, nbk));
+    k_row_split<<<grid_for(nbk + 1, 256), 256, 0, st>>>(g.off, n, 2 * m, nbk, rows);
+    k_bucket_starts<<<grid_for(nbk + 1, 256), 256, 0, st>>>(rows, nbk, g.off, bst, bcur);
+    const int64_t tiles = (m + 256 * kEdgeTile - 1) / (256 * kEdgeTile);
+    k_bucket_arcs<<<(unsigned)std::min<int64_t>(tiles, (int64_t)e->sms * 8), 256, 0, st>>>(
+        uv, m, n, g.rank, bst, nbk, bcur, arcs2, d_bad);
+    // one launch per bucket (GS_EDGE_PERBUCKET=0: one sweep of the resident
+    // grid): the whole GPU places one bucket's arcs at a time, so its cursors
+    // and output slots are all that is live in L2
+    int occ = 0;
+    GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_place_arcs, 256, 0));
+    const unsigned gp = (unsigned)(std::max(occ, 1) * e->sms);
+    static const bool per_bucket = !(getenv("GS_EDGE_PERBUCKET") && atoi(getenv("GS_EDGE_PERBUCKET")) == 0);
+    if (per_bucket) {
+      std::vector<int64_t> hrows(nbk + 1), hoff(nbk + 1);
+      GS_CUDA(cudaMemcpyAsync(hrows.data(), rows, sizeof(int64_t) * (nbk + 1), cudaMemcpyDeviceToHost, st));
+      GS_CUDA(cudaStreamSynchronize(st));
+      for (int k = 0; k <= nbk; ++k) {
+        GS_CUDA(cudaMemcpyAsync(&hoff[k], g.off + hrows[k], sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      }
+      GS_CUDA(cudaStreamSynchronize(st));
+      for (int k = 0; k < nbk; ++k) {
+        const int64_t a0 = hoff[k], a1 = hoff[k + 1];
+        if (a1 <= a0) continue;
+        k_place_arcs<<<(unsigned)std::min<int64_t>(gp, grid_for(a1 - a0, 256)), 256, 0, st>>>(
+            arcs2 + a0, a1 - a0, cur, arcs);
+      }
+      e->launches += nbk;
+    } else {
+      k_place_arcs<<<gp, 256, 0, st>>>(arcs2, 2 * m, cur, arcs);
+    }
+    e->launches += 4;
+    GS_CUDA(cudaGetLastError());
+    GS_CUDA(cudaStreamSynchronize(st));  // arcs2 / bcur are released below
+    e->release(rows);
+    e->release(bst);
+    e->release(bcur);
+    e->release(arcs2);
+  } else if (m > 0) {
     k_scatter_edges<<<e->sms * 8, 256, 0, st>>>(uv, m, n, g.rank, cur, arcs);
     e->launches++;
   }
