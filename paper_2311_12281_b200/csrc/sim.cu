@@ -409,7 +409,9 @@ __device__ __noinline__ int pf_claim_copy(int32_t* wq, const int32_t* pend, int6
 // cp.async.bulk, completion on an mbarrier) while the CTA works on the current
 // b, whose list is then read from shared memory by the survivor filter, the
 // table build and the bitmap clean-up (`nbuf_words` words per buffer).
-template <int NT, bool GTAB, bool PF = false>
+// S2: the identify stage-2 instance (SIM_PENDING edges only): the sketch
+// machinery of the other modes is compiled out (fewer registers, no spills)
+template <int NT, bool GTAB, bool PF = false, bool S2 = false>
 __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_hash(SimParams P, int64_t rlo, int64_t rhi,
                                                  uint32_t tcap, int qi, int chunk,
                                                  uint32_t hub_lo, uint32_t bm_words,
@@ -438,7 +440,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
   C.stash = s_stash;
   for (uint32_t i = tid; i < ((bm_words + 4 + 3) & ~3u); i += NT) bm[i] = 0u;
 
-  const bool p1 = P.p1_pend != nullptr;  // identify stage 2: SIM_PENDING edges only
+  constexpr bool p1 = S2;  // identify stage 2: SIM_PENDING edges only
   // PF: the prefetched claim, its buffer's mbarrier phase and its list offset
   __shared__ int s_pitem;
   __shared__ int s_pref[2];
@@ -688,7 +690,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
 static constexpr int kWarpBuckets = 256;  // 4 KB: deg < 512 -> <= 0.5 keys per slot
 static constexpr int kWarpWords = 4 * kWarpBuckets + kStash + 4;
 
-template <int NT, int MINB>
+template <int NT, int MINB, bool S2 = false>
 __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
                                                                int64_t rhi, int qi) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -701,7 +703,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
   __shared__ unsigned long long s_ctr[LC_N];
   HotCtr lc;
   shared_ctr_init(s_ctr);
-  const bool p1 = P.p1_pend != nullptr;  // identify stage 2: SIM_PENDING edges only
+  constexpr bool p1 = S2;  // identify stage 2: SIM_PENDING edges only
   for (;;) {
     int item = 0;
     if (lane == 0) item = atomicAdd(&P.wq[qi], 1);
@@ -1054,7 +1056,8 @@ static int launch_hash(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
       chunk /= 2;
     }
   }
-  auto kern = pf ? k_sim_hash<NT, GTAB, PF> : k_sim_hash<NT, GTAB, false>;
+  auto kern = pf ? k_sim_hash<NT, GTAB, PF, true>
+                 : p1 ? k_sim_hash<NT, GTAB, false, true> : k_sim_hash<NT, GTAB, false, false>;
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
@@ -1075,7 +1078,9 @@ static int launch_warp(gs_engine* e, const SimParams& P, int64_t rlo, int64_t rh
   constexpr int NT = 256;
   const size_t smem = (size_t)(NT / 32) * kWarpWords * 4;
   static const int minb = getenv("GS_WARP_MINB") ? atoi(getenv("GS_WARP_MINB")) : 4;
-  auto kern = minb == 3 ? k_sim_warp<NT, 3> : k_sim_warp<NT, 4>;
+  const bool s2 = P.p1_pend != nullptr;
+  auto kern = s2 ? (minb == 3 ? k_sim_warp<NT, 3, true> : k_sim_warp<NT, 4, true>)
+                 : (minb == 3 ? k_sim_warp<NT, 3> : k_sim_warp<NT, 4>);
   GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   GS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem));
