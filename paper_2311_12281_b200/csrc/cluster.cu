@@ -11,6 +11,8 @@
 // exact information classify_vertex_from_neighbors needs (scan.py:794-808).
 #include <algorithm>
 
+#include <cub/cub.cuh>
+
 #include "simcore.cuh"
 
 namespace gs {
@@ -470,6 +472,33 @@ __device__ bool warp_decide(const int64_t* __restrict__ off, const int32_t* __re
   return c >= cmin;
 }
 
+// Work items of the list kernels: 32-arc chunks of each listed vertex's run
+// (its owned prefix, or its whole run), so a hub's thousands of arcs spread
+// over many warps.  ipre = inclusive prefix of the per-entry chunk counts.
+__global__ void k_list_chunks(const int* __restrict__ cnt, const int32_t* __restrict__ list,
+                              const int64_t* __restrict__ off, const int64_t* __restrict__ eoff,
+                              bool owned, int32_t* __restrict__ ch) {
+  const int64_t c = *cnt;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = list[i];
+    const int64_t len = owned ? eoff[v + 1] - eoff[v] : off[v + 1] - off[v];
+    ch[i] = (int32_t)max((int64_t)1, (len + 31) >> 5);  // >= 1: every entry is visited
+  }
+}
+
+// item -> (list index k, first arc of the chunk)
+__device__ __forceinline__ int64_t item_entry(const int32_t* __restrict__ ipre, int64_t cnt,
+                                              int64_t item, int64_t& base) {
+  int64_t lo = 0, hi = cnt;  // first k with ipre[k] > item
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)ipre[mid] <= item) lo = mid + 1; else hi = mid;
+  }
+  base = (item - (lo > 0 ? (int64_t)ipre[lo - 1] : 0)) * 32;
+  return lo;
+}
+
 // the cores as a list, and the sum of their degrees (the sparse paths' work)
 // (deg_sum[0] += degrees, deg_sum[1] = max degree)
 __global__ void k_core_list(int64_t n, const uint8_t* __restrict__ role,
@@ -500,6 +529,7 @@ __global__ void k_core_list(int64_t n, const uint8_t* __restrict__ role,
 // (c is their high endpoint: e = eoff[c] + i); known-similar edges union, an
 // unknown one is decided unless both ends already share a root (scan.py:601-660)
 __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
+                               const int32_t* __restrict__ ipre,
                                const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
                                const int64_t* __restrict__ eoff, const int2* __restrict__ thr,
                                Eps2 eps, uint8_t* __restrict__ sim,
@@ -508,11 +538,13 @@ __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nc = *ncores;
+  const int64_t items = nc > 0 ? ipre[nc - 1] : 0;
   unsigned long long evals = 0, probes = 0, retries = 0;
-  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
-    const int32_t c = clist[k];
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    int64_t base = 0;
+    const int32_t c = clist[item_entry(ipre, nc, it, base)];
     const int64_t oc = off[c], e0 = eoff[c], nlow = eoff[c + 1] - e0;
-    for (int64_t base = 0; base < nlow; base += 32) {
+    {
       const int64_t i = base + lane;
       int32_t w = -1;
       uint8_t st = SIM_DISSIMILAR;
@@ -553,6 +585,7 @@ __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __
 // neighbour w (e = eoff[high] + position of low in high's run); similar ->
 // w's member labels take c's canonical label (scan.py:662-698)
 __global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
+                                const int32_t* __restrict__ ipre,
                                 const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
                                 const int64_t* __restrict__ eoff, const int2* __restrict__ thr,
                                 Eps2 eps, uint8_t* __restrict__ sim,
@@ -561,12 +594,14 @@ __global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* _
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nc = *ncores;
+  const int64_t items = nc > 0 ? ipre[nc - 1] : 0;
   unsigned long long evals = 0, probes = 0;
-  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
-    const int32_t c = clist[k];
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    int64_t base = 0;
+    const int32_t c = clist[item_entry(ipre, nc, it, base)];
     const int32_t L = lmin[c];
     const int64_t oc = off[c], dc = off[c + 1] - oc, nlow = eoff[c + 1] - eoff[c];
-    for (int64_t base = 0; base < dc; base += 32) {
+    {
       const int64_t i = base + lane;
       int32_t w = -1;
       int64_t e = -1;
@@ -643,6 +678,7 @@ __global__ void k_clustered_list(int64_t n, const int32_t* __restrict__ lmax,
 // ... whose final roles are set here, and whose unclustered neighbours (the
 // only hub candidates) are listed once each (first setter of their mark byte)
 __global__ void k_near_list(const int* __restrict__ nclu, const int32_t* __restrict__ clu,
+                            const int32_t* __restrict__ ipre,
                             const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
                             const int32_t* __restrict__ lmax, const uint8_t* __restrict__ role,
                             uint8_t* __restrict__ mark, int32_t* __restrict__ near,
@@ -650,10 +686,13 @@ __global__ void k_near_list(const int* __restrict__ nclu, const int32_t* __restr
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nc = *nclu;
-  for (int64_t k = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; k < nc; k += nw) {
-    const int32_t u = clu[k];
-    if (lane == 0) fin[u] = role[u] == ROLE_CORE ? ROLE_CORE : ROLE_MEMBER;
-    for (int64_t i = off[u] + lane; i < off[u + 1]; i += 32) {
+  const int64_t items = nc > 0 ? ipre[nc - 1] : 0;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    int64_t base = 0;
+    const int32_t u = clu[item_entry(ipre, nc, it, base)];
+    if (lane == 0 && base == 0) fin[u] = role[u] == ROLE_CORE ? ROLE_CORE : ROLE_MEMBER;
+    const int64_t i = off[u] + base + lane;
+    if (i < off[u + 1]) {
       const int32_t w = adj[i];
       if (lmax[w] >= 0) continue;
       const unsigned bit = 1u << (8 * (w & 3));
@@ -717,7 +756,33 @@ __global__ void __launch_bounds__(256) k_classify_list(const int* __restrict__ n
 // Sparse (core-centric) union / attach iff the cores' arcs are at most this
 // fraction of all arcs (GS_SPARSE_CLUSTER=0 / 1 forces the dense / sparse path)
 static constexpr int64_t kSparseDiv = 16;
-static constexpr int64_t kSparseMaxDeg = 4096;  // ... and no core / clustered vertex above this degree
+// ... and no core above this degree: a hub core's edges are decided by binary
+// searches in its run one by one (eps 0.2 at s24, a core of degree 92 K:
+// cluster 9.2 ms dense, 13.5 sparse; eps 0.15 mu 3, cores <= 31: 13.2 -> 5.1)
+static constexpr int64_t kSparseMaxDeg = 4096;
+// classification from the clustered side iff their arcs are <= 2m / 64 (eps 0.2:
+// 1.5 M arcs, 4.0 -> 2.6 ms; eps 0.15 mu 3 with 1.5 M hub candidates: 5.3 -> 9.0)
+static constexpr int64_t kListDiv = 64;
+
+// inclusive prefix of the 32-arc chunk counts of list[0, cnt) (owned prefix or
+// whole run); the caller releases *ipre once the launch using it is ordered
+static int list_chunks(gs_engine* e, int64_t cnt, const int* d_cnt, const int32_t* list,
+                       bool owned, int32_t** ipre) {
+  DevGraph& g = e->g;
+  int32_t* ch = nullptr;
+  GS_TRY(e->alloc_n(&ch, cnt));
+  GS_TRY(e->alloc_n(ipre, cnt));
+  k_list_chunks<<<gridv(e, cnt), 256, 0, e->stream>>>(d_cnt, list, g.off, g.eoff, owned, ch);
+  size_t tb = 0;
+  GS_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, ch, *ipre, (int)cnt, e->stream));
+  void* t = nullptr;
+  GS_TRY(e->alloc(&t, tb > 0 ? tb : 1));
+  GS_CUDA(cub::DeviceScan::InclusiveSum(t, tb, ch, *ipre, (int)cnt, e->stream));
+  e->release(t);
+  e->release(ch);
+  e->launches += 2;
+  return GS_OK;
+}
 
 static int sparse_mode() {
   static const int v = getenv("GS_SPARSE_CLUSTER") ? atoi(getenv("GS_SPARSE_CLUSTER")) : -1;
@@ -743,15 +808,17 @@ int phase_union(gs_engine* e) {
     GS_CUDA(cudaStreamSynchronize(e->stream));
     e->release(dsum);
     e->launches++;
-    // a core's edges are decided one by one by its warp: no hub cores
     s.sparse = sparse_mode() == 1 ||
                ((int64_t)h[0] <= 2 * g.m / kSparseDiv && (int64_t)h[1] <= kSparseMaxDeg);
   }
   if (s.sparse) {
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)(e->ncores + 7) / 8, (int64_t)e->sms * 16);
-    k_union_sparse<<<grid, 256, 0, e->stream>>>(s.lcnt, s.clist, g.off, g.adj, g.eoff, s.thr, e->eps,
-                                               s.sim, s.role, s.parent, s.ctr);
+    int32_t* ipre = nullptr;
+    GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, true, &ipre));
+    k_union_sparse<<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off, g.adj,
+                                                                g.eoff, s.thr, e->eps, s.sim,
+                                                                s.role, s.parent, s.ctr);
     e->launches++;
+    e->release(ipre);  // stream-ordered reuse
     GS_CUDA(cudaGetLastError());
     return GS_OK;
   }
@@ -866,10 +933,14 @@ int phase_attach(gs_engine* e) {
   DevGraph& g = e->g;
   DevState& s = e->s;
   if (s.sparse) {
-    const unsigned grid = (unsigned)std::min<int64_t>((int64_t)(e->ncores + 7) / 8, (int64_t)e->sms * 16);
-    k_attach_sparse<<<grid, 256, 0, e->stream>>>(s.lcnt, s.clist, g.off, g.adj, g.eoff, s.thr,
-                                                e->eps, s.sim, s.role, s.lmin, s.lmax, s.ctr);
+    int32_t* ipre = nullptr;
+    GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, false, &ipre));
+    k_attach_sparse<<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off,
+                                                                 g.adj, g.eoff, s.thr, e->eps,
+                                                                 s.sim, s.role, s.lmin, s.lmax,
+                                                                 s.ctr);
     e->launches++;
+    e->release(ipre);
     GS_CUDA(cudaGetLastError());
     return GS_OK;
   }
@@ -936,11 +1007,12 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     GS_CUDA(cudaMemsetAsync(dsum, 0, 2 * sizeof(unsigned long long), str));
     k_clustered_list<<<gridv(e, n), 256, 0, str>>>(n, s.lmax, clu, cnt, dsum, g.off);
     unsigned long long h[2] = {0, 0};
+    int hc = 0;
     GS_CUDA(cudaMemcpyAsync(h, dsum, sizeof(h), cudaMemcpyDeviceToHost, str));
+    GS_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, str));
     GS_CUDA(cudaStreamSynchronize(str));
     e->launches++;
-    listed = sparse_mode() == 1 ||
-             ((int64_t)h[0] <= 2 * m / kSparseDiv && (int64_t)h[1] <= kSparseMaxDeg);
+    listed = sparse_mode() == 1 || (int64_t)h[0] <= 2 * m / kListDiv;
     if (listed) {
       int32_t* nearl = nullptr;
       GS_TRY(e->alloc_n(&nearl, n));
@@ -948,8 +1020,11 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
       GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)((n + 3) & ~int64_t(3)), str));
       GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
       const unsigned gw = (unsigned)std::min<int64_t>(grid_for((int64_t)n * 32, 256), (int64_t)e->sms * 16);
-      k_near_list<<<gw, 256, 0, str>>>(cnt, clu, g.off, g.adj, s.lmax, s.role, s.coreadj, nearl,
-                                       cnt + 1, fin);
+      int32_t* ipre = nullptr;
+      GS_TRY(list_chunks(e, std::max(hc, 1), cnt, clu, false, &ipre));
+      k_near_list<<<gw, 256, 0, str>>>(cnt, clu, ipre, g.off, g.adj, s.lmax, s.role, s.coreadj,
+                                       nearl, cnt + 1, fin);
+      e->release(ipre);
       k_classify_list<<<(unsigned)e->sms * 8, 256, 0, str>>>(cnt + 1, nearl, g.off, g.adj, s.lmin,
                                                              s.lmax, fin);
       e->launches += 2;
