@@ -484,11 +484,11 @@ __global__ void k_scatter_csr_heavy(const int64_t* __restrict__ off, int64_t n, 
 // ---------------------------------------------------------------------------
 // Per-run sorts, in place.  Degrees ascend with the rank, so each size class
 // is a contiguous rank range: [2, 32] one warp per run (register bitonic
-// network over shuffles), (32, 256] one warp per run (bitonic in a 1 KB
-// shared-memory slice), (256, 4096) one CTA per run (bitonic in shared
-// memory), >= 4096 (a few thousand hub runs holding a large share of the
-// arcs) one radix sort over (run, neighbour) keys.  A repeated neighbour
-// after sorting is a duplicate undirected edge (bad = 5).
+// network over shuffles), (32, 512] one warp per run (2-16 keys per lane in
+// registers, k_sort_runs_wreg), (512, 4096) one CTA per run (block radix
+// sort), >= 4096 (a few thousand hub runs holding a large share of the arcs)
+// a segmented radix sort over the neighbour bits.  A repeated neighbour after
+// sorting is a duplicate undirected edge (bad = 5).
 
 static constexpr int32_t kPad = 0x7fffffff;
 
@@ -637,50 +637,6 @@ __global__ void __launch_bounds__(256) k_sort_runs_reg(const int64_t* __restrict
 }
 
 // bitonic sort of s[0, P) (P a power of two) by the `nt` threads of a group
-template <bool BLOCK>
-__device__ __forceinline__ void bitonic_smem(int32_t* s, int P, int t, int nt) {
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = t; i < (P >> 1); i += nt) {
-        const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
-        const int32_t a = s[lo], b = s[hi];
-        if ((a > b) == ((lo & k) == 0)) { s[lo] = b; s[hi] = a; }
-      }
-      if (BLOCK) __syncthreads(); else __syncwarp();
-    }
-  }
-}
-
-template <bool BLOCK, int CAP>
-__global__ void __launch_bounds__(256) k_sort_runs_smem(const int64_t* __restrict__ off,
-                                                        RunSet R, int32_t* __restrict__ arcs,
-                                                        int* __restrict__ bad) {
-  __shared__ int32_t buf[BLOCK ? CAP : 8 * CAP];
-  const int nt = BLOCK ? blockDim.x : 32;
-  const int t = BLOCK ? threadIdx.x : (threadIdx.x & 31);
-  int32_t* s = BLOCK ? buf : buf + (threadIdx.x >> 5) * CAP;
-  const int64_t groups = BLOCK ? gridDim.x : ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t g0 = BLOCK ? blockIdx.x : (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nr = rs_size(R);
-  for (int64_t it = g0; it < nr; it += groups) {
-    const int64_t v = rs_at(R, it);
-    const int64_t o = off[v];
-    const int d = (int)(off[v + 1] - o);
-    int P = 1;
-    while (P < d) P <<= 1;
-    for (int i = t; i < P; i += nt) s[i] = i < d ? arcs[o + i] : kPad;
-    if (BLOCK) __syncthreads(); else __syncwarp();
-    bitonic_smem<BLOCK>(s, P, t, nt);
-    bool dup = false;
-    for (int i = t; i < d; i += nt) {
-      arcs[o + i] = s[i];
-      dup |= (i + 1 < d && s[i + 1] == s[i]);
-    }
-    if (dup) atomicExch(bad, 5);
-    if (BLOCK) __syncthreads(); else __syncwarp();
-  }
-}
-
 // one CTA per run of up to 256*ITEMS neighbours: block radix sort over the
 // rank bits (+ one bit that sends the padding to the end)
 template <int NT, int ITEMS>
