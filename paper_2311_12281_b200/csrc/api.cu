@@ -131,19 +131,20 @@ int gs_engine::alloc(void** p, size_t bytes) {
   return GS_OK;
 }
 
-void gs_engine::kev_mark(int i) {
+void gs_engine::kev_mark(int i, cudaStream_t on) {
   if (!kev_on) return;
   if (kev[i] == nullptr && cudaEventCreate(&kev[i]) != cudaSuccess) {
     kev[i] = nullptr;
     return;
   }
-  cudaEventRecord(kev[i], stream);
+  cudaEventRecord(kev[i], on ? on : stream);
 }
 
 void gs_engine::kev_class_ms(double* out) {
   // class c runs between events from[c] and to[c] (the sketch filter first)
-  static const int from[kKernelClasses] = {0, 3, 4, 5, 6, 7, 2};
-  static const int to[kKernelClasses] = {1, 4, 5, 6, 7, 8, 3};
+  // (the tiny class runs on the copy stream, concurrently: events 9 / 10)
+  static const int from[kKernelClasses] = {0, 3, 4, 5, 6, 9, 2};
+  static const int to[kKernelClasses] = {1, 4, 5, 6, 7, 10, 3};
   for (int c = 0; c < kKernelClasses; ++c) {
     const int a = from[c], b = to[c];
     float t = 0;

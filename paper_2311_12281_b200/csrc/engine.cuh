@@ -203,9 +203,9 @@ struct gs_engine {
   // kev[2] at the start of the sweep, kev[3] after the sketch filter, kev[3 + c]
   // after class c (huge, large, medium, small, tiny); recorded when kev_on, read into
   // gs_stats.phase_ms[GS_PH_K_PREP ..] (kev_class_ms)
-  cudaEvent_t kev[gs::kKernelClasses + 2] = {};  // see kev_class_ms
+  cudaEvent_t kev[gs::kKernelClasses + 4] = {};  // see kev_class_ms
   bool kev_on = false;
-  void kev_mark(int i);
+  void kev_mark(int i, cudaStream_t on = nullptr);
   void kev_class_ms(double* out);  // [kKernelClasses], synchronises the events
 
   int alloc(void** p, size_t bytes);
