@@ -147,7 +147,6 @@ struct SimParams {
   float sk_gate;        // try the sketch bound iff expected false hits < gate * c_min
   int32_t sk_minscan;   //   and the scan would need at least this many misses
   int sk_thread;        // thread-per-survivor sketch pass before the warp scans
-  int sk_adapt = 0;     // stage 1: resolution per edge, target M ~ d_b * sk_adapt / 4 (0: a's row)
   int32_t sk_tmax;      //   for rows of at most this many words (longer: per warp)
   int bslot;            // counter slot of this launch's algorithmic bytes (CTR_B_*)
   // identify stage 2: the sketch filter (k_sk_filter) ran first; only edges

@@ -977,26 +977,11 @@ __global__ void __launch_bounds__(NT, MINB) k_sk_filter(SimParams P, int64_t rlo
         // endpoints both have a role (Alg. 2 line 2)
         if (ra == ROLE_UNKNOWN || rb == ROLE_UNKNOWN) {
           const int32_t cmin = (int32_t)c_min_exact(da, db, da - 1, P.eps);
-          // Resolution per edge (P.sk_adapt): the walk reads ~M e^(d_b / M) / 32 words
-          // to prove an edge at resolution M, least at M ~ d_b, so S_a and b's
-          // level are both taken at the stored level of a's slot nearest to that
-          // (a's row is the finest available)
-          const int64_t wa = skb ? sk_words(da, P.sk_lk) : 0;
-          int64_t wl = wa;
-          if (skb && P.sk_adapt > 0) {
-            const int64_t target = max((int64_t)4, (db * P.sk_adapt) >> 7);  // words
-            while (wl > 4 && (wl >> 1) >= target) wl >>= 1;
-          }
-          bool tryit = false;
-          if (skb && da >= P.sk_dmin && da - cmin + 1 >= P.sk_minscan) {
-            const float ma = 32.f * (float)wl, fa = (float)da;
-            const float ef = fa * (1.f - __expf(-(float)db / ma)) + fa * fa / (2.f * ma);
-            tryit = ef < P.sk_gate * (float)cmin;
-          }
-          if (tryit) {
+          if (skb && sk_try(P, da, db, cmin)) {
+            const int64_t wa = sk_words(da, P.sk_lk);
             unsigned long long words = 0;
-            dis = sk_rejects256<UNROLL, NA, NAB>(sk_row(P, a, da, wa) + 2 * (wa - wl),
-                                                 levb + 2 * (wb - wl), wl, da, cmin, words);
+            dis = sk_rejects256<UNROLL, NA, NAB>(sk_row(P, a, da, wa), levb + 2 * (wb - wa), wa,
+                                                 da, cmin, words);
             by += 4ull * words;  // S_a's words read (b's level: per b, above)
           }
           if (dis) {  // record_edge(dissimilar), the role decision deferred
@@ -1138,9 +1123,6 @@ int run_prepass(gs_engine* e, int32_t mu) {
 static constexpr int64_t kSketchDmin = 32;  // below: one scan step decides (measured: 32 < 48 < 64)
 static int sketch_lk(const Eps2& eps) {
   const double e = sqrt(eps.ratio);
-  // adaptive resolution (GS_SK_ADAPT > 0): k = 8 rows, stage 1 picks a level per edge
-  static const int adapt = getenv("GS_SK_ADAPT") ? atoi(getenv("GS_SK_ADAPT")) : 0;
-  if (adapt > 0) return 3;
   return e >= 0.33 ? 2 : 3;  // measured: k = 4 wins from eps 0.35, k = 8 at 0.3
 }
 
@@ -1202,7 +1184,6 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   P.sk_thread = 1;
   if (const char* v = getenv("GS_SKETCH_THREAD")) P.sk_thread = atoi(v);
   P.sk_tmax = 1 << 30;
-  P.sk_adapt = getenv("GS_SK_ADAPT") ? atoi(getenv("GS_SK_ADAPT")) : 0;
   if (const char* v = getenv("GS_SKETCH_TMAX")) P.sk_tmax = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
