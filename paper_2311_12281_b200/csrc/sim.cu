@@ -159,13 +159,20 @@ __global__ void __launch_bounds__(256) k_sim_tiny(SimParams P, int64_t rlo, int6
         const int64_t cmin = c_min_exact(da, db, cmax, P.eps);
         int64_t c = 0, ia = ia0, ib = ob;
         res = false;
-        while (ia < ea && ib < eb) {
-          const int32_t x = P.adj[ia], y = P.adj[ib];
-          if (x == y) { ++c; ++ia; ++ib; }
-          else if (x < y) ++ia;
-          else ++ib;
-          if (c >= cmin) { res = true; break; }
-          if (c + (ea - ia) < cmin) break;
+        // branch-free merge: both heads stay in registers, only the one that
+        // advanced is reloaded (the loop issued two loads per step before)
+        if (ia < ea && ib < eb) {
+          int32_t x = P.adj[ia], y = P.adj[ib];
+          for (;;) {
+            const bool le = x <= y, ge = x >= y;
+            c += (le && ge);
+            ia += le;
+            ib += ge;
+            if (c >= cmin) { res = true; break; }
+            if (ia >= ea || ib >= eb || c + (ea - ia) < cmin) break;
+            if (le) x = P.adj[ia];
+            if (ge) y = P.adj[ib];
+          }
         }
         lc.probes += (unsigned long long)(ia - ia0);
         lc.inters++;
