@@ -15,5 +15,5 @@ timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --python-ref-
 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --python-ref-seconds 0 --sharded > gpurun_out/rec/sharded_s24.json 2> gpurun_out/rec/sharded_s24.err
 GS_NO_WARMUP=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sk_filter|k_fused_warp" -c 2 -o gpurun_out/rec/s24_eps0.5_full $B > /dev/null 2>&1
 timeout 900 python tools/chunglu_bench.py --steps 3 > gpurun_out/rec/chunglu.json 2> gpurun_out/rec/chunglu.err
-timeout 900 python bench.py --scale 28 --steps 2 --warmup 1 --no-cpu-baseline --python-ref-seconds 0 --no-e2e > gpurun_out/rec/s28.json 2> gpurun_out/rec/s28.err
+timeout 900 python bench.py --scale 28 --steps 2 --warmup 3 --no-cpu-baseline --python-ref-seconds 0 --no-e2e > gpurun_out/rec/s28.json 2> gpurun_out/rec/s28.err
 ls -la gpurun_out/rec
