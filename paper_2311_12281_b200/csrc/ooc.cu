@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(NT, 1) k_ooc_cta(OocParams P, uint32_t tcap, i
   int2* surv_jc = surv_ad + chunk;
   uint32_t* surv_sk = reinterpret_cast<uint32_t*>(surv_jc + chunk);  // sketch row or ~0
   uint32_t* lev = surv_sk + chunk;  // b's sketch levels [skw] (16-byte aligned: chunk % 4 == 0)
-  __shared__ int s_item, s_nsurv, s_next, s_nstash, s_nkeep;
+  __shared__ int s_item, s_nsurv, s_next, s_nstash;
   __shared__ unsigned int s_bsim, s_bdis;
   __shared__ uint32_t s_stash[kStash];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -563,8 +563,10 @@ __global__ void k_ooc_to_root(int64_t n, const uint8_t* __restrict__ role, int32
 }
 
 // lmin (in parent) and lmax (in aux) from the root labels held in aux
-__global__ void k_ooc_labels(int64_t n, const uint8_t* __restrict__ role, int32_t* __restrict__ parent,
-                             const int32_t* __restrict__ rootlab, int32_t* __restrict__ lmin_out) {
+// lmin_out may be parent itself (in place: each thread reads parent[v] before
+// it writes slot v), so neither is __restrict__
+__global__ void k_ooc_labels(int64_t n, const uint8_t* __restrict__ role, const int32_t* parent,
+                             const int32_t* __restrict__ rootlab, int32_t* lmin_out) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x)
     lmin_out[v] = role[v] == ROLE_CORE ? rootlab[parent[v]] : 0x7fffffff;

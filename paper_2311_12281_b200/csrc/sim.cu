@@ -20,6 +20,7 @@
 #include <algorithm>
 
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include "simcore.cuh"
 
@@ -1111,7 +1112,7 @@ static constexpr int64_t kHubBits = 1 << 18;
 int run_prepass(gs_engine* e, int32_t mu) {
   DevGraph& g = e->g;
   DevState& s = e->s;
-  const int64_t n = g.n, rsplit = g.rclass[1];
+  const int64_t n = g.n;
   if (n == 0) return GS_OK;
   int64_t own_lo = 0, own_hi = n;
   if (e->shard_world > 1)
@@ -1296,7 +1297,7 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
       GS_TRY(e->alloc_n(&p1_list, nb));
       GS_TRY(e->alloc_n(&p1_cls, 8));
       size_t tb2 = 0;
-      cub::CountingInputIterator<int32_t> it((int32_t)lo);
+      thrust::counting_iterator<int32_t> it((int32_t)lo);
       const HasPending pred{p1_pend, lo};
       GS_CUDA(cub::DeviceSelect::If(nullptr, tb2, it, p1_list, p1_cls + 5, (int)nb, pred, e->stream));
       void* t2 = nullptr;
