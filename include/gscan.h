@@ -13,6 +13,7 @@
  *   gs_build_graph     build_graph(el)                           graph.py:162-259
  *   gs_scan_partitioned scan_out_of_core(meta, plan, mu, eps)    partition.py:666-757
  *   gs_check_sim       check_sim over a batch of edges           scan.py:241-258
+ *   gs_plan_closure    partition_graph(g, budget, spill_dir)     partition.py:231-333
  *   gs_engine_*        a reusable device context (stream, memory pool,
  *                      resident graph) behind the one-shot calls
  *
@@ -245,6 +246,20 @@ int gs_scan_partitioned_plan(int64_t n, int64_t m, const int64_t* offsets,
                              const int32_t* adjacency, int32_t mu, const gs_eps2* eps2,
                              uint64_t hbm_cap_bytes, int64_t nparts, const int64_t* part_bounds,
                              uint8_t* role_out, int32_t* cluster_out, gs_stats* stats);
+
+/* The reference's closure planner (partition_graph, partition.py:231-333), host
+ * only, for spill files in its GSCP format (partition.py:336-446): edges in
+ * edge_list order, each adding its closure (every edge at either endpoint);
+ * a partition is sealed when 25*|E_s| + 4*|V_s| + state_bytes would exceed
+ * budget_bytes.  Partition p owns edge ids [owned_bounds[p], owned_bounds[p+1])
+ * and its closure has n_local[p] vertices and m_local[p] edges.  Arrays hold
+ * `cap` partitions (owned_bounds cap + 1); *nparts is the full count, so a
+ * call with *nparts > cap is repeated with a larger cap.  GS_EBUDGET: one
+ * edge's closure cannot fit; bad_edge[3] = (u, v, required bytes). */
+int gs_plan_closure(int64_t n, int64_t m, const int64_t* offsets, const int32_t* adjacency,
+                    const int32_t* edge_ids, const int32_t* edge_list, uint64_t budget_bytes,
+                    int64_t state_bytes, int64_t* owned_bounds, int64_t* n_local,
+                    int64_t* m_local, int64_t cap, int64_t* nparts, int64_t* bad_edge);
 
 /* Deterministic R-MAT workload generator (bench/test input; same stream as
  * the CPU generator in oracle/): raw samples, device pointers. */

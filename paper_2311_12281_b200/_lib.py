@@ -122,6 +122,9 @@ SIGNATURES = [
     ("gs_scan_partitioned_plan", ctypes.c_int,
      [_I64, _I64, _P, _P, _I32, ctypes.POINTER(GsEps2), ctypes.c_uint64, _I64, _P, _P, _P,
       ctypes.POINTER(GsStats)]),
+    ("gs_plan_closure", ctypes.c_int,
+     [_I64, _I64, _P, _P, _P, _P, ctypes.c_uint64, _I64, _P, _P, _P, _I64,
+      ctypes.POINTER(_I64), _P]),
     ("gs_rmat_generate", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, _P, _P, _P]),
     ("gs_chunglu_generate", ctypes.c_int,
      [ctypes.c_int, ctypes.c_double, ctypes.c_double, _I64, ctypes.c_uint64, _P, _P, _P]),

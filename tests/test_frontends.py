@@ -126,6 +126,17 @@ def test_cli_runs(fixture_file, tmp_path, capsys):
     assert cli.main(["--input", fixture_file, "--epsilon", "0.6", "--mu", "3", "--mode",
                      "outofcore", "--budget", str(64 << 20), "--output", str(o3)]) == 0
     assert o3.read_bytes() == out.read_bytes()
+    # --spill-dir: the reference's partition files and manifest are written too
+    sd = tmp_path / "spill"
+    o4 = tmp_path / "o4.txt"
+    assert cli.main(["--input", fixture_file, "--epsilon", "0.6", "--mu", "3", "--mode",
+                     "outofcore", "--budget", str(64 << 20), "--spill-dir", str(sd),
+                     "--output", str(o4)]) == 0
+    assert o4.read_bytes() == out.read_bytes()
+    man = (sd / "plan.manifest").read_text().splitlines()
+    assert man[:2] == ["n=14", "m=23"] and man[3] == "global_state_bytes=210"
+    assert man[4] == "partitions=1" and man[5].split("\t")[1] == "part-00000.bin"
+    assert (sd / "part-00000.bin").read_bytes()[:4] == b"GSCP"
     assert cli.main(["--input", fixture_file, "--epsilon", "0.6", "--mu", "3", "--mode",
                      "outofcore", "--budget", "250"]) == 3
     assert "bytes" in capsys.readouterr().err

@@ -60,7 +60,7 @@ def test_plan_is_validated_before_any_device_work():
     plan = gs.partition_graph(g, budget)
     assert len(plan.partitions) >= 3
     meta = gs.GraphMeta.from_graph(g)
-    whole = gs.partition.PartitionInfo(0, 0, n, 0, 2 * g.m)  # one slice: too big for the cap
+    whole = gs.partition.StreamSlice(0, 0, n, 0, 2 * g.m)  # one slice: too big for the cap
     bad = gs.PartitionPlan(n=n, m=g.m, budget_bytes=budget, partitions=[whole], graph=g)
     with pytest.raises(gs.InfeasibleBudgetError, match="partition 0"):
         gs.scan_out_of_core(meta, bad, 3, "0.5")
