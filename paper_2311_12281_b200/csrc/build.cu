@@ -679,6 +679,85 @@ __global__ void __launch_bounds__(NT) k_sort_runs_block(const int64_t* __restric
   if (t == 0 && s_dup) atomicExch(bad, 5);
 }
 
+// ... and runs of up to NT*ITEMS (16384) neighbours in place, one 1024-thread
+// CTA per run, the radix sort's scratch in dynamic shared memory (the hub runs
+// of the host-CSR chunk pipeline, sorted while later chunks are in flight)
+template <int NT, int ITEMS, int RB>
+__global__ void __launch_bounds__(NT, 1) k_sort_runs_block_dyn(const int64_t* __restrict__ off,
+                                                                RunSet R, int endbit,
+                                                                int32_t* __restrict__ arcs,
+                                                                int* __restrict__ bad) {
+  using Sort = cub::BlockRadixSort<uint32_t, NT, ITEMS, cub::NullType, RB>;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  typename Sort::TempStorage& tmp = *reinterpret_cast<typename Sort::TempStorage*>(dsm);
+  __shared__ int s_dup;
+  const int t = threadIdx.x;
+  if (t == 0) s_dup = 0;
+  const int64_t nr = rs_size(R);
+  for (int64_t it = blockIdx.x; it < nr; it += gridDim.x) {
+    const int64_t v = rs_at(R, it);
+    const int64_t o = off[v];
+    const int d = (int)(off[v + 1] - o);
+    uint32_t k[ITEMS];
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      k[i] = idx < d ? (uint32_t)arcs[o + idx] : 0xFFFFFFFFu;
+    }
+    Sort(tmp).SortBlockedToStriped(k, 0, endbit);
+    bool dup = false;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx < d) arcs[o + idx] = (int32_t)k[i];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const int idx = i * NT + t;
+      if (idx + 1 < d) dup |= arcs[o + idx] == arcs[o + idx + 1];
+    }
+    if (dup) s_dup = 1;
+    __syncthreads();
+  }
+  if (t == 0 && s_dup) atomicExch(bad, 5);
+}
+
+// segment bounds of the listed runs for a segmented sort; slots past the
+// list's count are empty segments (the launch is sized for every hub run)
+__global__ void k_list_segments(const int64_t* __restrict__ off, const int32_t* __restrict__ list,
+                                const int* __restrict__ count, int64_t nseg,
+                                int64_t* __restrict__ beg, int64_t* __restrict__ end) {
+  const int64_t c = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseg;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i < c ? (int64_t)list[i] : -1;
+    beg[i] = v >= 0 ? off[v] : 0;
+    end[i] = v >= 0 ? off[v + 1] : 0;
+  }
+}
+
+// the listed runs back from the sort's alternate buffer (src, when the sort
+// ended there) and their duplicate check, one CTA per run
+__global__ void k_list_finish(const int64_t* __restrict__ off, const int32_t* __restrict__ list,
+                              const int* __restrict__ count, const int32_t* __restrict__ src,
+                              int32_t* __restrict__ arcs, int* __restrict__ bad) {
+  __shared__ int s_dup;
+  if (threadIdx.x == 0) s_dup = 0;
+  const int64_t c = *count;
+  for (int64_t it = blockIdx.x; it < c; it += gridDim.x) {
+    const int64_t v = list[it], lo = off[v], hi = off[v + 1];
+    if (src)
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) arcs[i] = src[i];
+    __syncthreads();
+    bool dup = false;
+    for (int64_t i = lo + threadIdx.x; i + 1 < hi; i += blockDim.x) dup |= arcs[i] == arcs[i + 1];
+    if (dup) s_dup = 1;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && s_dup) atomicExch(bad, 5);
+}
+
 // composite keys (run index within the tail, neighbour) of the long runs
 __global__ void k_tail_keys(const int64_t* __restrict__ off, int64_t rlo, int64_t rhi,
                             const int32_t* __restrict__ arcs, int B,
@@ -1185,15 +1264,16 @@ int build_from_csr(gs_engine* e, int64_t n, int64_t m, const int64_t* off, const
 
 // Per-run sort classes of the runs a host chunk completed (caller vertices
 // [ua, ub), their rank-space runs in [row_lo, row_hi)): ranks appended to
-// six class lists (the classes of sort_runs; runs >= 4096 and < 2 are left to
-// the final pass), one shared-memory count + one global reservation per
-// class per block.
-static constexpr int kChunkClasses = 6;
+// eight class lists (the six classes of sort_runs below 4096, then [4096,
+// 16384] and longer hub runs; runs < 2 need no sort), one shared-memory count
+// + one global reservation per class per block.  With `hubs` false the hub
+// runs are left to the final pass.
+static constexpr int kChunkClasses = 8;
 __global__ void __launch_bounds__(256) k_chunk_classes(const int64_t* __restrict__ off, int64_t ua,
                                                        int64_t ub, const int32_t* __restrict__ rank,
                                                        int64_t row_lo, int64_t row_hi,
                                                        int32_t* __restrict__ lists, int64_t stride,
-                                                       int* __restrict__ counts) {
+                                                       int* __restrict__ counts, bool hubs) {
   __shared__ int s_cnt[kChunkClasses], s_base[kChunkClasses];
   for (int64_t base = ua + (int64_t)blockIdx.x * blockDim.x; base < ub;
        base += (int64_t)gridDim.x * blockDim.x) {
@@ -1205,8 +1285,9 @@ __global__ void __launch_bounds__(256) k_chunk_classes(const int64_t* __restrict
     if (u < ub) {
       const int64_t d = off[u + 1] - off[u];
       r = rank[u];
-      if (r >= row_lo && r < row_hi && d >= 2 && d < 4096)
-        cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= 512 ? 2 : d <= 1024 ? 3 : d <= 2048 ? 4 : 5;
+      if (r >= row_lo && r < row_hi && d >= 2 && (hubs || d < 4096))
+        cls = d <= 32 ? 0 : d <= 256 ? 1 : d <= 512 ? 2 : d <= 1024 ? 3 : d <= 2048 ? 4
+            : d < 4096 ? 5 : d <= 16384 ? 6 : 7;
       if (cls >= 0) pos = atomicAdd(&s_cnt[cls], 1);
     }
     __syncthreads();
@@ -1218,15 +1299,32 @@ __global__ void __launch_bounds__(256) k_chunk_classes(const int64_t* __restrict
   }
 }
 
+// Hub runs of the chunk pipeline: [4096, 16384] by k_sort_runs_block_dyn, longer
+// ones by one segmented radix sort per chunk over the listed runs (segments
+// where they lie in `arcs`, the alternate buffer as long as `arcs`; the launch
+// covers nseg = every hub run of the part, the unlisted ones empty).
+struct HubChunkSort {
+  int64_t nseg = 0;
+  int64_t *beg = nullptr, *end = nullptr;
+  int32_t* alt = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  int smem = 0;
+  int nitems = 0;
+};
+using HubSortT = cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 5>;
+
 static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64_t ub,
                            int64_t row_lo, int64_t row_hi, int32_t* lists, int64_t stride,
-                           int* counts, int endbit, int32_t* arcs, int* d_bad) {
+                           int* counts, int endbit, int32_t* arcs, int* d_bad,
+                           const HubChunkSort* hub) {
   cudaStream_t st = e->stream;
   const DevGraph& g = e->g;
   if (ub <= ua) return GS_OK;
   GS_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * kChunkClasses, st));
   k_chunk_classes<<<(unsigned)std::min<int64_t>(grid_for(ub - ua, 256), (int64_t)e->sms * 8), 256,
-                    0, st>>>(d_off, ua, ub, g.rank, row_lo, row_hi, lists, stride, counts);
+                    0, st>>>(d_off, ua, ub, g.rank, row_lo, row_hi, lists, stride, counts,
+                             hub != nullptr);
   auto L = [&](int c) { return RunSet{0, 0, lists + c * stride, counts + c}; };
   const unsigned wg = (unsigned)std::min<int64_t>((ub - ua + 7) / 8, (int64_t)e->sms * 16);
   const unsigned bg = (unsigned)std::min<int64_t>(ub - ua, (int64_t)e->sms * 8);
@@ -1237,6 +1335,25 @@ static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64
   k_sort_runs_block<256, 8><<<bg, 256, 0, st>>>(g.off, L(4), endbit, arcs, d_bad);
   k_sort_runs_block<256, 16><<<bg, 256, 0, st>>>(g.off, L(5), endbit, arcs, d_bad);
   e->launches += 7;
+  if (hub) {
+    k_sort_runs_block_dyn<1024, 16, 5><<<(unsigned)e->sms, 1024, hub->smem, st>>>(
+        g.off, L(6), endbit, arcs, d_bad);
+    e->launches++;
+  }
+  if (hub && hub->nseg > 0) {
+    k_list_segments<<<grid_for(hub->nseg, 256), 256, 0, st>>>(g.off, lists + 7 * stride,
+                                                              counts + 7, hub->nseg, hub->beg,
+                                                              hub->end);
+    cub::DoubleBuffer<int32_t> db(arcs, hub->alt);
+    size_t tb = hub->tb;
+    GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(hub->tmp, tb, db, hub->nitems,
+                                                    (int)hub->nseg, hub->beg, hub->end, 0,
+                                                    bits_for(g.n > 0 ? g.n - 1 : 0), st));
+    k_list_finish<<<(unsigned)e->sms * 2, 256, 0, st>>>(
+        g.off, lists + 7 * stride, counts + 7, db.Current() == arcs ? nullptr : hub->alt, arcs,
+        d_bad);
+    e->launches += 4;
+  }
   GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
@@ -1762,6 +1879,40 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     cudaGetLastError();
   }
   const int endbit = std::min(32, bits_for(n - 1) + 1);
+  // the hub runs (>= 4096) sorted chunk by chunk as well, so that none of the
+  // sorting waits for the last chunk (GS_HUB_CHUNK=0: at the end, as before;
+  // off when the alternate buffer does not fit or the slots exceed an int)
+  HubChunkSort hub;
+  bool hub_chunk = chunk_sort && slots <= INT32_MAX &&
+                   !(getenv("GS_HUB_CHUNK") && atoi(getenv("GS_HUB_CHUNK")) == 0);
+  if (hub_chunk) {
+    hub.nseg = std::max<int64_t>(row_hi - std::max<int64_t>(h_cls[3], row_lo), 0);
+    hub.nitems = (int)slots;
+    hub.smem = (int)sizeof(HubSortT::TempStorage);
+    GS_CUDA(cudaFuncSetAttribute(k_sort_runs_block_dyn<1024, 16, 5>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, hub.smem));
+    if (hub.nseg > 0) {
+      bool ok = e->alloc_n(&hub.beg, hub.nseg) == GS_OK && e->alloc_n(&hub.end, hub.nseg) == GS_OK &&
+                e->alloc_n(&hub.alt, slots) == GS_OK;
+      if (ok) {
+        cub::DoubleBuffer<int32_t> db(arcs, hub.alt);
+        GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, hub.tb, db, hub.nitems,
+                                                        (int)hub.nseg, hub.beg, hub.end, 0,
+                                                        bits_for(n - 1), st));
+        ok = e->alloc(&hub.tmp, hub.tb > 0 ? hub.tb : 1) == GS_OK;
+      }
+      if (!ok) {
+        hub_chunk = false;
+        cudaGetLastError();
+      }
+    }
+  }
+  auto release_hub = [&]() {
+    for (void* p : {(void*)hub.beg, (void*)hub.end, (void*)hub.alt, hub.tmp})
+      if (p) e->release(p);
+    hub = HubChunkSort();
+  };
+  if (!hub_chunk) release_hub();
   for (int64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
@@ -1782,10 +1933,12 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     if (next < nchunks) GS_TRY(issue(next++));
     if (chunk_sort)
       GS_TRY(sort_chunk_runs(e, d_off, done[c], done[c + 1], row_lo, row_hi, clists,
-                             std::max<int64_t>(maxv, 1), ccounts, endbit, arcs, d_bad));
+                             std::max<int64_t>(maxv, 1), ccounts, endbit, arcs, d_bad,
+                             hub_chunk ? &hub : nullptr));
   }
   e->release(clists);
   e->release(ccounts);
+  release_hub();
   GS_CUDA(cudaGetLastError());
   GS_CUDA(cudaStreamSynchronize(cs));
   for (int k = 0; k < nring; ++k) e->release(ring[k]);
@@ -1794,7 +1947,8 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     cudaEventDestroy(copied[k]);
     cudaEventDestroy(freed[k]);
   }
-  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, chunk_sort);
+  return finish_part(e, n, m, arcs, h_cls, d_bad, row_lo, row_hi, part_world > 1, chunk_sort,
+                     hub_chunk);
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ d, int64_t n, int64_t* __restrict__ o) {

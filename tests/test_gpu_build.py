@@ -87,6 +87,61 @@ def test_host_csr_many_chunks(orc, chunk_env, chunk, scale):
     np.testing.assert_array_equal(got[1], cl)
 
 
+def _hub_graph(seed=5):
+    """Hub runs on both sides of 16384 (the chunk pipeline's CTA sort and its
+    segmented sort), spread over many chunks, on a sparse background."""
+    rng = np.random.default_rng(seed)
+    n = 60000
+    edges = set()
+    for _ in range(80000):
+        u, v = rng.integers(0, n, size=2)
+        if u != v:
+            edges.add((int(min(u, v)), int(max(u, v))))
+    for k, d in enumerate((4096, 6000, 16384, 16385, 21000, 40000)):
+        c = 1000 * (k + 1) + 7
+        for v in rng.choice(np.arange(0, n), size=d, replace=False):
+            if v != c:
+                edges.add((int(min(c, v)), int(max(c, v))))
+    return n, np.array(sorted(edges), dtype=np.int32)
+
+
+@pytest.mark.parametrize("hub_chunk", ["1", "0"])
+@pytest.mark.parametrize("chunk", [4093, 1 << 15])
+def test_host_csr_hub_runs_sorted_chunk_by_chunk(orc, chunk_env, monkeypatch, chunk, hub_chunk):
+    """Runs >= 4096 sorted as their last chunk lands (GS_HUB_CHUNK=1, default)
+    or at the end (0): the same graph and clustering as the oracle."""
+    n, e = _hub_graph()
+    c = orc.CSR(n, e)
+    g = make_graph(n, e)
+    monkeypatch.setenv("GS_HUB_CHUNK", hub_chunk)
+    os.environ["GS_H2D_CHUNK"] = str(chunk)
+    for eps, mu in (("0.2", 3), ("0.5", 5)):
+        roles, cl = orc.serial_scan(c, mu, eps)
+        got = _run(g, mu, eps)
+        np.testing.assert_array_equal(got[0], roles, err_msg=f"{eps} {mu}")
+        np.testing.assert_array_equal(got[1], cl, err_msg=f"{eps} {mu}")
+
+
+@pytest.mark.parametrize("victim", [2007, 4007, 6007])  # degrees 6000, 16385, 40000
+def test_host_csr_bad_hub_run_detected(chunk_env, victim):
+    n, e = _hub_graph()
+    g = make_graph(n, e)
+    off = np.asarray(g.vertex_offsets).copy()
+    lo, hi = int(off[victim]), int(off[victim + 1])
+    assert hi - lo >= 6000
+    os.environ["GS_H2D_CHUNK"] = "4093"
+    for how in ("swap", "dup"):
+        adj = np.asarray(g.adjacency).copy()
+        mid = (lo + hi) // 2
+        if how == "swap":
+            adj[mid], adj[mid + 1] = adj[mid + 1], adj[mid]
+        else:
+            adj[mid + 1] = adj[mid]
+        bad = _csr(n, [adj[off[v]:off[v + 1]] for v in range(n)])
+        with pytest.raises(ValueError):
+            gs.scan_in_memory(bad, 3, "0.5")
+
+
 def _csr(n, runs):
     off = np.zeros(n + 1, np.int64)
     off[1:] = np.cumsum([len(r) for r in runs])
