@@ -1311,6 +1311,7 @@ struct HubChunkSort {
   size_t tb = 0;
   int smem = 0;
   int nitems = 0;
+  int bits = 0;  // key bits (rank ids of the n vertices)
 };
 using HubSortT = cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 5>;
 
@@ -1348,7 +1349,7 @@ static int sort_chunk_runs(gs_engine* e, const int64_t* d_off, int64_t ua, int64
     size_t tb = hub->tb;
     GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(hub->tmp, tb, db, hub->nitems,
                                                     (int)hub->nseg, hub->beg, hub->end, 0,
-                                                    bits_for(g.n > 0 ? g.n - 1 : 0), st));
+                                                    hub->bits, st));
     k_list_finish<<<(unsigned)e->sms * 2, 256, 0, st>>>(
         g.off, lists + 7 * stride, counts + 7, db.Current() == arcs ? nullptr : hub->alt, arcs,
         d_bad);
@@ -1888,6 +1889,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
   if (hub_chunk) {
     hub.nseg = std::max<int64_t>(row_hi - std::max<int64_t>(h_cls[3], row_lo), 0);
     hub.nitems = (int)slots;
+    hub.bits = bits_for(n - 1);
     hub.smem = (int)sizeof(HubSortT::TempStorage);
     GS_CUDA(cudaFuncSetAttribute(k_sort_runs_block_dyn<1024, 16, 5>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, hub.smem));
@@ -1898,7 +1900,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
         cub::DoubleBuffer<int32_t> db(arcs, hub.alt);
         GS_CUDA(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, hub.tb, db, hub.nitems,
                                                         (int)hub.nseg, hub.beg, hub.end, 0,
-                                                        bits_for(n - 1), st));
+                                                        hub.bits, st));
         ok = e->alloc(&hub.tmp, hub.tb > 0 ? hub.tb : 1) == GS_OK;
       }
       if (!ok) {
