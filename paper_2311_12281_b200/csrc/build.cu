@@ -1915,6 +1915,17 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     hub = HubChunkSort();
   };
   if (!hub_chunk) release_hub();
+  // the sketch rows (sketch.cu) of every run a chunk completes, built while
+  // later chunks are in flight, at the resolution of eps >= 0.33 (k = 4,
+  // rows from degree 32; a scan at another resolution rebuilds them).  Needs
+  // every run listed (hub_chunk); GS_SK_STREAM=0: built by the scan.
+  constexpr int kSkLk = 2;
+  constexpr int64_t kSkDmin = 32;
+  int32_t* sk_rdeg = nullptr;
+  const int64_t dmax_b = h_cls[DevGraph::kClasses];
+  if (hub_chunk && part_world == 1 &&
+      !(getenv("GS_SK_STREAM") && atoi(getenv("GS_SK_STREAM")) == 0))
+    GS_TRY(sketch_stream_begin(e, n, dmax_b, kSkLk, kSkDmin, &sk_rdeg));
   for (int64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c % kSlots);
     const int64_t i0 = c * kChunk, len = std::min<int64_t>(kChunk, slots - i0);
@@ -1937,6 +1948,15 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
       GS_TRY(sort_chunk_runs(e, d_off, done[c], done[c + 1], row_lo, row_hi, clists,
                              std::max<int64_t>(maxv, 1), ccounts, endbit, arcs, d_bad,
                              hub_chunk ? &hub : nullptr));
+    if (sk_rdeg)
+      GS_TRY(sketch_stream_rows(e, dmax_b, kSkLk, kSkDmin, sk_rdeg, arcs, clists,
+                                std::max<int64_t>(maxv, 1), ccounts, 0, kChunkClasses,
+                                done[c + 1] - done[c]));
+  }
+  if (sk_rdeg) {
+    e->release(sk_rdeg);
+    g.sk_lk = kSkLk;
+    g.sk_dmin = kSkDmin;
   }
   e->release(clists);
   e->release(ccounts);

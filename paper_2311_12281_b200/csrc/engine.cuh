@@ -247,6 +247,12 @@ int run_prepass(gs_engine* e, int32_t mu);  // O(1)-decided edges -> initial bou
 // sketch.cu: neighbourhood sketches for the exact dissimilarity bound (needs
 // the per-scan rdeg table); lk < 0 releases them
 int build_sketch(gs_engine* e, int lk, int64_t dmin);
+// sketch rows built while a host CSR streams in (sketch.cu)
+int sketch_stream_begin(gs_engine* e, int64_t n, int64_t dmax, int lk, int64_t dmin,
+                        int32_t** rdeg_out);
+int sketch_stream_rows(gs_engine* e, int64_t dmax, int lk, int64_t dmin, const int32_t* rdeg,
+                       const int32_t* adj, const int32_t* lists, int64_t stride,
+                       const int* counts, int c0, int c1, int64_t nlisted);
 // cluster.cu: the scan as phases (single GPU: all of them in a row; sharded:
 // the host layer runs the collectives between them, see dist.py)
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,

@@ -97,39 +97,107 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
   }
 }
 
-// CTA per vertex: shared memory up to smem_words, global atomics beyond
+// the row of vertex v by a CTA: shared memory up to smem_words, global atomics beyond
+__device__ __forceinline__ void sk_cta_row(const int64_t* __restrict__ off,
+                                           const int32_t* __restrict__ adj, int64_t v,
+                                           const int32_t* __restrict__ rdeg,
+                                           const int64_t* __restrict__ skbase, int lk,
+                                           uint32_t* __restrict__ sk, uint32_t* s,
+                                           int64_t smem_words) {
+  const int64_t o = off[v], d = off[v + 1] - o;
+  const int64_t W = sk_words(d, lk);
+  const uint32_t mask = (uint32_t)(W * 32 - 1);
+  uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
+  const bool in_smem = W <= smem_words;
+  uint32_t* t = in_smem ? s : out;
+  for (int64_t j = threadIdx.x; j < W; j += blockDim.x) t[j] = 0u;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+    const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+    atomicOr(&t[h >> 5], 1u << (h & 31));
+  }
+  __syncthreads();
+  if (in_smem) {
+    sk_fold_levels(s, W, threadIdx.x, blockDim.x, [] { __syncthreads(); });
+    for (int64_t j = threadIdx.x; j < 2 * W - 4; j += blockDim.x) out[j] = s[j];
+  } else {  // level 0 was built with global atomics (at L2): fold through L2
+    for (int64_t lo = 0, w = W; w > 4; lo += w, w >>= 1) {
+      const int64_t h = w >> 1;
+      for (int64_t i = threadIdx.x; i < h; i += blockDim.x)
+        out[lo + w + i] = __ldcg(out + lo + i) | __ldcg(out + lo + h + i);
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+}
+
+// CTA per vertex of the rank range [r0, r1)
 __global__ void __launch_bounds__(512) k_sk_cta(const int64_t* __restrict__ off,
                                                 const int32_t* __restrict__ adj, int64_t r0,
                                                 int64_t r1, const int32_t* __restrict__ rdeg,
                                                 const int64_t* __restrict__ skbase, int lk,
                                                 uint32_t* __restrict__ sk, int64_t smem_words) {
   extern __shared__ uint32_t s[];  // [2 * smem_words]
-  for (int64_t v = r0 + blockIdx.x; v < r1; v += gridDim.x) {
-    const int64_t o = off[v], d = off[v + 1] - o;
-    const int64_t W = sk_words(d, lk);
-    const uint32_t mask = (uint32_t)(W * 32 - 1);
-    uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
-    const bool in_smem = W <= smem_words;
-    uint32_t* t = in_smem ? s : out;
-    for (int64_t j = threadIdx.x; j < W; j += blockDim.x) t[j] = 0u;
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-      const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-      atomicOr(&t[h >> 5], 1u << (h & 31));
-    }
-    __syncthreads();
-    if (in_smem) {
-      sk_fold_levels(s, W, threadIdx.x, blockDim.x, [] { __syncthreads(); });
-      for (int64_t j = threadIdx.x; j < 2 * W - 4; j += blockDim.x) out[j] = s[j];
-    } else {  // level 0 was built with global atomics (at L2): fold through L2
-      for (int64_t lo = 0, w = W; w > 4; lo += w, w >>= 1) {
-        const int64_t h = w >> 1;
-        for (int64_t i = threadIdx.x; i < h; i += blockDim.x)
-          out[lo + w + i] = __ldcg(out + lo + i) | __ldcg(out + lo + h + i);
-        __syncthreads();
+  for (int64_t v = r0 + blockIdx.x; v < r1; v += gridDim.x)
+    sk_cta_row(off, adj, v, rdeg, skbase, lk, sk, s, smem_words);
+}
+
+// Rows of listed ranks (the host-CSR chunk pipeline: the runs a chunk
+// completed, in its sort-class lists [c0, c1), stride apart), those of degree
+// in [dlo, dhi]: a warp per row (WARP, rows of <= 2 * WMAX words with the
+// levels) or a CTA per row
+template <bool WARP, int NT, int WMAX>
+__global__ void __launch_bounds__(NT) k_sk_list(const int64_t* __restrict__ off,
+                                                const int32_t* __restrict__ adj,
+                                                const int32_t* __restrict__ lists, int64_t stride,
+                                                const int* __restrict__ counts, int c0, int c1,
+                                                int64_t dlo, int64_t dhi,
+                                                const int32_t* __restrict__ rdeg,
+                                                const int64_t* __restrict__ skbase, int lk,
+                                                uint32_t* __restrict__ sk, int64_t smem_words) {
+  extern __shared__ uint32_t dyn[];
+  const int64_t g0 = WARP ? (blockIdx.x * (int64_t)NT + threadIdx.x) >> 5 : blockIdx.x;
+  const int64_t ng = WARP ? ((int64_t)gridDim.x * NT) >> 5 : gridDim.x;
+  const int lane = threadIdx.x & 31;
+  uint32_t* s = WARP ? dyn + (threadIdx.x >> 5) * 2 * WMAX : dyn;
+  for (int c = c0; c < c1; ++c) {
+    const int64_t cnt = counts[c];
+    for (int64_t j = g0; j < cnt; j += ng) {
+      const int64_t v = lists[c * stride + j];
+      const int64_t o = off[v], d = off[v + 1] - o;
+      if (d < dlo || d > dhi) continue;  // uniform over the warp / CTA
+      if (!WARP) {
+        sk_cta_row(off, adj, v, rdeg, skbase, lk, sk, s, smem_words);
+        continue;
       }
+      const int64_t W = sk_words(d, lk);
+      const uint32_t mask = (uint32_t)(W * 32 - 1);
+      for (int64_t k = lane; k < W; k += 32) s[k] = 0u;
+      __syncwarp();
+      for (int64_t i = lane; i < d; i += 32) {
+        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
+        atomicOr(&s[h >> 5], 1u << (h & 31));
+      }
+      __syncwarp();
+      sk_fold_levels(s, W, lane, 32);
+      uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
+      for (int64_t k = lane; k < 2 * W - 4; k += 32) out[k] = s[k];
+      __syncwarp();
     }
-    __syncthreads();
+  }
+}
+
+// rdeg[d] = first rank of degree >= d (d in [0, dmax + 2]), as k_degree_tables
+__global__ void k_sk_rdeg(const int64_t* __restrict__ off, int64_t n, int64_t dmax,
+                          int32_t* __restrict__ rdeg) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d <= dmax + 2;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid + 1] - off[mid] < d) lo = mid + 1; else hi = mid;
+    }
+    rdeg[d] = (int32_t)lo;
   }
 }
 
@@ -236,6 +304,76 @@ int build_sketch(gs_engine* e, int lk, int64_t dmin) {
   GS_CUDA(cudaGetLastError());
   g.sk_lk = lk;
   g.sk_dmin = dmin;
+  return GS_OK;
+}
+
+// --- rows built while the graph streams in (host-CSR chunk pipeline) -------
+// The layout of build_sketch at resolution lk (the rank-space offsets exist,
+// the runs do not yet): rdeg (returned, the caller releases it), skbase and
+// the rows' buffer.  Leaves g.sk null when there is no room (HBM cap).
+int sketch_stream_begin(gs_engine* e, int64_t n, int64_t dmax, int lk, int64_t dmin,
+                        int32_t** rdeg_out) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  *rdeg_out = nullptr;
+  if (n == 0 || dmax < dmin) return GS_OK;
+  int32_t* rdeg = nullptr;
+  int64_t* sizes = nullptr;
+  GS_TRY(e->alloc_n(&rdeg, dmax + 3));
+  GS_TRY(e->alloc_n(&sizes, dmax + 2));
+  GS_TRY(e->alloc_n(&g.skbase, dmax + 2));
+  k_sk_rdeg<<<grid_for(dmax + 3, 256), 256, 0, st>>>(g.off, n, dmax, rdeg);
+  k_sk_sizes<<<grid_for(dmax + 2, 256), 256, 0, st>>>(dmax, dmin, lk, rdeg, sizes);
+  size_t tb = 0;
+  GS_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, sizes, g.skbase, dmax + 2, st));
+  void* tmp = nullptr;
+  GS_TRY(e->alloc(&tmp, tb > 0 ? tb : 1));
+  GS_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, sizes, g.skbase, dmax + 2, st));
+  e->launches += 3;
+  e->release(tmp);
+  e->release(sizes);
+  int64_t total = 0;
+  GS_CUDA(cudaMemcpyAsync(&total, g.skbase + dmax + 1, sizeof(total), cudaMemcpyDeviceToHost, st));
+  GS_CUDA(cudaStreamSynchronize(st));
+  if (e->alloc_n(&g.sk, std::max<int64_t>(total, 1)) != GS_OK) {
+    cudaGetLastError();
+    e->release(g.skbase);
+    g.skbase = nullptr;
+    e->release(rdeg);
+    return GS_OK;
+  }
+  *rdeg_out = rdeg;
+  return GS_OK;
+}
+
+// rows of the runs listed in [c0, c1) of a chunk's class lists (runs complete,
+// in any order: a row is a set)
+int sketch_stream_rows(gs_engine* e, int64_t dmax, int lk, int64_t dmin, const int32_t* rdeg,
+                       const int32_t* adj, const int32_t* lists, int64_t stride,
+                       const int* counts, int c0, int c1, int64_t nlisted) {
+  DevGraph& g = e->g;
+  cudaStream_t st = e->stream;
+  if (!g.sk || nlisted == 0) return GS_OK;
+  constexpr int NT = 256, WMAX = 256;
+  const int64_t dsplit = (int64_t)WMAX * 32 >> lk, dsplit2 = (int64_t)2048 * 32 >> lk;
+  const unsigned wg = (unsigned)std::min<int64_t>((nlisted + 7) / 8, (int64_t)e->sms * 8);
+  k_sk_list<true, NT, WMAX><<<wg, NT, (NT / 32) * 2 * WMAX * 4, st>>>(
+      g.off, adj, lists, stride, counts, c0, c1, dmin, dsplit, rdeg, g.skbase, lk, g.sk, 0);
+  const unsigned cg = (unsigned)std::min<int64_t>(nlisted, (int64_t)e->sms * 8);
+  k_sk_list<false, NT, WMAX><<<cg, NT, 2048 * 8, st>>>(g.off, adj, lists, stride, counts, c0,
+                                                         c1, std::max(dmin, dsplit + 1), dsplit2,
+                                                         rdeg, g.skbase, lk, g.sk, 2048);
+  if (dmax > dsplit2) {
+    const int64_t smem_words = std::min<int64_t>(16384, sk_words(dmax, lk));
+    auto kern = k_sk_list<false, 512, WMAX>;
+    GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(smem_words * 8)));
+    kern<<<(unsigned)std::min<int64_t>(nlisted, (int64_t)e->sms * 2), 512, smem_words * 8, st>>>(
+        g.off, adj, lists, stride, counts, c0, c1, std::max(dmin, dsplit2 + 1), dmax, rdeg,
+        g.skbase, lk, g.sk, smem_words);
+  }
+  e->launches += 3;
+  GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
 

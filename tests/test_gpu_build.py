@@ -122,6 +122,29 @@ def test_host_csr_hub_runs_sorted_chunk_by_chunk(orc, chunk_env, monkeypatch, ch
         np.testing.assert_array_equal(got[1], cl, err_msg=f"{eps} {mu}")
 
 
+@pytest.mark.parametrize("chunk", [4093, 1 << 15])
+def test_host_csr_streamed_sketch_rows_equal_the_scan_built_ones(orc, chunk_env, monkeypatch,
+                                                                  chunk):
+    """Sketch rows built chunk by chunk while the CSR streams in (GS_SK_STREAM=1)
+    decide exactly the edges the scan-built rows decide (same counters), and
+    the clustering equals the oracle's."""
+    n, e = _hub_graph()
+    g = make_graph(n, e)
+    os.environ["GS_H2D_CHUNK"] = str(chunk)
+    for eps, mu in (("0.5", 5), ("0.35", 3), ("0.2", 3)):  # 0.2: k = 8, rebuilt by the scan
+        out = {}
+        for flag in ("1", "0"):
+            monkeypatch.setenv("GS_SK_STREAM", flag)
+            r, st = gs.scan_in_memory(g, mu, eps)
+            out[flag] = (r.role_codes.copy(), r.cluster_ids.copy(),
+                         st.extra["sim_decided_by_sketch"], st.sim_evals)
+        assert out["1"][2] == out["0"][2] and out["1"][3] == out["0"][3], eps
+        roles, cl = orc.serial_scan(orc.CSR(n, e), mu, eps)
+        for flag in ("1", "0"):
+            np.testing.assert_array_equal(out[flag][0], roles)
+            np.testing.assert_array_equal(out[flag][1], cl)
+
+
 @pytest.mark.parametrize("victim", [2007, 4007, 6007])  # degrees 6000, 16385, 40000
 def test_host_csr_bad_hub_run_detected(chunk_env, victim):
     n, e = _hub_graph()
