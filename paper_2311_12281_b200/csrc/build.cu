@@ -1950,8 +1950,7 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
                              hub_chunk ? &hub : nullptr));
     if (sk_rdeg)
       GS_TRY(sketch_stream_rows(e, dmax_b, kSkLk, kSkDmin, sk_rdeg, arcs, clists,
-                                std::max<int64_t>(maxv, 1), ccounts, 0, kChunkClasses,
-                                done[c + 1] - done[c]));
+                                std::max<int64_t>(maxv, 1), ccounts, done[c + 1] - done[c]));
   }
   if (sk_rdeg) {
     e->release(sk_rdeg);

@@ -528,6 +528,9 @@ __global__ void k_core_list(int64_t n, const uint8_t* __restrict__ role,
 // union over the core-core edges: warp per core c, the cores w < c of its run
 // (c is their high endpoint: e = eoff[c] + i); known-similar edges union, an
 // unknown one is decided unless both ends already share a root (scan.py:601-660)
+// (DECIDE false: the known-similar unions only -- the dense path, whose class
+// kernels decide the unknown edges after it)
+template <bool DECIDE>
 __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
                                const int32_t* __restrict__ ipre,
                                const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
@@ -553,7 +556,7 @@ __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __
         if (role[w] == ROLE_CORE) st = sim[e0 + i];
       }
       if (st == SIM_SIMILAR) uf_union(parent, w, c, retries);
-      uint32_t mask = __ballot_sync(0xffffffffu, st == SIM_UNKNOWN);
+      uint32_t mask = DECIDE ? __ballot_sync(0xffffffffu, st == SIM_UNKNOWN) : 0u;
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -584,6 +587,9 @@ __global__ void k_union_sparse(const int* __restrict__ ncores, const int32_t* __
 // attach over the core / non-core edges: warp per core c, every non-core
 // neighbour w (e = eoff[high] + position of low in high's run); similar ->
 // w's member labels take c's canonical label (scan.py:662-698)
+// (DECIDE false: the known-similar edges only, after the dense path's class
+// kernels decided the rest)
+template <bool DECIDE>
 __global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
                                 const int32_t* __restrict__ ipre,
                                 const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
@@ -619,7 +625,7 @@ __global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* _
         atomicMin(&lmin[w], L);
         atomicMax(&lmax[w], L);
       }
-      uint32_t mask = __ballot_sync(0xffffffffu, st == SIM_UNKNOWN);
+      uint32_t mask = DECIDE ? __ballot_sync(0xffffffffu, st == SIM_UNKNOWN) : 0u;
       while (mask) {
         const int src = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -646,6 +652,23 @@ __global__ void k_attach_sparse(const int* __restrict__ ncores, const int32_t* _
     atomicAdd(&ctr[CTR_INTERSECTIONS], evals);
   }
   if (lane == 0 && probes) atomicAdd(&ctr[CTR_PROBES], probes);
+}
+
+// flag[w] = 1 for every neighbour w of a listed core (32-arc items of the
+// whole runs): the dense attach pass's core-adjacency marks from the core list
+__global__ void k_flag_list(const int* __restrict__ ncores, const int32_t* __restrict__ clist,
+                            const int32_t* __restrict__ ipre, const int64_t* __restrict__ off,
+                            const int32_t* __restrict__ adj, uint8_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nc = *ncores;
+  const int64_t items = nc > 0 ? ipre[nc - 1] : 0;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; it < items; it += nw) {
+    int64_t base = 0;
+    const int32_t c = clist[item_entry(ipre, nc, it, base)];
+    const int64_t i = base + lane, oc = off[c];
+    if (i < off[c + 1] - oc) flag[adj[oc + i]] = 1;
+  }
 }
 
 // classification from the clustered side: the clustered vertices (lmax >= 0)
@@ -814,7 +837,7 @@ int phase_union(gs_engine* e) {
   if (s.sparse) {
     int32_t* ipre = nullptr;
     GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, true, &ipre));
-    k_union_sparse<<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off, g.adj,
+    k_union_sparse<true><<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off, g.adj,
                                                                 g.eoff, s.thr, e->eps, s.sim,
                                                                 s.role, s.parent, s.ctr);
     e->launches++;
@@ -822,7 +845,15 @@ int phase_union(gs_engine* e) {
     GS_CUDA(cudaGetLastError());
     return GS_OK;
   }
-  if (g.m > 0) {
+  if (g.m > 0 && s.clist) {  // known-similar core-core unions from the core list
+    int32_t* ipre = nullptr;
+    GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, true, &ipre));
+    k_union_sparse<false><<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(
+        s.lcnt, s.clist, ipre, g.off, g.adj, g.eoff, s.thr, e->eps, s.sim, s.role, s.parent,
+        s.ctr);
+    e->launches++;
+    e->release(ipre);
+  } else if (g.m > 0) {  // ... or by a sweep over every edge (sharded, or GS_SPARSE_CLUSTER=0)
     GS_TRY(ensure_endpoints(e));
     k_union_known<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.parent,
                                                        s.ctr, e->shard_rank, e->shard_world);
@@ -935,7 +966,7 @@ int phase_attach(gs_engine* e) {
   if (s.sparse) {
     int32_t* ipre = nullptr;
     GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, false, &ipre));
-    k_attach_sparse<<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off,
+    k_attach_sparse<true><<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off,
                                                                  g.adj, g.eoff, s.thr, e->eps,
                                                                  s.sim, s.role, s.lmin, s.lmax,
                                                                  s.ctr);
@@ -946,9 +977,26 @@ int phase_attach(gs_engine* e) {
   }
   if (!s.coreadj) GS_TRY(e->alloc_n(&s.coreadj, (g.n + 3) & ~int64_t(3)));
   GS_CUDA(cudaMemsetAsync(s.coreadj, 0, (size_t)(g.n > 0 ? g.n : 1), e->stream));
-  if (g.n > 0) flag_neighbours<true>(e, s.coreadj);
+  // with the core list (single GPU): the cores' neighbours flagged and the
+  // known-similar edges attached from the cores' runs instead of sweeping
+  // every vertex / every edge
+  int32_t* ipre = nullptr;
+  if (g.m > 0 && s.clist) {
+    GS_TRY(list_chunks(e, (int64_t)e->ncores, s.lcnt, s.clist, false, &ipre));
+    k_flag_list<<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(s.lcnt, s.clist, ipre, g.off, g.adj,
+                                                             s.coreadj);
+    e->launches++;
+  } else if (g.n > 0) {
+    flag_neighbours<true>(e, s.coreadj);
+  }
   GS_TRY(run_similarity(e, MODE_ATTACH, e->eps, e->mu));
-  if (g.m > 0) {
+  if (ipre) {
+    k_attach_sparse<false><<<(unsigned)e->sms * 16, 256, 0, e->stream>>>(
+        s.lcnt, s.clist, ipre, g.off, g.adj, g.eoff, s.thr, e->eps, s.sim, s.role, s.lmin, s.lmax,
+        s.ctr);
+    e->launches++;
+    e->release(ipre);
+  } else if (g.m > 0) {
     GS_TRY(ensure_endpoints(e));
     k_attach<<<gridv(e, g.m), 256, 0, e->stream>>>(g.m, g.elo, g.ehi, s.sim, s.role, s.lmin, s.lmax,
                                                   e->shard_rank, e->shard_world);

@@ -252,7 +252,7 @@ int sketch_stream_begin(gs_engine* e, int64_t n, int64_t dmax, int lk, int64_t d
                         int32_t** rdeg_out);
 int sketch_stream_rows(gs_engine* e, int64_t dmax, int lk, int64_t dmin, const int32_t* rdeg,
                        const int32_t* adj, const int32_t* lists, int64_t stride,
-                       const int* counts, int c0, int c1, int64_t nlisted);
+                       const int* counts, int64_t nlisted);
 // cluster.cu: the scan as phases (single GPU: all of them in a row; sharded:
 // the host layer runs the collectives between them, see dist.py)
 int run_scan(gs_engine* e, int32_t mu, const Eps2& eps, uint8_t* role_out,

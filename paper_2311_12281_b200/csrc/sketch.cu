@@ -348,31 +348,38 @@ int sketch_stream_begin(gs_engine* e, int64_t n, int64_t dmax, int lk, int64_t d
 
 // rows of the runs listed in [c0, c1) of a chunk's class lists (runs complete,
 // in any order: a row is a set)
+//
+// The chunk's lists are its sort classes (build.cu k_chunk_classes: <= 32,
+// <= 256, <= 512, <= 1024, <= 2048, < 4096, <= 16384, longer); at k = 4 the
+// warp rows (<= 2048 neighbours) are classes 0-4, the 2048-word CTA rows
+// classes 5-6 and the long rows class 7, so each kernel walks only its own
+// lists (every kernel still filters by degree).
 int sketch_stream_rows(gs_engine* e, int64_t dmax, int lk, int64_t dmin, const int32_t* rdeg,
                        const int32_t* adj, const int32_t* lists, int64_t stride,
-                       const int* counts, int c0, int c1, int64_t nlisted) {
+                       const int* counts, int64_t nlisted) {
   DevGraph& g = e->g;
   cudaStream_t st = e->stream;
   if (!g.sk || nlisted == 0) return GS_OK;
+  if (lk != 2) { set_error("streamed sketch rows are built at k = 4 only"); return GS_EINVAL; }
   constexpr int NT = 256, WMAX = 256;
   const int64_t dsplit = (int64_t)WMAX * 32 >> lk, dsplit2 = (int64_t)2048 * 32 >> lk;
   const unsigned wg = (unsigned)std::min<int64_t>((nlisted + 7) / 8, (int64_t)e->sms * 8);
   k_sk_list<true, NT, WMAX><<<wg, NT, (NT / 32) * 2 * WMAX * 4, st>>>(
-      g.off, adj, lists, stride, counts, c0, c1, dmin, dsplit, rdeg, g.skbase, lk, g.sk, 0);
-  const unsigned cg = (unsigned)std::min<int64_t>(nlisted, (int64_t)e->sms * 8);
-  k_sk_list<false, NT, WMAX><<<cg, NT, 2048 * 8, st>>>(g.off, adj, lists, stride, counts, c0,
-                                                         c1, std::max(dmin, dsplit + 1), dsplit2,
-                                                         rdeg, g.skbase, lk, g.sk, 2048);
+      g.off, adj, lists, stride, counts, 0, 5, dmin, dsplit, rdeg, g.skbase, lk, g.sk, 0);
+  k_sk_list<false, NT, WMAX><<<(unsigned)e->sms * 2, NT, 2048 * 8, st>>>(
+      g.off, adj, lists, stride, counts, 5, 7, std::max(dmin, dsplit + 1), dsplit2, rdeg,
+      g.skbase, lk, g.sk, 2048);
+  e->launches += 2;
   if (dmax > dsplit2) {
     const int64_t smem_words = std::min<int64_t>(16384, sk_words(dmax, lk));
     auto kern = k_sk_list<false, 512, WMAX>;
     GS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(smem_words * 8)));
-    kern<<<(unsigned)std::min<int64_t>(nlisted, (int64_t)e->sms * 2), 512, smem_words * 8, st>>>(
-        g.off, adj, lists, stride, counts, c0, c1, std::max(dmin, dsplit2 + 1), dmax, rdeg,
+    kern<<<(unsigned)e->sms, 512, smem_words * 8, st>>>(
+        g.off, adj, lists, stride, counts, 7, 8, std::max(dmin, dsplit2 + 1), dmax, rdeg,
         g.skbase, lk, g.sk, smem_words);
+    e->launches++;
   }
-  e->launches += 3;
   GS_CUDA(cudaGetLastError());
   return GS_OK;
 }
