@@ -915,6 +915,17 @@ __global__ void k_p1_bounds(const int32_t* __restrict__ list, const int* __restr
   if (t == 4) cls[4] = cnt;
 }
 
+// union / attach: the b's whose owned edges can need a decision (b_needed)
+struct NeedB {
+  const uint8_t* role;
+  const uint8_t* coreadj;
+  int mode, rank, world;
+  __device__ bool operator()(int32_t b) const {
+    if (!owns(b, rank, world)) return false;
+    return role[b] == ROLE_CORE || (mode == MODE_ATTACH && coreadj[b]);
+  }
+};
+
 struct HasPending {
   const int32_t* pend;
   int64_t lo;
@@ -1308,6 +1319,27 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
       e->launches += 2;
       P.p1_list = p1_list;
     }
+  }
+  // union / attach: the class launches claim only the b's that can need a
+  // decision (cores; for attach also the cores' neighbours), listed
+  // ascending and sliced per class like stage 2's list, instead of claiming
+  // every b of their class from one work counter (GS_CLUSTER_LIST=0)
+  static const bool clu_list = !(getenv("GS_CLUSTER_LIST") && atoi(getenv("GS_CLUSTER_LIST")) == 0);
+  if (!ident && clu_list && (mode == MODE_UNION || mode == MODE_ATTACH) && g.n > rc[1]) {
+    const int64_t lo = rc[1], nb = g.n - lo;
+    GS_TRY(e->alloc_n(&p1_list, nb));
+    GS_TRY(e->alloc_n(&p1_cls, 8));
+    size_t tb2 = 0;
+    thrust::counting_iterator<int32_t> it((int32_t)lo);
+    const NeedB pred{s.role, s.coreadj, mode, e->shard_rank, e->shard_world};
+    GS_CUDA(cub::DeviceSelect::If(nullptr, tb2, it, p1_list, p1_cls + 5, (int)nb, pred, e->stream));
+    void* t2 = nullptr;
+    GS_TRY(e->alloc(&t2, tb2 > 0 ? tb2 : 1));
+    GS_CUDA(cub::DeviceSelect::If(t2, tb2, it, p1_list, p1_cls + 5, (int)nb, pred, e->stream));
+    e->release(t2);
+    k_p1_bounds<<<1, 32, 0, e->stream>>>(p1_list, p1_cls + 5, rc[1], rc[2], rc[3], rc[4], p1_cls);
+    e->launches += 2;
+    P.p1_list = p1_list;
   }
   if (ident) e->kev_mark(3);
   // huge b first (longest work items), with an L2-resident table per CTA
