@@ -1915,16 +1915,18 @@ int build_from_csr_host(gs_engine* e, int64_t n, int64_t m, const int64_t* off_h
     hub = HubChunkSort();
   };
   if (!hub_chunk) release_hub();
-  // the sketch rows (sketch.cu) of every run a chunk completes, built while
-  // later chunks are in flight, at the resolution of eps >= 0.33 (k = 4,
-  // rows from degree 32; a scan at another resolution rebuilds them).  Needs
-  // every run listed (hub_chunk); GS_SK_STREAM=0: built by the scan.
+  // GS_SK_STREAM=1: the sketch rows (sketch.cu) of every run a chunk
+  // completes, built while later chunks are in flight, at the resolution of
+  // eps >= 0.33 (k = 4, rows from degree 32; a scan at another resolution
+  // rebuilds them).  Needs every run listed (hub_chunk).  Measured and off by
+  // default: the chunk pipeline is not idle enough to hide them (s24 e2e from
+  // the pinned host CSR 58.2 -> 60.9 ms, the scan's prep 2.2 ms shorter).
   constexpr int kSkLk = 2;
   constexpr int64_t kSkDmin = 32;
   int32_t* sk_rdeg = nullptr;
   const int64_t dmax_b = h_cls[DevGraph::kClasses];
   if (hub_chunk && part_world == 1 &&
-      !(getenv("GS_SK_STREAM") && atoi(getenv("GS_SK_STREAM")) == 0))
+      getenv("GS_SK_STREAM") && atoi(getenv("GS_SK_STREAM")) == 1)
     GS_TRY(sketch_stream_begin(e, n, dmax_b, kSkLk, kSkDmin, &sk_rdeg));
   for (int64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c % kSlots);

@@ -29,8 +29,8 @@ VARIANTS = {
     "dense_cluster_forced": {"GS_SPARSE_CLUSTER": "0"},
     "cluster_no_b_list": {"GS_CLUSTER_LIST": "0"},
     "hub_runs_at_end": {"GS_HUB_CHUNK": "0", "GS_H2D_CHUNK": "65536"},
-    "sketch_built_by_scan": {"GS_SK_STREAM": "0", "GS_H2D_CHUNK": "65536"},
-    "sketch_streamed_small_chunks": {"GS_H2D_CHUNK": "65536"},
+    "sketch_streamed_small_chunks": {"GS_SK_STREAM": "1", "GS_H2D_CHUNK": "65536"},
+    "small_chunks": {"GS_H2D_CHUNK": "65536"},
     "edge_buckets": {"GS_EDGE_BUCKETS": "1", "GS_EDGE_BSHIFT": "12"},
     "one_build_stream": {"GS_BUILD_STREAMS": "1"},
     "fused_build_off": {"GS_FUSED_BUILD": "0"},
