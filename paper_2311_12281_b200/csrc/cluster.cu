@@ -705,7 +705,9 @@ __global__ void k_near_list(const int* __restrict__ nclu, const int32_t* __restr
                             const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
                             const int32_t* __restrict__ lmax, const uint8_t* __restrict__ role,
                             uint8_t* __restrict__ mark, int32_t* __restrict__ near,
-                            int* __restrict__ nnear, uint8_t* __restrict__ fin) {
+                            int* __restrict__ nnear, uint8_t* __restrict__ fin,
+                            const int32_t* __restrict__ lmin, int32_t* __restrict__ hacc,
+                            int64_t n) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t nc = *nclu;
@@ -721,57 +723,26 @@ __global__ void k_near_list(const int* __restrict__ nclu, const int32_t* __restr
       const unsigned bit = 1u << (8 * (w & 3));
       const unsigned old = atomicOr(reinterpret_cast<unsigned*>(mark) + (w >> 2), bit);
       if (!(old & bit)) near[atomicAdd(nnear, 1)] = w;
+      // u's contribution to w's hub test, pushed from the clustered side
+      // (zero-initialised: count, INT_MAX - min label, max label + 1)
+      atomicAdd(&hacc[w], 1);
+      atomicMax(&hacc[n + w], 0x7fffffff - lmin[u]);
+      atomicMax(&hacc[2 * n + w], lmax[u] + 1);
     }
   }
 }
 
-// hub or outlier for each listed candidate (scan.py:779-829), CTA per vertex
-// (a candidate can be a hub of the whole graph: its list is split 256 ways)
-__global__ void __launch_bounds__(256) k_classify_list(const int* __restrict__ nnear,
-                                                       const int32_t* __restrict__ near,
-                                                       const int64_t* __restrict__ off,
-                                                       const int32_t* __restrict__ adj,
-                                                       const int32_t* __restrict__ lmin,
-                                                       const int32_t* __restrict__ lmax,
-                                                       uint8_t* __restrict__ fin) {
-  __shared__ int s_cnt[8];
-  __shared__ int32_t s_min[8], s_max[8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+// hub or outlier for each listed candidate (scan.py:779-829) from what its
+// clustered neighbours pushed (k_near_list): >= 2 of them, >= 2 labels
+__global__ void k_classify_near(const int* __restrict__ nnear, const int32_t* __restrict__ near,
+                                const int32_t* __restrict__ hacc, int64_t n,
+                                uint8_t* __restrict__ fin) {
   const int64_t nn = *nnear;
-  for (int64_t k = blockIdx.x; k < nn; k += gridDim.x) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nn;
+       k += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = near[k];
-    int cnt = 0;
-    int32_t umin = 0x7fffffff, umax = -1;
-    for (int64_t i = off[v] + threadIdx.x; i < off[v + 1]; i += blockDim.x) {
-      const int32_t x = adj[i];
-      const int32_t hx = lmax[x];
-      if (hx < 0) continue;
-      ++cnt;
-      const int32_t lx = lmin[x];
-      umin = lx < umin ? lx : umin;
-      umax = hx > umax ? hx : umax;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      umin = min(umin, __shfl_xor_sync(0xffffffffu, umin, o));
-      umax = max(umax, __shfl_xor_sync(0xffffffffu, umax, o));
-    }
-    if (lane == 0) {
-      s_cnt[wid] = cnt;
-      s_min[wid] = umin;
-      s_max[wid] = umax;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-        cnt += s_cnt[w];
-        umin = min(umin, s_min[w]);
-        umax = max(umax, s_max[w]);
-      }
-      fin[v] = (cnt >= 2 && umin != umax) ? ROLE_HUB : ROLE_OUTLIER;
-    }
-    __syncthreads();
+    const int32_t umin = 0x7fffffff - hacc[n + v], umax = hacc[2 * n + v] - 1;
+    fin[v] = (hacc[v] >= 2 && umin != umax) ? ROLE_HUB : ROLE_OUTLIER;
   }
 }
 
@@ -1060,7 +1031,8 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
     GS_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, str));
     GS_CUDA(cudaStreamSynchronize(str));
     e->launches++;
-    listed = sparse_mode() == 1 || (int64_t)h[0] <= 2 * m / kListDiv;
+    static const int64_t list_div = getenv("GS_LIST_DIV") ? atoll(getenv("GS_LIST_DIV")) : kListDiv;
+    listed = sparse_mode() == 1 || (int64_t)h[0] <= 2 * m / std::max<int64_t>(list_div, 1);
     if (listed) {
       int32_t* nearl = nullptr;
       GS_TRY(e->alloc_n(&nearl, n));
@@ -1069,13 +1041,16 @@ int phase_finish(gs_engine* e, uint8_t* role_out, int32_t* cluster_out, int out_
       GS_CUDA(cudaMemsetAsync(fin, ROLE_OUTLIER, (size_t)n, str));
       const unsigned gw = (unsigned)std::min<int64_t>(grid_for((int64_t)n * 32, 256), (int64_t)e->sms * 16);
       int32_t* ipre = nullptr;
+      int32_t* hacc = nullptr;  // per vertex: clustered-neighbour count, min / max label
+      GS_TRY(e->alloc_n(&hacc, 3 * n));
+      GS_CUDA(cudaMemsetAsync(hacc, 0, sizeof(int32_t) * 3 * (size_t)n, str));
       GS_TRY(list_chunks(e, std::max(hc, 1), cnt, clu, false, &ipre));
       k_near_list<<<gw, 256, 0, str>>>(cnt, clu, ipre, g.off, g.adj, s.lmax, s.role, s.coreadj,
-                                       nearl, cnt + 1, fin);
+                                       nearl, cnt + 1, fin, s.lmin, hacc, n);
       e->release(ipre);
-      k_classify_list<<<(unsigned)e->sms * 8, 256, 0, str>>>(cnt + 1, nearl, g.off, g.adj, s.lmin,
-                                                             s.lmax, fin);
+      k_classify_near<<<gridv(e, n), 256, 0, str>>>(cnt + 1, nearl, hacc, n, fin);
       e->launches += 2;
+      e->release(hacc);
       GS_CUDA(cudaGetLastError());
       GS_CUDA(cudaStreamSynchronize(str));  // the lists are released below
       e->release(nearl);
