@@ -754,9 +754,12 @@ static constexpr int64_t kSparseDiv = 16;
 // searches in its run one by one (eps 0.2 at s24, a core of degree 92 K:
 // cluster 9.2 ms dense, 13.5 sparse; eps 0.15 mu 3, cores <= 31: 13.2 -> 5.1)
 static constexpr int64_t kSparseMaxDeg = 4096;
-// classification from the clustered side iff their arcs are <= 2m / 64 (eps 0.2:
-// 1.5 M arcs, 4.0 -> 2.6 ms; eps 0.15 mu 3 with 1.5 M hub candidates: 5.3 -> 9.0)
-static constexpr int64_t kListDiv = 64;
+// classification from the clustered side iff their arcs are <= 2m / kListDiv:
+// with the hub test pushed from the clustered side (k_near_list) the listed
+// path only walks the clustered vertices' arcs, so it always wins (s24 eps
+// 0.15 mu 3, 1.5 M hub candidates: 5.4 ms dense, 3.2 at 2m/4, 3.0 at 2m;
+// eps 0.2: 2.7 -> 0.39 ms)
+static constexpr int64_t kListDiv = 1;
 
 // inclusive prefix of the 32-arc chunk counts of list[0, cnt) (owned prefix or
 // whole run); the caller releases *ipre once the launch using it is ordered
