@@ -174,3 +174,73 @@ def test_scan_out_of_core_from_the_reference_spill_files(name):
     assert np.array_equal(res.cluster_ids, cids)
     assert "".join(r.name[0] for r in res.roles) == c["roles"]
     assert stats.extra["partitions"] == len(parts)
+
+
+def _plan_closure_py(g, budget, state):
+    """The reference's greedy closure planner restated line for line
+    (partition.py:245-312) as the checker for the native one."""
+    off, adj, eids = g.vertex_offsets, g.adjacency, g.edge_ids
+    pairs = g.edge_list
+    in_v, in_e = [-1] * g.n, [-1] * g.m
+    out, index, owned_lo, cur_v, cur_e, cost = [], 0, 0, 0, 0, 0
+
+    def closure(u, v):
+        nv, ne, sv, se = [], [], set(), set()
+        for x in (u, v):
+            if in_v[x] != index and x not in sv:
+                sv.add(x)
+                nv.append(x)
+            for i in range(off[x], off[x + 1]):
+                w, e = int(adj[i]), int(eids[i])
+                if in_v[w] != index and w not in sv:
+                    sv.add(w)
+                    nv.append(w)
+                if in_e[e] != index and e not in se:
+                    se.add(e)
+                    ne.append(e)
+        return nv, ne
+
+    for k in range(g.m):
+        u, v = int(pairs[2 * k]), int(pairs[2 * k + 1])
+        nv, ne = closure(u, v)
+        add = 25 * len(ne) + 4 * len(nv)
+        if cur_e and cost + add + state > budget:
+            out.append((owned_lo, k, cur_v, cur_e))
+            index, owned_lo, cur_v, cur_e, cost = index + 1, k, 0, 0, 0
+            nv, ne = closure(u, v)
+            add = 25 * len(ne) + 4 * len(nv)
+        if cost + add + state > budget:
+            return ("infeasible", (u, v), cost + add + state)
+        for x in nv:
+            in_v[x] = index
+        for e in ne:
+            in_e[e] = index
+        cur_v, cur_e, cost = cur_v + len(nv), cur_e + len(ne), cost + add
+    if cur_e:
+        out.append((owned_lo, g.m, cur_v, cur_e))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_closure_planner_matches_a_restatement_on_random_graphs(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(5, 120))
+    hot = max(1, n // 10)
+    e = set()
+    for _ in range(int(rng.integers(n, 5 * n))):
+        u = int(rng.integers(0, hot)) if rng.random() < 0.4 else int(rng.integers(0, n))
+        v = int(rng.integers(0, n))
+        if u != v:
+            e.add((min(u, v), max(u, v)))
+    if not e:
+        return
+    g = make_graph(n, sorted(e))
+    est = 25 * g.m + 4 * g.n
+    for budget in (15 * n + est // int(rng.integers(2, 12)), 15 * n + 400, 15 * n + est + 1):
+        want = _plan_closure_py(g, budget, 15 * n)
+        if isinstance(want, tuple):
+            with pytest.raises(gs.InfeasibleBudgetError) as ei:
+                P._plan_closure(g, budget, 15 * n)
+            assert ei.value.edge == want[1] and ei.value.required_bytes == want[2]
+        else:
+            assert P._plan_closure(g, budget, 15 * n) == want
