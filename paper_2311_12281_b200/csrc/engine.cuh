@@ -158,11 +158,6 @@ struct SimParams {
   // [p1_rng[0], p1_rng[1]) of it: the stage-2 launches visit only those
   const int32_t* p1_list = nullptr;
   const int* p1_rng = nullptr;
-  // survivor scans (scan_survivor): at least scan_minu loads per lane per step,
-  // and with scan_spec the next step prefetched even when this one may decide
-  // (over-reads the run's tail to take round trips off low-eps scans)
-  int scan_minu = 1;
-  int scan_spec = 0;
   int shard_rank;       // this process owns the edges whose high endpoint
   int shard_world;      //   b satisfies b % shard_world == shard_rank
   Eps2 eps;

@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT > 2 ? 2048 / NT / 2 : 1) k_sim_h
           }
           const bool res = !skd && scan_survivor<GTAB>(P.adj + surv_oa[s], ad.y, jc.y, bm, hub_lo,
                                                        rmax, C, nstash, nb, nlo, lane, scanned,
-                                                       first, P.scan_minu, P.scan_spec);
+                                                       first);
           if (lane == 0) {
             ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
             ctr_add(lc, skd ? LC_SKETCH : LC_INTERS, 1);
@@ -822,8 +822,7 @@ __global__ void __launch_bounds__(NT, MINB) k_sim_warp(SimParams P, int64_t rlo,
                                sda, scm, lane);
         }
         const bool res = !skd && scan_survivor<false>(P.adj + soa, sda, scm, nullptr, 0xffffffffu,
-                                                      0, C, nstash, nb, db, lane, scanned, first,
-                                                      P.scan_minu, P.scan_spec);
+                                                      0, C, nstash, nb, db, lane, scanned, first);
         if (res) ++bsim; else ++bdis;
         if (lane == 0) {
           ctr_add(lc, LC_PROBES, (unsigned long long)scanned);
@@ -1207,10 +1206,6 @@ int run_similarity(gs_engine* e, int mode, const Eps2& eps, int32_t mu) {
   if (const char* v = getenv("GS_SKETCH_TMAX")) P.sk_tmax = atoi(v);
   P.shard_rank = e->shard_rank;
   P.shard_world = e->shard_world;
-  static const int scan_minu = getenv("GS_SCAN_MINU") ? std::max(1, std::min(4, atoi(getenv("GS_SCAN_MINU")))) : 1;
-  static const int scan_spec = getenv("GS_SCAN_SPEC") ? atoi(getenv("GS_SCAN_SPEC")) : 0;
-  P.scan_minu = scan_minu;
-  P.scan_spec = scan_spec;
   const bool ident = mode == MODE_IDENTIFY;
   auto slot = [&](int c) { P.bslot = ident ? c : CTR_B_OTHER; };
   if (ident) e->kev_mark(2);

@@ -369,8 +369,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
                                               int32_t cmin, const uint32_t* bm, uint32_t hub_lo,
                                               uint32_t rmax, const Cuckoo& C, int nstash,
                                               const int32_t* __restrict__ nb, int64_t nlo,
-                                              int lane, int32_t& scanned, uint32_t first,
-                                              int minu = 1, bool spec = false) {
+                                              int lane, int32_t& scanned, uint32_t first) {
   // Element j (0 = the top of N(a)) is a_run[da - 1 - j]; in a step based at
   // element s, lane l reads j = s + 32u + l for u < cu: one base pointer per
   // step, the four loads use immediate offsets.
@@ -384,7 +383,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
 #pragma unroll
   for (int u = 0; u < 4; ++u) cur[u] = nxt[u] = kPast;
   cur[0] = first;
-  int32_t cu = min(4, max(minu, (min(need_miss, cmin) + 31) >> 5));
+  int32_t cu = min(4, max(1, (min(need_miss, cmin) + 31) >> 5));
   {
     const int32_t rem = da - lane;
 #pragma unroll
@@ -397,10 +396,10 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
     const int32_t wstep = min(32 * cu, da - scanned);
     const int32_t nbase = scanned + wstep;
     const int32_t rest = min(need_miss - (scanned - c), cmin - c) - wstep;  // still certain
-    const bool pre = (rest > 0 || spec) && nbase < da;
+    const bool pre = rest > 0 && nbase < da;
     int32_t nu = 0;
     if (pre) {
-      nu = min(4, max(minu, (rest + 31) >> 5));
+      nu = min(4, (rest + 31) >> 5);
       const int32_t* __restrict__ q = top - nbase;
       const int32_t rem = da - nbase - lane;
 #pragma unroll
@@ -429,7 +428,7 @@ __device__ __forceinline__ bool scan_survivor(const int32_t* __restrict__ a_run,
       for (int u = 0; u < 4; ++u) cur[u] = nxt[u];
       cu = nu;
     } else {
-      cu = min(4, max(minu, (min(need_miss - (scanned - c), cmin - c) + 31) >> 5));
+      cu = min(4, max(1, (min(need_miss - (scanned - c), cmin - c) + 31) >> 5));
       const int32_t* __restrict__ q = top - scanned;
       const int32_t rem = da - scanned - lane;
 #pragma unroll
