@@ -244,3 +244,27 @@ def test_closure_planner_matches_a_restatement_on_random_graphs(seed):
             assert ei.value.edge == want[1] and ei.value.required_bytes == want[2]
         else:
             assert P._plan_closure(g, budget, 15 * n) == want
+
+
+@pytest.mark.gpu
+def test_spill_interop_with_the_reference_package():
+    """Both directions with the reference's own code (baseline/_ref, shipped with
+    the snapshot; skipped without it): the reference's spill plan executed by
+    this engine, and this package's spill plan executed by the reference's
+    scan_out_of_core (tools/spill_interop.py)."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    ref_src = os.path.join(ROOT, "baseline", "_ref", "pkg", "src")
+    if not os.path.isdir(ref_src):
+        pytest.skip("baseline/_ref/pkg (the reference package) not shipped")
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([ref_src, ROOT,
+                                                       os.environ.get("PYTHONPATH", "")]))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "spill_interop.py")],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    rep = json.loads(r.stdout.strip().splitlines()[-1])
+    assert rep["ok"] and all(c["reference_plan_on_engine"]["partitions"] >= 3
+                             for c in rep["cases"]), rep
