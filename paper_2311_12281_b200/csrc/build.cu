@@ -1722,21 +1722,47 @@ static int fused_scatter_sort(gs_engine* e, int64_t n, int64_t m, const int64_t*
   // beat 7 of 4 -- 12.07 -> 11.57 ms -- and 5 of 6)
   static const int rb = getenv("GS_SORT_RB") ? atoi(getenv("GS_SORT_RB")) : 5;
   static const int rbd = getenv("GS_SORT_RBD") ? atoi(getenv("GS_SORT_RBD")) : 5;
+  // CTA shape of the two mid classes: fewer threads holding more keys each
+  // (measured at s24, build ms: 256 x 8 / 256 x 16 keys 8.95, 512 x 4 / 512 x 8
+  // 10.5, 128 x 16 / 128 x 32 8.60, 64 x 32 / 128 x 32 8.49, 64 x 32 / 64 x 64
+  // 8.42; GS_FB_SHAPE 0 / 1 / 2 / 5 / 6, default 5)
+  static const int fbs = getenv("GS_FB_SHAPE") ? atoi(getenv("GS_FB_SHAPE")) : 5;
   auto kb8 = rb == 4 ? k_fused_block<256, 8, 4> : k_fused_block<256, 8, 5>;
   auto kb16 = rb == 4 ? k_fused_block<256, 16, 4> : k_fused_block<256, 16, 5>;
+  int nt8 = 256, nt16 = 256;
+  if (fbs == 1) { kb8 = k_fused_block<512, 4, 5>; kb16 = k_fused_block<512, 8, 5>; nt8 = nt16 = 512; }
+  if (fbs == 2) { kb8 = k_fused_block<128, 16, 5>; kb16 = k_fused_block<128, 32, 5>; nt8 = nt16 = 128; }
+  if (fbs == 3) { kb8 = k_fused_block<128, 16, 5>; nt8 = 128; }
+  if (fbs == 4) { kb16 = k_fused_block<128, 32, 5>; nt16 = 128; }
+  if (fbs == 5) { kb8 = k_fused_block<64, 32, 5>; kb16 = k_fused_block<128, 32, 5>; nt8 = 64; nt16 = 128; }
+  if (fbs == 6) { kb8 = k_fused_block<64, 32, 5>; kb16 = k_fused_block<64, 64, 5>; nt8 = nt16 = 64; }
   if (h2049 > h1025)
-    kb8<<<blocks(h2049 - h1025), 256, 0, st>>>(
+    kb8<<<blocks(h2049 - h1025), nt8, 0, st>>>(
         off, n, h1025, h2049, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
   if (h4096 > h2049)
-    kb16<<<blocks(h4096 - h2049), 256, 0, st>>>(
+    kb16<<<blocks(h4096 - h2049), nt16, 0, st>>>(
         off, n, h2049, h4096, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
   if (h16k > h4096) {
+    // 4096-16384: 512 threads x 32 keys (GS_FBD_SHAPE=1, default; with the mid
+    // classes at 64 x 32 / 128 x 32 the build is 8.31 ms against 8.49 with
+    // 1024 x 16 (0) and 8.36 with 256 x 64 (2))
+    static const int fbd = getenv("GS_FBD_SHAPE") ? atoi(getenv("GS_FBD_SHAPE")) : 1;
     auto kb = rbd == 5 ? k_fused_block_dyn<1024, 16, 5> : k_fused_block_dyn<1024, 16, 4>;
-    const int sm = (int)std::max({sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 4>::TempStorage),
-                                  sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 5>::TempStorage)});
+    int ntd = 1024;
+    int sm = (int)std::max({sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 4>::TempStorage),
+                            sizeof(typename cub::BlockRadixSort<uint32_t, 1024, 16, cub::NullType, 5>::TempStorage)});
+    if (fbd == 1) {
+      kb = k_fused_block_dyn<512, 32, 5>;
+      ntd = 512;
+      sm = (int)sizeof(typename cub::BlockRadixSort<uint32_t, 512, 32, cub::NullType, 5>::TempStorage);
+    } else if (fbd == 2) {
+      kb = k_fused_block_dyn<256, 64, 5>;
+      ntd = 256;
+      sm = (int)sizeof(typename cub::BlockRadixSort<uint32_t, 256, 64, cub::NullType, 5>::TempStorage);
+    }
     GS_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    kb<<<(unsigned)std::min<int64_t>(h16k - h4096, (int64_t)e->sms), 1024, sm, st>>>(
-        off, n, h4096, h16k, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
+    kb<<<(unsigned)std::min<int64_t>(h16k - h4096, (int64_t)e->sms * (1024 / ntd)), ntd, sm,
+         st>>>(off, n, h4096, h16k, g.orig, adj, g.rank, g.off, endbit, arcs, d_bad);
   }
   e->launches += 4;
   GS_CUDA(cudaGetLastError());

@@ -31,6 +31,8 @@ VARIANTS = {
     "hub_runs_at_end": {"GS_HUB_CHUNK": "0", "GS_H2D_CHUNK": "65536"},
     "sketch_streamed_small_chunks": {"GS_SK_STREAM": "1", "GS_H2D_CHUNK": "65536"},
     "small_chunks": {"GS_H2D_CHUNK": "65536"},
+    "fused_block_shapes_round2": {"GS_FB_SHAPE": "0", "GS_FBD_SHAPE": "0"},
+    "fused_block_shapes_alt": {"GS_FB_SHAPE": "6", "GS_FBD_SHAPE": "2"},
     "edge_buckets": {"GS_EDGE_BUCKETS": "1", "GS_EDGE_BSHIFT": "12"},
     "one_build_stream": {"GS_BUILD_STREAMS": "1"},
     "fused_build_off": {"GS_FUSED_BUILD": "0"},
