@@ -41,8 +41,32 @@ __global__ void k_sk_sizes(int64_t dmax, int64_t dmin, int lk, const int32_t* __
     sizes[d] = (d >= dmin && d <= dmax) ? (int64_t)(rdeg[d + 1] - rdeg[d]) * 2 * sk_words(d, lk) : 0;
 }
 
+// hash a run's neighbours into the bitmap t (threads i0, i0 + step, ...): with
+// UNR 4, four loads in flight per thread before their atomics
+template <int UNR>
+__device__ __forceinline__ void sk_hash_run(const int32_t* __restrict__ a, int64_t d, int i0,
+                                            int step, uint32_t mask, uint32_t* t) {
+  int64_t i = i0;
+  if (UNR > 1) {
+    for (; i + (UNR - 1) * step < d; i += UNR * step) {
+      uint32_t x[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) x[u] = (uint32_t)__ldg(a + i + u * step);
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint32_t h = sk_hash(x[u]) & mask;
+        atomicOr(&t[h >> 5], 1u << (h & 31));
+      }
+    }
+  }
+  for (; i < d; i += step) {
+    const uint32_t h = sk_hash((uint32_t)__ldg(a + i)) & mask;
+    atomicOr(&t[h >> 5], 1u << (h & 31));
+  }
+}
+
 // warp per vertex, sketch of <= WMAX words built in shared memory
-template <int NT, int WMAX>
+template <int NT, int WMAX, int UNR = 1>
 __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
                                                 const int32_t* __restrict__ adj, int64_t r0,
                                                 int64_t r1, const int32_t* __restrict__ rdeg,
@@ -67,10 +91,7 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
       uint32_t* t = s + hf * WMAX;
       for (int64_t j = hl; j < W; j += 16) t[j] = 0u;
       __syncwarp();
-      for (int64_t i = hl; i < d; i += 16) {
-        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-        atomicOr(&t[h >> 5], 1u << (h & 31));
-      }
+      sk_hash_run<UNR>(adj + o, d, hl, 16, mask, t);
       __syncwarp();
       sk_fold_levels(t, W, hl, 16);
       uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
@@ -84,10 +105,7 @@ __global__ void __launch_bounds__(NT) k_sk_warp(const int64_t* __restrict__ off,
       const uint32_t mask = (uint32_t)(W * 32 - 1);
       for (int64_t j = lane; j < W; j += 32) s[j] = 0u;
       __syncwarp();
-      for (int64_t i = lane; i < d; i += 32) {
-        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-        atomicOr(&s[h >> 5], 1u << (h & 31));
-      }
+      sk_hash_run<UNR>(adj + o, d, lane, 32, mask, s);
       __syncwarp();
       sk_fold_levels(s, W, lane, 32);
       uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
@@ -112,10 +130,7 @@ __device__ __forceinline__ void sk_cta_row(const int64_t* __restrict__ off,
   uint32_t* t = in_smem ? s : out;
   for (int64_t j = threadIdx.x; j < W; j += blockDim.x) t[j] = 0u;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-    const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-    atomicOr(&t[h >> 5], 1u << (h & 31));
-  }
+  sk_hash_run<4>(adj + o, d, threadIdx.x, blockDim.x, mask, t);
   __syncthreads();
   if (in_smem) {
     sk_fold_levels(s, W, threadIdx.x, blockDim.x, [] { __syncthreads(); });
@@ -174,10 +189,7 @@ __global__ void __launch_bounds__(NT) k_sk_list(const int64_t* __restrict__ off,
       const uint32_t mask = (uint32_t)(W * 32 - 1);
       for (int64_t k = lane; k < W; k += 32) s[k] = 0u;
       __syncwarp();
-      for (int64_t i = lane; i < d; i += 32) {
-        const uint32_t h = sk_hash((uint32_t)__ldg(adj + o + i)) & mask;
-        atomicOr(&s[h >> 5], 1u << (h & 31));
-      }
+      sk_hash_run<4>(adj + o, d, lane, 32, mask, s);
       __syncwarp();
       sk_fold_levels(s, W, lane, 32);
       uint32_t* out = sk + skbase[d] + (v - rdeg[d]) * 2 * W;
@@ -248,6 +260,9 @@ int build_sketch(gs_engine* e, int lk, int64_t dmin) {
   // words (8 KB CTA), larger (one big CTA per vertex)
   // rows of <= 256 words by a warp (measured: 128 / 256 / 512 words -> prep 2.33 / 2.21 / 2.64 ms)
   static const int wmax = getenv("GS_SK_WMAX") ? atoi(getenv("GS_SK_WMAX")) : 256;
+  // four neighbour loads in flight per lane before their shared atomics
+  // (measured: prep 2.22 -> 2.00 ms at s24 eps 0.5, step 21.11 -> 20.89; GS_SK_UNROLL=1: one)
+  static const int sk_unr = getenv("GS_SK_UNROLL") ? atoi(getenv("GS_SK_UNROLL")) : 4;
   const int64_t dsplit = (int64_t)wmax * 32 >> lk, dsplit2 = 2048 * 32 >> lk;
   GS_CUDA(cudaMemcpyAsync(&total, g.skbase + g.dmax + 1, sizeof(total), cudaMemcpyDeviceToHost, st));
   GS_CUDA(cudaMemcpyAsync(&r[0], s.rdeg + dmin, 4, cudaMemcpyDeviceToHost, st));
@@ -271,6 +286,9 @@ int build_sketch(gs_engine* e, int lk, int64_t dmin) {
     if (wmax >= 512)
       k_sk_warp<NT, 512><<<(unsigned)grid, NT, 0, st>>>(g.off, g.adj, r0, r1, s.rdeg, g.skbase, lk,
                                                         g.sk);
+    else if (wmax >= 256 && sk_unr == 4)
+      k_sk_warp<NT, 256, 4><<<(unsigned)grid, NT, 0, st>>>(g.off, g.adj, r0, r1, s.rdeg, g.skbase,
+                                                           lk, g.sk);
     else if (wmax >= 256)
       k_sk_warp<NT, 256><<<(unsigned)grid, NT, 0, st>>>(g.off, g.adj, r0, r1, s.rdeg, g.skbase, lk,
                                                         g.sk);
